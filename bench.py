@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""ChebyPower bench: GTEPS and queries/s on seeded synthetic graphs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+
+A "step" is one pass of the hot path over one batch of queries: every source
+of the config (16 or 64) runs its K Chebyshev iterations.  The default workload
+is config 3 (LiveJournal-size Chung-Lu, single-source SpMV path, 1 GPU).
+
+value  = GTEPS = K * nnz * sources / t   (the reference's push_work / wall_seconds,
+         solvers.cpp:214,223), device-resident inputs, CUDA events, max over ranks.
+e2e    = same metric through the C-ABI call with HOST buffers: sources and
+         coefficients H2D, every result vector D2H into pinned memory, inside the
+         timed region.
+roofline: dominant kernel cheby_step_kernel (or cheby_batch_kernel); achieved =
+         algorithmic bytes per launch (12*nnz + 8*(n+1) + 32*n) /
+         mean CUDA-event launch duration measured here.
+cpu_baseline: the reference's own cheby_power (oracle/_ref, compiled from
+         /root/reference sources) on the host cores, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PPR, HKPR = 0, 1
+
+# Synthetic stand-ins for the paper's datasets (BASELINE.json configs).
+CONFIGS = {
+    1: dict(name="rmat-s16-ef8 ppr", gen="rmat", scale=16, samples=8 << 16, seed=1,
+            family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
+    2: dict(name="chunglu-dblp-size hkpr", gen="chunglu", n_ids=317_080, samples=1_052_000, exponent=2.5,
+            mean=6.6, cap=0, seed=2, family=HKPR, param=5.0, eps=1e-8, sources=64, mode="single"),
+    3: dict(name="chunglu-livejournal-size ppr", gen="chunglu", n_ids=4_846_609, samples=44_200_000,
+            exponent=2.3, mean=17.8, cap=20_000, seed=3, family=PPR, param=0.2, eps=1e-8, sources=64,
+            mode="single"),
+    4: dict(name="chunglu-orkut-size hkpr batched", gen="chunglu", n_ids=3_072_626, samples=121_000_000,
+            exponent=2.1, mean=76.0, cap=33_000, seed=4, family=HKPR, param=5.0, eps=1e-8, sources=64,
+            mode="batched"),
+    5: dict(name="rmat-friendster-size ppr", gen="rmat", scale=26, samples=2_280_000_000, seed=5,
+            family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
+}
+DEFAULT_CONFIG = 3
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_host_graph(cfg):
+    import paper_2412_10789_b200 as P
+
+    if cfg["gen"] == "rmat":
+        return P.gen_rmat(cfg["scale"], cfg["samples"], seed=cfg["seed"])
+    return P.gen_chunglu(cfg["n_ids"], cfg["samples"], cfg["exponent"], cfg["mean"], cfg["cap"], seed=cfg["seed"])
+
+
+def make_device_csr(cfg, device):
+    import paper_2412_10789_b200 as P
+
+    if cfg["gen"] == "rmat":
+        return P.gen_rmat(cfg["scale"], cfg["samples"], seed=cfg["seed"], device=device)
+    return P.gen_chunglu(cfg["n_ids"], cfg["samples"], cfg["exponent"], cfg["mean"], cfg["cap"],
+                         seed=cfg["seed"], device=device)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:6]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(cfg, off, nb, sources, K, budget_s=20.0, threads=None):
+    """Reference cheby_power (oracle/_ref) on host cores, bounded sample.
+
+    The checker library is used only here, as the timed CPU baseline."""
+    import oracle
+
+    threads = threads or os.cpu_count() or 1
+    coeffs = oracle.Port.cheby_coeffs(cfg["family"], cfg["param"], K)
+    nnz = len(nb)
+    kind = "reference" if oracle.Ref.available() else "port"
+    # size the sample: one query per thread per round, rounds until ~budget
+    t0 = time.perf_counter()
+    if kind == "reference":
+        g = oracle.RefGraph.from_csr(off, nb)
+    setup = time.perf_counter() - t0
+    done, wall = 0, 0.0
+    sample = []
+    while wall < budget_s and done < len(sources) * 4:
+        batch = [int(sources[(done + i) % len(sources)]) for i in range(threads)]
+        t = time.perf_counter()
+        if kind == "reference":
+            g.cheby_power_pool(cfg["family"], cfg["param"], batch, K, threads, keep=False)
+        else:
+            oracle.Port.cheby_power_pool(off, nb, coeffs, K, batch, threads, keep=False)
+        wall += time.perf_counter() - t
+        done += len(batch)
+        sample.append(len(batch))
+        if wall > budget_s / 2 and len(sample) >= 1:
+            break
+    gteps = K * nnz * done / wall / 1e9
+    return {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
+            "queries_per_s": done / wall,
+            "sample": f"{done} queries x K={K} on {threads} threads ({wall:.1f}s; graph setup {setup:.1f}s excluded)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's CPU cheby_power on all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import paper_2412_10789_b200 as P
+
+    off, nb = make_host_graph(cfg)
+    n = len(off) - 1
+    kernel = P.Kernel.ppr(cfg["param"]) if cfg["family"] == PPR else P.Kernel.hkpr(cfg["param"])
+    K = P.plan_truncation(kernel, cfg["eps"]).cheby_steps
+    sources = P.select_sources_uniform(n, cfg["sources"], 1)
+    threads = os.cpu_count() or 1
+    kind = "reference" if oracle.Ref.available() else "port"
+    coeffs = oracle.Port.cheby_coeffs(cfg["family"], cfg["param"], K)
+    g = oracle.RefGraph.from_csr(off, nb) if kind == "reference" else None
+    per_step = max(1, min(len(sources), threads))  # bounded sample: one query per thread per step
+
+    def one_step(i):
+        batch = [int(sources[(i * per_step + j) % len(sources)]) for j in range(per_step)]
+        if g is not None:
+            g.cheby_power_pool(cfg["family"], cfg["param"], batch, K, threads, keep=False)
+        else:
+            oracle.Port.cheby_power_pool(off, nb, coeffs, K, batch, threads, keep=False)
+
+    for i in range(args.warmup):
+        one_step(i)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        one_step(args.warmup + i)
+    wall = time.perf_counter() - t
+    gteps = K * len(nb) * per_step * args.steps / wall / 1e9
+    line = {"metric": METRIC, "value": gteps, "unit": "GTEPS", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "queries_per_s": per_step * args.steps / wall,
+            "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": len(nb), "K": K,
+                       "sources_per_step": per_step},
+            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
+                             "sample": f"{per_step} queries per step x {args.steps} steps", "cpu_model": _cpu_model()},
+            "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "ChebyPower GTEPS (K*nnz*sources/s) on the config graph; queries/s and % HBM roofline alongside"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    run_ours(args, cfg)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2412_10789_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    kernel = P.Kernel.ppr(cfg["param"]) if cfg["family"] == PPR else P.Kernel.hkpr(cfg["param"])
+    K = P.plan_truncation(kernel, cfg["eps"]).cheby_steps
+    coeffs = kernel.cheby_coeffs(K)
+
+    t0 = time.perf_counter()
+    csr = make_device_csr(cfg, dev)
+    n, nnz = csr.n, csr.nnz
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if world == 1:
+        dg = P.DeviceGraph.from_device(csr)
+    else:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
+        pg.broadcast(uid, 0)
+        dg = P.DeviceGraph.sharded(csr.offsets_ptr, csr.neighbors_ptr, n, nnz, True, dev, rank, world,
+                                   bytes(uid.cpu().numpy()))
+    torch.cuda.synchronize()
+    t_up = time.perf_counter() - t0
+    log(f"[bench] cfg{args.config} n={n} nnz={nnz} K={K} gen {t_gen:.1f}s upload {t_up:.1f}s "
+        f"hubs={dg.info.n_hubs} items={dg.info.n_items} maxdeg={dg.info.max_degree}")
+
+    sources = P.select_sources_uniform(n, cfg["sources"], 1)
+    batched = cfg["mode"] == "batched"
+    tile = 64
+    L = P._lib.lib()
+    import ctypes
+
+    src_np = np.ascontiguousarray(sources, dtype=np.uint32)
+    c_np = np.ascontiguousarray(coeffs)
+    d_out = torch.empty((len(sources), n), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    stats = P._lib.cpg_stats()
+
+    def step_device():
+        if batched:
+            rc = L.cpg_chebypower_batched_device(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), tile,
+                                                 ctypes.c_void_p(d_out.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
+                                                 None)
+        else:
+            rc = L.cpg_chebypower_device(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np),
+                                         ctypes.c_void_p(d_out.data_ptr()), ctypes.c_void_p(stream.cuda_stream), None)
+        P._check(rc, "step")
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if pg is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: device-resident, K steps timed with CUDA events -------------------------
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms / args.steps
+    queries = len(sources) * args.steps
+    gteps = K * nnz * queries / (ms / 1e3) / 1e9
+    launches_per_step = (len(sources) * (K + 4) if not batched else ((len(sources) + tile - 1) // tile) * (K + 2))
+
+    # ---- roofline: per-launch step-kernel time (events bracket each launch) ----------------
+    L.cpg_set_profiling(1)
+    s = P._lib.cpg_stats()
+    if batched:
+        P._check(L.cpg_chebypower_batched(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), tile, None,
+                                          ctypes.byref(s)))
+    else:
+        P._check(L.cpg_chebypower(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), None, ctypes.byref(s)))
+    L.cpg_set_profiling(0)
+    bytes_launch = dg.bytes_per_step(tile if batched else 1)
+    per_launch_ms = max_over_ranks(s.step_ms / max(1, s.step_launches))
+    achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+    step_share = s.step_ms / max(1e-9, s.device_ms)
+
+    # ---- e2e: host buffers through the C-ABI call -------------------------------------------
+    pinned = torch.empty((len(sources), n), dtype=torch.float64, pin_memory=True)
+    out_np = pinned.numpy()
+
+    def step_host():
+        st = P._lib.cpg_stats()
+        if batched:
+            P._check(L.cpg_chebypower_batched(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), tile,
+                                              out_np.ctypes.data, ctypes.byref(st)))
+        else:
+            P._check(L.cpg_chebypower(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), out_np.ctypes.data,
+                                      ctypes.byref(st)))
+        return st
+
+    step_host()
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        st = step_host()  # synchronous: returns after the last D2H lands in pinned memory
+    wall_e2e = time.perf_counter() - t
+    e3.record(stream)
+    barrier()
+    wall_e2e = max_over_ranks(wall_e2e)
+    e2e_gteps = K * nnz * queries / wall_e2e / 1e9
+    mass_err = st.mass_err_max
+
+    # ---- parity spot check of the timed outputs against the device-resident run -----
+    same = bool(np.array_equal(out_np[0], d_out[0].cpu().numpy()))
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        off, nb = csr.to_host()
+        cpu = cpu_baseline(cfg, off, nb, sources, K, budget_s=args.cpu_budget)
+    csr.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator; stand-in for the paper's SNAP dataset)",
+            "queries_per_s": queries / (ms / 1e3),
+            "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": nnz, "K": K,
+                       "sources_per_step": len(sources), "mode": cfg["mode"],
+                       "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "kernel": "cheby_batch_kernel" if batched else "cheby_step_kernel",
+                         "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms,
+                         "step_share_of_device_time": step_share},
+            "e2e": {"value": e2e_gteps, "unit": "GTEPS",
+                    "h2d_bytes_per_step": int(src_np.nbytes + c_np.nbytes),
+                    "d2h_bytes_per_step": int(len(sources) * n * 8), "queries_per_s": queries / wall_e2e},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clk.summary(),
+            "mass_err_max": mass_err,
+            "e2e_matches_device_run": same,
+            "setup_s": {"generate": t_gen, "upload_relabel": t_up},
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    dg.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

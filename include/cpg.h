@@ -1,0 +1,191 @@
+/*
+ * cpg.h -- C ABI of the B200-native ChebyPower library (libcpg.so).
+ *
+ * This is the drop-in boundary for the reference's ChebyPower path
+ * (reference paths relative to /root/reference/proj):
+ *
+ *   Estimate cheby_power(const Graph&, const Kernel&, NodeId source,
+ *                        std::size_t cheby_steps, const StepObserver& = {})
+ *                                               include/chebyprop/solvers.hpp:59-61
+ *   Estimate cheby_power_vec(const Graph&, const Kernel&, const NodeVector& seed,
+ *                            std::size_t cheby_steps, ...)   solvers.hpp:62-64
+ *   std::vector<double> ppr_cheby_coeffs / hkpr_cheby_coeffs   kernels.hpp:69-74
+ *   TruncationPlan plan_truncation(const Kernel&, double)      kernels.hpp:81
+ *   Graph::from_csr validation                                  graph.hpp:51-53
+ *   general_gp_matrix (batched columns)                         solvers.hpp:107-111
+ *
+ * Plain pointers and sizes only; no C++ or torch types.  Every entry returns
+ * a status code; cpg_last_error() gives the calling thread's message for the
+ * last failure.  Status mapping to the reference's exceptions (error.hpp):
+ *   CPG_EINVAL  -> ParameterError   (bad source, K < 1, bad alpha/t/eps, length)
+ *   CPG_ESTRUCT -> StructuralError  (invalid CSR)
+ *   CPG_ECUDA / CPG_ENOMEM / CPG_ENCCL -> runtime failures (no CPU fallback).
+ *
+ * Node ids, offsets and the CSR layout are the reference's own
+ * (Graph::offsets() uint64[n+1], Graph::neighbor_array() uint32[2m],
+ * graph.hpp:40-41), so a reference Graph can be handed over without copies.
+ */
+#ifndef CPG_H
+#define CPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    CPG_OK = 0,
+    CPG_EINVAL = 1,
+    CPG_ECUDA = 2,
+    CPG_ENCCL = 3,
+    CPG_ENOMEM = 4,
+    CPG_ESTRUCT = 5
+};
+
+enum { CPG_PPR = 0, CPG_HKPR = 1 };
+
+typedef struct cpg_graph cpg_graph;
+
+/* SolveStats (solvers.hpp:18-25) plus device-side evidence. */
+typedef struct {
+    uint32_t iterations;   /* K per query (solvers.cpp:228)                  */
+    uint64_t push_work;    /* K * vol summed over queries (solvers.cpp:214)  */
+    double wall_seconds;   /* host wall time of the call                     */
+    double device_ms;      /* CUDA-event time of the K steps (all queries)   */
+    double mass_err_max;   /* max_k |sum T_k - sum seed| over queries/steps  */
+    double bytes_model;    /* algorithmic HBM bytes           */
+    uint32_t launches;     /* kernels launched by this call                  */
+    double step_ms;        /* summed CUDA-event time of the step kernels only
+                              (filled when cpg_set_profiling(1); else 0)     */
+    uint32_t step_launches;/* step-kernel launches behind step_ms            */
+} cpg_stats;
+
+/* TruncationPlan (kernels.hpp:48-53). */
+typedef struct {
+    uint64_t cheby_steps;
+    uint64_t taylor_steps;
+    double epsilon;
+    double tail_bound;
+} cpg_plan;
+
+/* Graph description produced at upload (read-only). */
+typedef struct {
+    uint32_t n;            /* nodes of the whole graph                       */
+    uint64_t nnz;          /* 2m of the whole graph                          */
+    uint32_t n_local;      /* rows owned by this handle (shard)              */
+    uint64_t nnz_local;
+    uint32_t row_begin;    /* first owned row in the device (relabelled) order */
+    uint32_t n_padded;     /* length of the replicated iterate (ranks*rows)  */
+    uint32_t n_hubs;       /* rows split across CTAs                         */
+    uint32_t n_items;      /* work items per single-source step              */
+    uint32_t max_degree;
+    int rank, nranks, device;
+    uint64_t structure_hash; /* FNV-1a of (n, m, offsets, neighbors), graph.cpp:97-102 */
+} cpg_graph_info;
+
+const char* cpg_last_error(void);
+const char* cpg_version(void);
+/* Bracket every step-kernel launch with CUDA events (cpg_stats.step_ms). */
+void cpg_set_profiling(int on);
+
+/* ---- host-side math (kernels.cpp restated in C++) ------------------------ */
+int cpg_ppr_cheby_coeffs(double alpha, uint64_t max_index, double* out);   /* kernels.cpp:157-170 */
+int cpg_hkpr_cheby_coeffs(double t, uint64_t max_index, double* out);      /* kernels.cpp:172-194 */
+int cpg_cheby_coeffs(int family, double param, uint64_t max_index, double* out);
+int cpg_plan_truncation(int family, double param, double epsilon, cpg_plan* out); /* :253-341 */
+/* "ppr:alpha=0.2" / "hkpr:t=5" (kernels.cpp:343-362) */
+int cpg_parse_kernel_spec(const char* spec, int* family, double* param);
+
+/* Graph::from_csr invariants (graph.cpp:48-104) + FNV-1a structure hash. */
+int cpg_validate_csr(const uint64_t* offsets, const uint32_t* neighbors, uint64_t n,
+                     uint64_t nnz, uint64_t* structure_hash);
+
+/* ---- graph upload --------------------------------------------------------
+ * Copies the CSR to `device`, relabels rows by descending degree (results are
+ * reported in the caller's ids), and builds the load-balanced work tables.
+ * The host arrays are only borrowed for the call.  validate != 0 runs the
+ * from_csr checks first (CPG_ESTRUCT on failure). */
+int cpg_graph_create(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n,
+                     uint64_t nnz, int device, int validate, cpg_graph** out);
+
+/* Same, from arrays already resident on `device` (e.g. produced by the device
+ * generator); the arrays stay owned by the caller. */
+int cpg_graph_create_device(const uint64_t* d_offsets, const uint32_t* d_neighbors,
+                            uint32_t n, uint64_t nnz, int device, cpg_graph** out);
+
+/* Row-partitioned shard for multi-GPU: rank `rank` of
+ * `nranks` keeps the rows it owns plus a full-length iterate replica and joins
+ * an NCCL communicator identified by `nccl_unique_id` (128 bytes from
+ * cpg_nccl_unique_id on one rank, broadcast by the caller).  Every rank passes
+ * the whole CSR (host or device pointers per `on_device`). */
+int cpg_nccl_unique_id(void* out128);
+int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n,
+                             uint64_t nnz, int on_device, int device, int rank, int nranks,
+                             const void* nccl_unique_id, cpg_graph** out);
+
+int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info);
+int cpg_graph_destroy(cpg_graph* g);
+
+/* ---- the hot path ----------------------------------------------------------
+ * ChebyPower (solvers.cpp:197-239): for each source s_j,
+ *   out[j*n : (j+1)*n] = sum_{k=0..K} c_k T_k(P) e_{s_j},   P = A D^-1,
+ * with coeffs[0..K] supplied by the caller (cpg_cheby_coeffs).  K fused
+ * SpMV+recurrence steps per query on the device.  `out` is a HOST buffer
+ * (n_sources*n doubles) or NULL to discard; stats may be NULL.
+ * Sharded handles: every rank calls collectively; out is filled on every rank. */
+int cpg_chebypower(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                   uint32_t n_sources, double* out, cpg_stats* stats);
+
+/* Device-resident variant: d_out is a DEVICE buffer (n_sources*n doubles, or
+ * NULL), work is enqueued on `stream` (cudaStream_t, NULL = the handle's own
+ * stream) and the call returns without synchronising. */
+int cpg_chebypower_device(cpg_graph* g, const double* coeffs, uint32_t K,
+                          const uint32_t* sources, uint32_t n_sources, double* d_out,
+                          void* stream, cpg_stats* stats);
+
+/* cheby_power_vec (solvers.cpp:197-234): dense seeds (n_seeds x n, host). */
+int cpg_chebypower_vec(cpg_graph* g, const double* coeffs, uint32_t K, const double* seeds,
+                       uint32_t n_seeds, double* out, cpg_stats* stats);
+
+/* Batched multi-source variant: sources processed in tiles of `tile` (1..64)
+ * columns with one SpMM per step (the general_gp_matrix loop of
+ * solvers.cpp:405-414 with a = 0 fused into one sweep). */
+int cpg_chebypower_batched(cpg_graph* g, const double* coeffs, uint32_t K,
+                           const uint32_t* sources, uint32_t n_sources, uint32_t tile,
+                           double* out, cpg_stats* stats);
+int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K,
+                                  const uint32_t* sources, uint32_t n_sources, uint32_t tile,
+                                  double* d_out, void* stream, cpg_stats* stats);
+
+/* Test/observer slow path: T_k(P)e_s for k = 0..K ((K+1) x n, host) and the
+ * partial estimates after each step ((K+1) x n), the StepObserver arguments of
+ * solvers.cpp:215,219,226.  Either trace pointer may be NULL. */
+int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source,
+                         double* out, double* r_trace, double* est_trace);
+
+/* Single walk y = A D^-1 x (graph.cpp:257-267) for tests; host vectors. */
+int cpg_apply_walk(cpg_graph* g, const double* x, double* y);
+
+/* Algorithmic bytes of one single-source step for this handle. */
+double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile);
+
+/* ---- synthetic inputs (bench/test harness; deterministic, seed-addressed) ----
+ * R-MAT (a,b,c,d) with 2^scale ids and n_samples draws, or Chung-Lu with
+ * power-law weights; both symmetrised, deduplicated, self-loops dropped,
+ * isolated ids compacted (ascending).  Output CSR lands on `device` (pass
+ * device = -1 to build on the host).  Buffers are allocated by the library and
+ * released with cpg_free_csr. */
+int cpg_gen_rmat(uint32_t scale, uint64_t n_samples, double a, double b, double c,
+                 uint64_t seed, int device, uint64_t** offsets, uint32_t** neighbors,
+                 uint32_t* n, uint64_t* nnz);
+int cpg_gen_chunglu(uint32_t n_ids, uint64_t n_samples, double exponent, double mean_degree,
+                    uint32_t max_degree, uint64_t seed, int device, uint64_t** offsets,
+                    uint32_t** neighbors, uint32_t* n, uint64_t* nnz);
+int cpg_free_csr(uint64_t* offsets, uint32_t* neighbors, int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPG_H */

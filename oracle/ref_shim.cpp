@@ -1,0 +1,260 @@
+// oracle/ref_shim.cpp -- extern "C" shim over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources as they lie under /root/reference/proj/src (never copied
+// into this repo) into oracle/_ref/libchebyprop_ref.so.  Used by tests/ to pin
+// the oracle restatement (oracle/cheby_oracle.c), by tests/golden/make_golden.py
+// to produce golden vectors, and by bench.py's cpu_baseline / --impl reference
+// legs to time the reference's own cheby_power on the host cores.
+//
+// Every entry calls the reference's public C++ API (include/chebyprop/*.hpp)
+// and converts its exceptions to status codes:
+//   0 ok, 1 ParameterError, 5 StructuralError/ParseError, 6 other.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "chebyprop/error.hpp"
+#include "chebyprop/eval.hpp"
+#include "chebyprop/graph.hpp"
+#include "chebyprop/kernels.hpp"
+#include "chebyprop/solvers.hpp"
+
+using namespace chebyprop;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ParameterError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const StructuralError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 6;
+    }
+}
+
+Kernel make_kernel(int family, double param) {
+    if (family == 0) return Kernel::ppr(param);
+    if (family == 1) return Kernel::hkpr(param);
+    throw ParameterError("ref_shim: unknown kernel family");
+}
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_ppr_cheby_coeffs(double alpha, uint64_t max_index, double* out) {
+    return guarded([&] {
+        auto c = ppr_cheby_coeffs(alpha, max_index);
+        std::memcpy(out, c.data(), c.size() * sizeof(double));
+    });
+}
+
+int ref_hkpr_cheby_coeffs(double t, uint64_t max_index, double* out) {
+    return guarded([&] {
+        auto c = hkpr_cheby_coeffs(t, max_index);
+        std::memcpy(out, c.data(), c.size() * sizeof(double));
+    });
+}
+
+int ref_taylor_coeffs(int family, double param, uint64_t max_index, double* out) {
+    return guarded([&] {
+        auto z = make_kernel(family, param).taylor_coeffs(max_index);
+        std::memcpy(out, z.data(), z.size() * sizeof(double));
+    });
+}
+
+// out4 = {cheby_steps, taylor_steps} as u64, tail/eps as doubles.
+int ref_plan_truncation(int family, double param, double eps, uint64_t* steps2,
+                        double* tail_eps2) {
+    return guarded([&] {
+        auto p = plan_truncation(make_kernel(family, param), eps);
+        steps2[0] = p.cheby_steps;
+        steps2[1] = p.taylor_steps;
+        tail_eps2[0] = p.tail_bound;
+        tail_eps2[1] = p.epsilon;
+    });
+}
+
+uint64_t ref_ground_truth_steps(int family, double param) {
+    uint64_t s = 0;
+    guarded([&] { s = ground_truth_steps(make_kernel(family, param)); });
+    return s;
+}
+
+// Graph handle = heap-allocated reference Graph built by Graph::from_csr.
+int ref_graph_from_csr(const uint64_t* offsets, const uint32_t* nbrs, uint64_t n,
+                       uint64_t nnz, void** out) {
+    return guarded([&] {
+        std::vector<std::uint64_t> off(offsets, offsets + n + 1);
+        std::vector<NodeId> nb(nbrs, nbrs + nnz);
+        *out = new Graph(Graph::from_csr(std::move(off), std::move(nb)));
+    });
+}
+
+// Text edge list through the reference loader (graph.cpp:113-171).
+int ref_graph_from_edge_text(const char* text, void** out) {
+    return guarded([&] {
+        std::istringstream in{std::string(text)};
+        *out = new Graph(load_edge_list(in));
+    });
+}
+
+void ref_graph_free(void* g) { delete static_cast<Graph*>(g); }
+
+uint64_t ref_graph_n(void* g) { return static_cast<Graph*>(g)->node_count(); }
+uint64_t ref_graph_nnz(void* g) { return static_cast<Graph*>(g)->volume(); }
+uint64_t ref_graph_hash(void* g) { return static_cast<Graph*>(g)->structure_hash(); }
+
+int ref_graph_csr(void* gp, uint64_t* offsets, uint32_t* nbrs) {
+    const Graph& g = *static_cast<Graph*>(gp);
+    std::memcpy(offsets, g.offsets().data(), g.offsets().size() * sizeof(uint64_t));
+    std::memcpy(nbrs, g.neighbor_array().data(), g.neighbor_array().size() * sizeof(uint32_t));
+    return 0;
+}
+
+int ref_apply_walk(void* gp, const double* x, double* out) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        NodeVector xv(x, x + g.node_count());
+        auto y = apply_walk(g, xv);
+        std::memcpy(out, y.data(), y.size() * sizeof(double));
+    });
+}
+
+// cheby_power (solvers.cpp:236) with optional per-step residual-sum trace
+// (mass_out[K+1]) captured through the reference's StepObserver.
+int ref_cheby_power(void* gp, int family, double param, uint32_t source, uint64_t K,
+                    double* out, double* mass_out, uint64_t* stats_u64, double* wall) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        StepObserver obs;
+        if (mass_out)
+            obs = [&](std::uint32_t k, const NodeVector& r, const NodeVector&) {
+                double s = 0.0;
+                for (double v : r) s += v;
+                mass_out[k] = s;
+            };
+        Estimate est = cheby_power(g, make_kernel(family, param), source, K, obs);
+        std::memcpy(out, est.values.data(), est.values.size() * sizeof(double));
+        if (stats_u64) {
+            stats_u64[0] = est.stats.iterations;
+            stats_u64[1] = est.stats.push_work;
+        }
+        if (wall) *wall = est.stats.wall_seconds;
+    });
+}
+
+// cheby_power with a full residual/estimate trace ((K+1) x n each).
+int ref_cheby_power_trace(void* gp, int family, double param, uint32_t source, uint64_t K,
+                          double* out, double* r_trace, double* est_trace) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const std::size_t n = g.node_count();
+        StepObserver obs = [&](std::uint32_t k, const NodeVector& r, const NodeVector& e) {
+            std::memcpy(r_trace + k * n, r.data(), n * sizeof(double));
+            std::memcpy(est_trace + k * n, e.data(), n * sizeof(double));
+        };
+        Estimate est = cheby_power(g, make_kernel(family, param), source, K, obs);
+        std::memcpy(out, est.values.data(), n * sizeof(double));
+    });
+}
+
+int ref_cheby_power_vec(void* gp, int family, double param, const double* seed, uint64_t K,
+                        double* out) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        NodeVector s(seed, seed + g.node_count());
+        Estimate est = cheby_power_vec(g, make_kernel(family, param), s, K);
+        std::memcpy(out, est.values.data(), est.values.size() * sizeof(double));
+    });
+}
+
+// general_gp_vector with ChebyPower (solvers.cpp:390-403).
+int ref_general_gp_vector(void* gp, int family, double param, double a, const double* x,
+                          uint64_t steps, double* out) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        NodeVector xv(x, x + g.node_count());
+        GpParams p;
+        p.steps = steps;
+        auto z = general_gp_vector(g, make_kernel(family, param), a, xv, Algorithm::ChebyPower, p);
+        std::memcpy(out, z.data(), z.size() * sizeof(double));
+    });
+}
+
+int ref_ground_truth(void* gp, int family, double param, uint32_t source, double* out) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        auto t = ground_truth(g, make_kernel(family, param), source);
+        std::memcpy(out, t.values.data(), t.values.size() * sizeof(double));
+    });
+}
+
+int ref_select_sources_uniform(void* gp, uint64_t count, uint64_t seed, uint32_t* out) {
+    return guarded([&] {
+        auto s = select_sources(*static_cast<Graph*>(gp), SourceStrategy::Uniform, count, seed);
+        std::memcpy(out, s.data(), s.size() * sizeof(uint32_t));
+    });
+}
+
+// The reference bench's worker pool (tools/chebyprop.cpp:305-334): P threads
+// pull sources from an atomic cursor; each runs the reference cheby_power.
+// Returns the summed per-query wall_seconds (stats.wall_seconds, solvers.cpp:232)
+// in *sum_wall; out may be NULL (results discarded).
+int ref_cheby_power_pool(void* gp, int family, double param, const uint32_t* sources,
+                         uint64_t n_sources, uint64_t K, int n_threads, double* out,
+                         double* sum_wall) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const Kernel kernel = make_kernel(family, param);
+        const std::size_t n = g.node_count();
+        std::atomic<std::size_t> cursor{0};
+        std::vector<double> walls(n_sources, 0.0);
+        std::atomic<int> failed{0};
+        auto worker = [&]() {
+            for (;;) {
+                const std::size_t i = cursor.fetch_add(1);
+                if (i >= n_sources) return;
+                try {
+                    Estimate est = cheby_power(g, kernel, sources[i], K);
+                    walls[i] = est.stats.wall_seconds;
+                    if (out) std::memcpy(out + i * n, est.values.data(), n * sizeof(double));
+                } catch (...) {
+                    failed = 1;
+                }
+            }
+        };
+        if (n_threads <= 1) {
+            worker();
+        } else {
+            std::vector<std::thread> pool;
+            for (int i = 0; i < n_threads; ++i) pool.emplace_back(worker);
+            for (auto& th : pool) th.join();
+        }
+        if (failed) throw ParameterError("cheby_power failed in pool");
+        double s = 0.0;
+        for (double w : walls) s += w;
+        if (sum_wall) *sum_wall = s;
+    });
+}
+
+} // extern "C"

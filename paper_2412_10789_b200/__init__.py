@@ -1,0 +1,521 @@
+"""paper_2412_10789_b200 -- B200-native ChebyPower (arXiv 2412.10789) behind the
+reference's own API.
+
+Python mirror of the reference C++ surface for the hot path
+(reference paths relative to /root/reference/proj):
+
+=============================  ==================================================
+this package                   reference
+=============================  ==================================================
+``Graph.from_csr``             ``Graph::from_csr``            graph.hpp:51-53, graph.cpp:48-104
+``Kernel.ppr / Kernel.hkpr``   ``Kernel::ppr / Kernel::hkpr``  kernels.hpp:15-42, kernels.cpp:37-51
+``ppr_cheby_coeffs``           ``ppr_cheby_coeffs``            kernels.cpp:157-170
+``hkpr_cheby_coeffs``          ``hkpr_cheby_coeffs``           kernels.cpp:172-194
+``plan_truncation``            ``plan_truncation``             kernels.cpp:253-341
+``parse_kernel_spec``          ``parse_kernel_spec``           kernels.cpp:343-383 (ppr/hkpr)
+``cheby_power``                ``cheby_power``                 solvers.cpp:236-239
+``cheby_power_vec``            ``cheby_power_vec``             solvers.cpp:197-234
+``apply_walk``                 ``apply_walk``                  graph.cpp:269-273
+``general_gp_vector/matrix``   same (ChebyPower only)          solvers.cpp:390-414
+``cheby_power_many``           bench worker pool of cheby_power (tools/chebyprop.cpp:305-334),
+                               single-source or batched 64-column SpMM tiles
+=============================  ==================================================
+
+Errors follow error.hpp: ``ParameterError`` (a ``ValueError``) for bad sources,
+K < 1, alpha/t/epsilon out of domain, length mismatches; ``StructuralError`` for
+invalid CSR.  All compute runs in ``libcpg.so`` (sm_100a); there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import cpg_graph_info, cpg_plan, cpg_stats
+
+__all__ = [
+    "ParameterError", "StructuralError", "DeviceError", "Graph", "DeviceGraph", "Kernel", "KernelFamily",
+    "TruncationPlan", "SolveStats", "Estimate", "ppr_cheby_coeffs", "hkpr_cheby_coeffs", "plan_truncation",
+    "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
+    "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR",
+]
+
+
+# ---- errors (error.hpp:7-30) -------------------------------------------------------------
+class ParameterError(ValueError):
+    pass
+
+
+class StructuralError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str = "") -> None:
+    if rc == L.CPG_OK:
+        return
+    msg = L.last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == L.CPG_EINVAL:
+        raise ParameterError(msg)
+    if rc == L.CPG_ESTRUCT:
+        raise StructuralError(msg)
+    raise DeviceError(f"[status {rc}] {msg}")
+
+
+def _f64p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _u32p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def _u64p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+# ---- kernels (kernels.hpp) ---------------------------------------------------------------
+class KernelFamily:
+    Ppr = 0
+    Hkpr = 1
+
+
+def ppr_cheby_coeffs(alpha: float, max_index: int) -> np.ndarray:
+    out = np.empty(max_index + 1)
+    _check(L.lib().cpg_ppr_cheby_coeffs(float(alpha), int(max_index), _f64p(out)))
+    return out
+
+
+def hkpr_cheby_coeffs(t: float, max_index: int) -> np.ndarray:
+    out = np.empty(max_index + 1)
+    _check(L.lib().cpg_hkpr_cheby_coeffs(float(t), int(max_index), _f64p(out)))
+    return out
+
+
+def _fmt(v: float) -> str:
+    r = repr(float(v))
+    return r[:-2] if r.endswith(".0") else r
+
+
+class Kernel:
+    """Propagation kernel f (PPR or HKPR), validated like kernels.cpp:26-51."""
+
+    def __init__(self, family: int, param: float):
+        self._family = family
+        self._param = float(param)
+
+    @staticmethod
+    def ppr(alpha: float) -> "Kernel":
+        if not (0.0 < alpha < 1.0):
+            raise ParameterError(f"ppr: alpha must lie in (0,1), got {alpha}")
+        return Kernel(KernelFamily.Ppr, alpha)
+
+    @staticmethod
+    def hkpr(t: float) -> "Kernel":
+        if not (t > 0.0):
+            raise ParameterError(f"hkpr: t must be positive, got {t}")
+        return Kernel(KernelFamily.Hkpr, t)
+
+    def family(self) -> int:
+        return self._family
+
+    def alpha(self) -> float:
+        if self._family != KernelFamily.Ppr:
+            raise ParameterError("kernel is not ppr")
+        return self._param
+
+    def t(self) -> float:
+        if self._family != KernelFamily.Hkpr:
+            raise ParameterError("kernel is not hkpr")
+        return self._param
+
+    @property
+    def param(self) -> float:
+        return self._param
+
+    def cheby_coeffs(self, max_index: int) -> np.ndarray:
+        out = np.empty(max_index + 1)
+        _check(L.lib().cpg_cheby_coeffs(self._family, self._param, int(max_index), _f64p(out)))
+        return out
+
+    def descriptor(self) -> str:  # kernels.cpp:132-137
+        if self._family == KernelFamily.Ppr:
+            return "ppr:alpha=" + _fmt(self._param)
+        return "hkpr:t=" + _fmt(self._param)
+
+    def __repr__(self) -> str:
+        return f"Kernel({self.descriptor()})"
+
+
+def parse_kernel_spec(spec: str) -> Kernel:
+    fam, par = ctypes.c_int(), ctypes.c_double()
+    _check(L.lib().cpg_parse_kernel_spec(spec.encode(), ctypes.byref(fam), ctypes.byref(par)))
+    return Kernel(fam.value, par.value)
+
+
+@dataclass
+class TruncationPlan:  # kernels.hpp:48-53
+    cheby_steps: int
+    taylor_steps: int
+    epsilon: float
+    tail_bound: float
+
+
+def plan_truncation(kernel: Kernel, epsilon: float) -> TruncationPlan:
+    p = cpg_plan()
+    _check(L.lib().cpg_plan_truncation(kernel.family(), kernel.param, float(epsilon), ctypes.byref(p)))
+    return TruncationPlan(int(p.cheby_steps), int(p.taylor_steps), p.epsilon, p.tail_bound)
+
+
+# ---- graph (graph.hpp) -------------------------------------------------------------------
+class Graph:
+    """Immutable CSR of a simple undirected graph (graph.hpp:26-66).
+
+    ``offsets`` uint64[n+1] and ``neighbors`` uint32[2m] in the reference's own
+    layout; device copies are created lazily per GPU (``device(i)``) and cached.
+    """
+
+    def __init__(self, offsets: np.ndarray, neighbors: np.ndarray, structure_hash: int = 0):
+        self._off = offsets
+        self._nbr = neighbors
+        self._hash = structure_hash
+        self._dev: dict[int, DeviceGraph] = {}
+
+    @staticmethod
+    def from_csr(offsets, neighbors, validate: bool = True) -> "Graph":
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        h = ctypes.c_uint64(0)
+        if validate:
+            if len(off) == 0:
+                raise StructuralError("CSR offsets must start at 0")
+            _check(L.lib().cpg_validate_csr(_u64p(off), _u32p(nbr), len(off) - 1, len(nbr), ctypes.byref(h)))
+        return Graph(off, nbr, h.value)
+
+    def node_count(self) -> int:
+        return len(self._off) - 1
+
+    def edge_count(self) -> int:
+        return len(self._nbr) // 2
+
+    def volume(self) -> int:
+        return len(self._nbr)
+
+    def degree(self, u: int) -> int:
+        return int(self._off[u + 1] - self._off[u])
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self._off).astype(np.int64)
+
+    def offsets(self) -> np.ndarray:
+        return self._off
+
+    def neighbor_array(self) -> np.ndarray:
+        return self._nbr
+
+    def structure_hash(self) -> int:
+        return self._hash
+
+    def device(self, dev: int = 0) -> "DeviceGraph":
+        if dev not in self._dev:
+            self._dev[dev] = DeviceGraph.from_host(self._off, self._nbr, dev)
+        return self._dev[dev]
+
+
+class DeviceGraph:
+    """A ``cpg_graph*`` handle: the relabelled CSR resident on one GPU (or one row shard)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        self.info = cpg_graph_info()
+        _check(L.lib().cpg_graph_info_get(self._h, ctypes.byref(self.info)))
+
+    @classmethod
+    def from_host(cls, offsets, neighbors, device: int = 0, validate: bool = False) -> "DeviceGraph":
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _check(L.lib().cpg_graph_create(_u64p(off), _u32p(nbr), len(off) - 1, len(nbr), device, int(validate),
+                                        ctypes.byref(h)), "cpg_graph_create")
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, csr: "DeviceCSR") -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        _check(L.lib().cpg_graph_create_device(csr.offsets_ptr, csr.neighbors_ptr, csr.n, csr.nnz, csr.device,
+                                               ctypes.byref(h)), "cpg_graph_create_device")
+        return cls(h)
+
+    @classmethod
+    def sharded(cls, offsets_ptr, neighbors_ptr, n: int, nnz: int, on_device: bool, device: int, rank: int,
+                nranks: int, nccl_id: Optional[bytes]) -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(L.lib().cpg_graph_create_sharded(offsets_ptr, neighbors_ptr, n, nnz, int(on_device), device, rank,
+                                                nranks, idbuf, ctypes.byref(h)), "cpg_graph_create_sharded")
+        return cls(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n(self) -> int:
+        return self.info.n
+
+    def bytes_per_step(self, tile: int = 1) -> float:
+        return float(L.lib().cpg_bytes_per_step(self._h, tile))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().cpg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(L.lib().cpg_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ---- solvers (solvers.hpp) ---------------------------------------------------------------
+@dataclass
+class SolveStats:  # solvers.hpp:18-25 + device evidence
+    iterations: int = 0
+    push_work: int = 0
+    walks: int = 0
+    wall_seconds: float = 0.0
+    algorithm: str = "chebypower"
+    params: str = ""
+    device_ms: float = 0.0
+    mass_err_max: float = 0.0
+    bytes_model: float = 0.0
+    launches: int = 0
+
+
+@dataclass
+class Estimate:  # solvers.hpp:27-30
+    values: np.ndarray
+    stats: SolveStats = field(default_factory=SolveStats)
+
+
+StepObserver = Callable[[int, np.ndarray, np.ndarray], None]
+
+
+def _to_stats(s: cpg_stats, K: int) -> SolveStats:
+    return SolveStats(iterations=int(s.iterations), push_work=int(s.push_work), wall_seconds=s.wall_seconds,
+                      algorithm="chebypower", params=f"K={K}", device_ms=s.device_ms,
+                      mass_err_max=s.mass_err_max, bytes_model=s.bytes_model, launches=int(s.launches))
+
+
+def _dev(g, device: int) -> DeviceGraph:
+    return g if isinstance(g, DeviceGraph) else g.device(device)
+
+
+def _steps(cheby_steps) -> int:
+    K = int(cheby_steps)
+    if K < 1:
+        raise ParameterError("cheby_power: cheby_steps must be >= 1")  # solvers.cpp:201
+    return K
+
+
+def cheby_power(g, kernel: Kernel, source: int, cheby_steps: int, observer: Optional[StepObserver] = None,
+                device: int = 0) -> Estimate:
+    """yhat = sum_{k=0..K} c_k T_k(P) e_source (solvers.cpp:236-239) on the GPU."""
+    t0 = time.perf_counter()
+    K = _steps(cheby_steps)
+    c = kernel.cheby_coeffs(K)  # coefficients inside the call, like solvers.cpp:205
+    dg = _dev(g, device)
+    if source < 0 or source >= dg.n:
+        raise ParameterError(f"source node {source} out of range")
+    n = dg.n
+    out = np.empty(n)
+    if observer is not None:  # slow path: per-step T_k and partial estimates (tests only)
+        rt = np.empty((K + 1, n))
+        et = np.empty((K + 1, n))
+        _check(L.lib().cpg_chebypower_trace(dg.handle, _f64p(c), K, int(source), out.ctypes.data,
+                                            rt.ctypes.data, et.ctypes.data))
+        for k in range(K + 1):
+            observer(k, rt[k], et[k])
+        st = SolveStats(iterations=K, push_work=K * int(dg.info.nnz), params=f"K={K}")
+    else:
+        s = cpg_stats()
+        src = np.array([source], dtype=np.uint32)
+        _check(L.lib().cpg_chebypower(dg.handle, _f64p(c), K, _u32p(src), 1, out.ctypes.data, ctypes.byref(s)))
+        st = _to_stats(s, K)
+    st.wall_seconds = time.perf_counter() - t0
+    return Estimate(out, st)
+
+
+def cheby_power_vec(g, kernel: Kernel, seed, cheby_steps: int, device: int = 0) -> Estimate:
+    """cheby_power_vec (solvers.cpp:197-234) for a dense seed vector (or an (s, n) stack)."""
+    t0 = time.perf_counter()
+    K = _steps(cheby_steps)
+    dg = _dev(g, device)
+    seeds = np.ascontiguousarray(seed, dtype=np.float64)
+    single = seeds.ndim == 1
+    seeds = seeds.reshape(-1, seeds.shape[-1])
+    if seeds.shape[1] != dg.n:
+        raise ParameterError("seed vector length mismatch")  # solvers.cpp:36-37
+    c = kernel.cheby_coeffs(K)
+    out = np.empty_like(seeds)
+    s = cpg_stats()
+    _check(L.lib().cpg_chebypower_vec(dg.handle, _f64p(c), K, _f64p(seeds), seeds.shape[0], out.ctypes.data,
+                                      ctypes.byref(s)))
+    st = _to_stats(s, K)
+    st.wall_seconds = time.perf_counter() - t0
+    return Estimate(out[0] if single else out, st)
+
+
+def cheby_power_many(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, out: Optional[np.ndarray] = None,
+                     batched: bool = False, tile: int = 64, device: int = 0):
+    """Many single-source queries in one call: returns (values[n_sources, n], SolveStats).
+
+    ``batched=False`` runs each source through the fused SpMV step;
+    ``batched=True`` runs tiles of ``tile`` sources through the SpMM step.
+    ``out`` may be a pinned host buffer (then D2H overlaps compute).
+    """
+    K = _steps(cheby_steps)
+    dg = _dev(g, device)
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    c = kernel.cheby_coeffs(K)
+    if out is None:
+        out = np.empty((len(src), dg.n))
+    s = cpg_stats()
+    ptr = out.ctypes.data if isinstance(out, np.ndarray) else int(out)
+    if batched:
+        _check(L.lib().cpg_chebypower_batched(dg.handle, _f64p(c), K, _u32p(src), len(src), tile, ptr,
+                                              ctypes.byref(s)))
+    else:
+        _check(L.lib().cpg_chebypower(dg.handle, _f64p(c), K, _u32p(src), len(src), ptr, ctypes.byref(s)))
+    return out, _to_stats(s, K)
+
+
+def apply_walk(g, x, device: int = 0) -> np.ndarray:
+    """y = A D^-1 x (graph.cpp:257-273) on the GPU."""
+    dg = _dev(g, device)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.shape != (dg.n,):
+        raise ParameterError("apply_walk: vector length mismatch")
+    y = np.empty(dg.n)
+    _check(L.lib().cpg_apply_walk(dg.handle, _f64p(x), _f64p(y)))
+    return y
+
+
+def general_gp_vector(g: Graph, kernel: Kernel, a: float, x, steps: int, device: int = 0) -> np.ndarray:
+    """z = D^-a f(P) D^a x with ChebyPower (solvers.cpp:390-403)."""
+    deg = g.degrees().astype(np.float64)
+    x = np.asarray(x, dtype=np.float64)
+    scaled = np.power(deg, a) * x
+    est = cheby_power_vec(g, kernel, scaled, steps, device=device)
+    return np.power(deg, -a) * est.values
+
+
+def general_gp_matrix(g: Graph, kernel: Kernel, a: float, columns, steps: int, device: int = 0):
+    """Column-wise general_gp_vector (solvers.cpp:405-414), all columns in one device call."""
+    cols = np.atleast_2d(np.asarray(columns, dtype=np.float64))
+    deg = g.degrees().astype(np.float64)
+    scaled = cols * np.power(deg, a)[None, :]
+    est = cheby_power_vec(g, kernel, scaled, steps, device=device)
+    return list(est.values * np.power(deg, -a)[None, :])
+
+
+# ---- synthetic inputs ----------------------------------------------------------------------
+class DeviceCSR:
+    """A generator-built CSR resident on one GPU (owned; freed on close)."""
+
+    def __init__(self, off_ptr: int, nbr_ptr: int, n: int, nnz: int, device: int):
+        self.offsets_ptr = off_ptr
+        self.neighbors_ptr = nbr_ptr
+        self.n = n
+        self.nnz = nnz
+        self.device = device
+
+    def close(self):
+        if self.offsets_ptr:
+            L.lib().cpg_free_csr(ctypes.c_void_p(self.offsets_ptr), ctypes.c_void_p(self.neighbors_ptr), self.device)
+            self.offsets_ptr = self.neighbors_ptr = 0
+
+    def to_host(self):
+        import torch  # plumbing only: device->host copy of the generated CSR
+
+        off = np.empty(self.n + 1, dtype=np.uint64)
+        nbr = np.empty(self.nnz, dtype=np.uint32)
+        cudart = torch.cuda.cudart()
+        torch.cuda.synchronize(self.device)
+        # cudaMemcpy(dst, src, bytes, DeviceToHost=2)
+        cudart.cudaMemcpy(off.ctypes.data, self.offsets_ptr, off.nbytes, 2)
+        cudart.cudaMemcpy(nbr.ctypes.data, self.neighbors_ptr, nbr.nbytes, 2)
+        return off, nbr
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _gen_result(rc, off, nbr, n, nnz, device):
+    _check(rc, "generator")
+    if device < 0:
+        o = np.ctypeslib.as_array(ctypes.cast(off, ctypes.POINTER(ctypes.c_uint64)), shape=(n.value + 1,)).copy()
+        b = np.ctypeslib.as_array(ctypes.cast(nbr, ctypes.POINTER(ctypes.c_uint32)), shape=(nnz.value,)).copy()
+        L.lib().cpg_free_csr(off, nbr, -1)
+        return o, b
+    return DeviceCSR(off.value, nbr.value, n.value, nnz.value, device)
+
+
+def gen_rmat(scale: int, n_samples: int, a=0.57, b=0.19, c=0.19, seed: int = 1, device: int = -1):
+    """Seeded R-MAT, symmetrised/deduplicated/compacted.  device=-1: host (offsets, neighbors)."""
+    off, nbr = ctypes.c_void_p(), ctypes.c_void_p()
+    n, nnz = ctypes.c_uint32(), ctypes.c_uint64()
+    rc = L.lib().cpg_gen_rmat(scale, n_samples, a, b, c, seed, device, ctypes.byref(off), ctypes.byref(nbr),
+                              ctypes.byref(n), ctypes.byref(nnz))
+    return _gen_result(rc, off, nbr, n, nnz, device)
+
+
+def gen_chunglu(n_ids: int, n_samples: int, exponent: float, mean_degree: float, max_degree: int = 0,
+                seed: int = 1, device: int = -1):
+    """Seeded Chung-Lu with power-law expected degrees.  device=-1: host (offsets, neighbors)."""
+    off, nbr = ctypes.c_void_p(), ctypes.c_void_p()
+    n, nnz = ctypes.c_uint32(), ctypes.c_uint64()
+    rc = L.lib().cpg_gen_chunglu(n_ids, n_samples, exponent, mean_degree, max_degree, seed, device,
+                                 ctypes.byref(off), ctypes.byref(nbr), ctypes.byref(n), ctypes.byref(nnz))
+    return _gen_result(rc, off, nbr, n, nnz, device)
+
+
+def select_sources_uniform(n: int, count: int, seed: int) -> np.ndarray:
+    """Seeded uniform sources without replacement: the reference's partial
+    Fisher-Yates over SplitMix64 (eval.cpp:67-90, rng.hpp:13-27)."""
+    if count > n:
+        raise ParameterError("select_sources: count exceeds node count")
+    M = (1 << 64) - 1
+    state = seed & M
+    picked: dict[int, int] = {}
+    out = np.empty(count, dtype=np.uint32)
+    for i in range(count):
+        state = (state + 0x9E3779B97F4A7C15) & M
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        z ^= z >> 31
+        j = i + ((z * (n - i)) >> 64)
+        vi, vj = picked.get(i, i), picked.get(j, j)
+        picked[i], picked[j] = vj, vi
+        out[i] = vj
+    return out

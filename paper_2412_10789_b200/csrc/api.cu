@@ -1,0 +1,625 @@
+// api.cu -- C-ABI entry points (include/cpg.h): graph handles and the query
+// drivers that sequence the fused step kernels.
+//
+// Per single-source query (cheby_power, solvers.cpp:197-239):
+//   memset(w_a) ; w_a[s] = 1/d_s                       (w_0 = D^-1 e_s)
+//   for k = 1..K: step(w_cur = w_{k-1}, w_io = w_{k-2} -> w_k)   [+ all-gather if sharded]
+//   per-step mass sums -> |sum T_k - 1| check           (acceptance C13)
+//   unpermute d*acc into the caller's ids
+// Host outputs are copied on a second stream, one query behind the compute
+// stream, so D2H of query q overlaps the K steps of query q+1.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cpg_graph.hpp"
+
+using namespace cpg;
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t count) {
+    T* p = nullptr;
+    CPG_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+    return p;
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        CPG_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+std::atomic<int> g_profile{0};
+
+// Event pairs around step-kernel launches (profiling mode only).
+struct StepProf {
+    std::vector<cudaEvent_t> ev;
+    void before(cudaStream_t st) { rec(st); }
+    void after(cudaStream_t st) { rec(st); }
+    void rec(cudaStream_t st) {
+        cudaEvent_t e;
+        CPG_CUDA(cudaEventCreate(&e));
+        CPG_CUDA(cudaEventRecord(e, st));
+        ev.push_back(e);
+    }
+    double total_ms() {
+        double t = 0.0;
+        for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+            float ms = 0.f;
+            cudaEventSynchronize(ev[i + 1]);
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            t += ms;
+        }
+        return t;
+    }
+    ~StepProf() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t n, uint64_t nnz, int device,
+                         int rank, int nranks) {
+    auto g = std::make_unique<cpg_graph>();
+    g->device = device;
+    g->rank = rank;
+    g->nranks = nranks;
+    g->n = n;
+    g->nnz = nnz;
+    CPG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    CPG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : g->ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CPG_CUDA(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device));
+    build_device_graph(g.get(), d_off, d_nbr, g->stream);
+    g->hub_partial = dalloc<double>(g->n_hub_items);
+    g->hub_count = dalloc<unsigned int>(g->n_hubs);
+    CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_hubs)));
+    const int occ = std::max(1, step_occupancy());
+    g->step_grid = static_cast<int>(std::max<uint32_t>(
+        1, std::min<uint64_t>(g->n_items, static_cast<uint64_t>(occ) * g->sm_count)));
+    g->batch_grid = std::max(1, batch_occupancy()) * g->sm_count;
+    g->d_mass_err = dalloc<double>(2);
+    CPG_CUDA(cudaDeviceSynchronize());
+    return g.release();
+}
+
+void ensure_ws(cpg_graph* g, size_t cols) {
+    if (g->ws_cols >= cols) return;
+    dfree(g->w_a);
+    dfree(g->w_b);
+    dfree(g->acc);
+    dfree(g->full);
+    g->w_a = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    g->w_b = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    g->acc = dalloc<double>(static_cast<size_t>(g->n_loc) * cols);
+    if (g->nranks > 1) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    CPG_CUDA(cudaMemset(g->w_a, 0, sizeof(double) * g->n_pad * cols));
+    CPG_CUDA(cudaMemset(g->w_b, 0, sizeof(double) * g->n_pad * cols));
+    g->ws_cols = cols;
+}
+
+void ensure_params(cpg_graph* g, uint32_t K, uint32_t n_sources) {
+    if (g->coeff_cap < K + 1) {
+        dfree(g->d_coeffs);
+        dfree(g->d_step_mass);
+        g->d_coeffs = dalloc<double>(K + 1);
+        g->d_step_mass = dalloc<double>(K + 1);
+        g->coeff_cap = K + 1;
+    }
+    if (g->src_cap < n_sources) {
+        dfree(g->d_sources);
+        g->d_sources = dalloc<uint32_t>(n_sources);
+        g->src_cap = n_sources;
+    }
+    const size_t need = static_cast<size_t>(K) * g->step_grid;
+    if (g->mass_cap < need) {
+        dfree(g->d_mass_partial);
+        g->d_mass_partial = dalloc<double>(need);
+        g->mass_cap = need;
+    }
+}
+
+void ensure_stage(cpg_graph* g, size_t doubles) {
+    if (g->stage_cap >= doubles) return;
+    dfree(g->d_stage);
+    g->d_stage = dalloc<double>(2 * doubles);
+    g->stage_cap = doubles;
+}
+
+void check_query(const cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t ns) {
+    require(g != nullptr, "null graph handle");
+    require(K >= 1, "cheby_power: cheby_steps must be >= 1");  // solvers.cpp:201
+    require(coeffs != nullptr, "null coefficient array");
+    require(ns == 0 || sources != nullptr, "null source array");
+    for (uint32_t i = 0; i < ns; ++i)
+        require(sources[i] < g->n, "source node " + std::to_string(sources[i]) + " out of range");  // :28-29
+}
+
+// One single-source (or dense-seed, when seed_dev != null) query into
+// local acc; then d_dst[n] (caller ids) if non-null.
+uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
+                    cudaStream_t st, StepProf* prof) {
+    uint32_t launches = 0;
+    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
+    if (seed_dev)
+        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, st);
+    else
+        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
+    ++launches;
+    for (uint32_t k = 1; k <= K; ++k) {
+        StepArgs a;
+        a.rowptr = g->rowptr;
+        a.col = g->col;
+        a.items = g->items;
+        a.w_cur = (k & 1) ? g->w_a : g->w_b;
+        a.w_io = (k & 1) ? g->w_b : g->w_a;
+        a.acc = g->acc;
+        a.out = g->acc;
+        a.hub_partial = g->hub_partial;
+        a.hub_count = g->hub_count;
+        a.mass_partial = g->d_mass_partial + static_cast<size_t>(k - 1) * g->step_grid;
+        a.coeffs = g->d_coeffs;
+        a.row0 = g->row0;
+        a.n_items = g->n_items;
+        a.k = static_cast<int>(k);
+        a.first = k == 1;
+        a.last = k == K;
+        if (prof) prof->before(st);
+        launch_step(a, g->step_grid, st);
+        if (prof) prof->after(st);
+        ++launches;
+        if (g->nranks > 1) nccl_allgather_f64(a.w_io + g->row0, a.w_io, g->n_loc, g->nccl_comm, st);
+    }
+    launch_mass_steps(g->d_mass_partial, g->step_grid, K, g->d_step_mass, st);
+    ++launches;
+    if (g->nranks > 1) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
+    launch_mass_err(g->d_step_mass, K, mass0, g->d_mass_err, st);
+    ++launches;
+    if (d_dst) {
+        const double* src = g->acc;
+        if (g->nranks > 1) {
+            nccl_allgather_f64(g->acc, g->full, g->n_loc, g->nccl_comm, st);
+            src = g->full;
+        }
+        launch_unpermute(d_dst, src, g->new_of_old, g->n, st);
+        ++launches;
+    }
+    CPG_CUDA(cudaGetLastError());
+    return launches;
+}
+
+// One tile of up to 64 sources (q0 .. q0+count) through the batched step.
+uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t count, double* d_dst, cudaStream_t st,
+                   StepProf* prof) {
+    uint32_t launches = 0;
+    const size_t cols = kBatchCols;
+    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
+    launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, st);
+    ++launches;
+    for (uint32_t k = 1; k <= K; ++k) {
+        BatchArgs b;
+        b.rowptr = g->rowptr;
+        b.col = g->col;
+        b.hub_items = g->bitems;
+        b.n_hub_items = g->n_bhub_items;
+        b.hub_rows = g->n_bhubs;
+        b.n_loc = g->n_loc;
+        b.w_cur = (k & 1) ? g->w_a : g->w_b;
+        b.w_io = (k & 1) ? g->w_b : g->w_a;
+        b.acc = g->acc;
+        b.out = g->acc;
+        b.hub_partial = g->bhub_partial;
+        b.hub_count = g->bhub_count;
+        b.coeffs = g->d_coeffs;
+        b.row0 = g->row0;
+        b.k = static_cast<int>(k);
+        b.first = k == 1;
+        b.last = k == K;
+        if (prof) prof->before(st);
+        launch_batch(b, g->batch_grid, st);
+        if (prof) prof->after(st);
+        ++launches;
+        if (g->nranks > 1)
+            nccl_allgather_f64(b.w_io + static_cast<size_t>(g->row0) * cols, b.w_io, g->n_loc * cols, g->nccl_comm,
+                               st);
+    }
+    if (d_dst) {
+        const double* src = g->acc;
+        if (g->nranks > 1) {
+            nccl_allgather_f64(g->acc, g->full, g->n_loc * cols, g->nccl_comm, st);
+            src = g->full;
+        }
+        launch_unpermute_batch(d_dst, src, g->new_of_old, g->n, count, st);
+        ++launches;
+    }
+    CPG_CUDA(cudaGetLastError());
+    return launches;
+}
+
+void upload_params(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t ns,
+                   cudaStream_t st) {
+    ensure_params(g, K, std::max<uint32_t>(ns, 1));
+    CPG_CUDA(cudaMemcpyAsync(g->d_coeffs, coeffs, sizeof(double) * (K + 1), cudaMemcpyHostToDevice, st));
+    if (ns) CPG_CUDA(cudaMemcpyAsync(g->d_sources, sources, sizeof(uint32_t) * ns, cudaMemcpyHostToDevice, st));
+    CPG_CUDA(cudaMemsetAsync(g->d_mass_err, 0, sizeof(double), st));
+}
+
+void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, double wall, float dev_ms,
+                uint32_t launches, uint32_t cols) {
+    if (!stats) return;
+    double merr = 0.0;
+    CPG_CUDA(cudaMemcpy(&merr, g->d_mass_err, sizeof(double), cudaMemcpyDeviceToHost));
+    stats->iterations = K;
+    stats->push_work = static_cast<uint64_t>(K) * g->nnz * queries;
+    stats->wall_seconds = wall;
+    stats->device_ms = dev_ms;
+    stats->mass_err_max = cols == 1 ? merr : 0.0;
+    const double tiles = cols == 1 ? static_cast<double>(queries) : std::ceil(static_cast<double>(queries) / cols);
+    stats->bytes_model = tiles * K * cpg_bytes_per_step(g, cols);
+    stats->launches = launches;
+    stats->step_ms = 0.0;
+    stats->step_launches = 0;
+}
+
+// Shared driver for host / device outputs.  mode 0 = one-hot single source,
+// 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources.
+int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
+          uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
+          cpg_stats* stats) {
+    return guarded([&] {
+        require(g != nullptr, "null graph handle");
+        if (mode == 1) {
+            require(K >= 1, "cheby_power: cheby_steps must be >= 1");
+            require(coeffs && (nq == 0 || seeds_host), "null argument");
+        } else {
+            check_query(g, coeffs, K, sources, nq);
+        }
+        std::lock_guard<std::mutex> lock(g->mu);
+        DeviceGuard dg(g->device);
+        const double t0 = now_s();
+        cudaStream_t st = g->stream;
+        cudaEvent_t e0, e1;
+        CPG_CUDA(cudaEventCreate(&e0));
+        CPG_CUDA(cudaEventCreate(&e1));
+        if (user_stream) {
+            CPG_CUDA(cudaEventRecord(g->ev[4], static_cast<cudaStream_t>(user_stream)));
+            CPG_CUDA(cudaStreamWaitEvent(st, g->ev[4], 0));
+        }
+        const size_t cols = mode == 2 ? kBatchCols : 1;
+        if (mode == 2) {
+            require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
+            ensure_batch_tables(g);
+            if (!g->bhub_partial) {
+                g->bhub_partial = dalloc<double>(static_cast<size_t>(g->n_bhub_items) * kBatchCols);
+                g->bhub_count = dalloc<unsigned int>(g->n_bhubs);
+                CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_bhubs)));
+            }
+        }
+        ensure_ws(g, cols);
+        upload_params(g, coeffs, K, sources, mode == 1 ? 0 : nq, st);
+        const size_t n = g->n;
+        const uint32_t per = mode == 2 ? tile : 1;
+        const uint32_t nbatches = (nq + per - 1) / per;
+        const size_t slot = n * per;  // doubles per result slot
+        double* seed_dev = nullptr;
+        if (mode == 1) seed_dev = dalloc<double>(n);
+        if (!out_on_device && out) ensure_stage(g, slot);
+        uint32_t launches = 0;
+        std::unique_ptr<StepProf> prof(g_profile.load() ? new StepProf : nullptr);
+        CPG_CUDA(cudaEventRecord(e0, st));
+        for (uint32_t b = 0; b < nbatches; ++b) {
+            const uint32_t q0 = b * per;
+            const uint32_t count = std::min<uint32_t>(per, nq - q0);
+            double* dst = nullptr;
+            if (out && out_on_device) {
+                dst = out + static_cast<size_t>(q0) * n;
+            } else if (out) {
+                dst = g->d_stage + (b & 1) * slot;
+                CPG_CUDA(cudaStreamWaitEvent(st, g->ev[b & 1], 0));  // slot free (copy of b-2 done)
+            }
+            if (mode == 0) {
+                launches += run_single(g, K, q0, nullptr, 1.0, dst, st, prof.get());
+            } else if (mode == 1) {
+                const double* sh = seeds_host + static_cast<size_t>(q0) * n;
+                double mass0 = 0.0;
+                for (size_t v = 0; v < n; ++v) mass0 += sh[v];
+                CPG_CUDA(cudaMemcpyAsync(seed_dev, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+                launches += run_single(g, K, q0, seed_dev, mass0, dst, st, prof.get());
+            } else {
+                launches += run_batch(g, K, q0, count, dst, st, prof.get());
+            }
+            if (out && !out_on_device) {
+                // compute of batch b is queued; now drain batch b-1 (overlaps b's steps)
+                CPG_CUDA(cudaEventRecord(g->ev[2 + (b & 1)], st));
+                if (b >= 1) {
+                    CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + ((b - 1) & 1)], 0));
+                    const uint32_t pq0 = (b - 1) * per, pc = std::min<uint32_t>(per, nq - pq0);
+                    CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + ((b - 1) & 1) * slot,
+                                             sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
+                    CPG_CUDA(cudaEventRecord(g->ev[(b - 1) & 1], g->copy_stream));
+                }
+            }
+        }
+        CPG_CUDA(cudaEventRecord(e1, st));
+        if (out && !out_on_device && nbatches > 0) {
+            const uint32_t b = nbatches - 1;
+            const uint32_t pq0 = b * per, pc = std::min<uint32_t>(per, nq - pq0);
+            CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + (b & 1)], 0));
+            CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + (b & 1) * slot,
+                                     sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
+            CPG_CUDA(cudaEventRecord(g->ev[b & 1], g->copy_stream));
+            CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
+        }
+        if (user_stream) {
+            CPG_CUDA(cudaEventRecord(g->ev[4], st));
+            CPG_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(user_stream), g->ev[4], 0));
+        }
+        float ms = 0.f;
+        if (!user_stream || stats) {
+            CPG_CUDA(cudaStreamSynchronize(st));
+            CPG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (seed_dev) cudaFree(seed_dev);
+        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, static_cast<uint32_t>(cols));
+        if (stats && prof) {
+            stats->step_ms = prof->total_ms();
+            stats->step_launches = static_cast<uint32_t>(prof->ev.size() / 2);
+        }
+    });
+}
+
+} // namespace
+
+extern "C" {
+
+void cpg_set_profiling(int on) { g_profile.store(on ? 1 : 0); }
+
+int cpg_graph_create(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz, int device,
+                     int validate, cpg_graph** out) {
+    return guarded([&] {
+        require(offsets && neighbors && out, "null argument");
+        require(n > 0, "empty graph");
+        uint64_t h = 0;
+        if (validate) h = validate_csr(offsets, neighbors, n, nnz);
+        DeviceGuard dg(device);
+        uint64_t* d_off = dalloc<uint64_t>(static_cast<size_t>(n) + 1);
+        uint32_t* d_nbr = dalloc<uint32_t>(nnz);
+        CPG_CUDA(cudaMemcpy(d_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyHostToDevice));
+        CPG_CUDA(cudaMemcpy(d_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+        cpg_graph* g = nullptr;
+        try {
+            g = create_common(d_off, d_nbr, n, nnz, device, 0, 1);
+        } catch (...) {
+            cudaFree(d_off);
+            cudaFree(d_nbr);
+            throw;
+        }
+        cudaFree(d_off);
+        cudaFree(d_nbr);
+        g->hash = h;
+        *out = g;
+    });
+}
+
+int cpg_graph_create_device(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint32_t n, uint64_t nnz,
+                            int device, cpg_graph** out) {
+    return guarded([&] {
+        require(d_offsets && d_neighbors && out, "null argument");
+        require(n > 0, "empty graph");
+        DeviceGuard dg(device);
+        *out = create_common(d_offsets, d_neighbors, n, nnz, device, 0, 1);
+    });
+}
+
+int cpg_nccl_unique_id(void* out128) {
+    return guarded([&] {
+        require(out128 != nullptr, "null argument");
+        nccl_get_unique_id(out128);
+    });
+}
+
+int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                             int on_device, int device, int rank, int nranks, const void* nccl_unique_id,
+                             cpg_graph** out) {
+    return guarded([&] {
+        require(offsets && neighbors && out, "null argument");
+        require(n > 0, "empty graph");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank/nranks");
+        require(nranks == 1 || nccl_unique_id != nullptr, "sharded graph needs an NCCL unique id");
+        DeviceGuard dg(device);
+        const uint64_t* d_off = offsets;
+        const uint32_t* d_nbr = neighbors;
+        uint64_t* t_off = nullptr;
+        uint32_t* t_nbr = nullptr;
+        if (!on_device) {
+            t_off = dalloc<uint64_t>(static_cast<size_t>(n) + 1);
+            t_nbr = dalloc<uint32_t>(nnz);
+            CPG_CUDA(cudaMemcpy(t_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyHostToDevice));
+            CPG_CUDA(cudaMemcpy(t_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+            d_off = t_off;
+            d_nbr = t_nbr;
+        }
+        cpg_graph* g = nullptr;
+        try {
+            g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks);
+            if (nranks > 1) g->nccl_comm = nccl_comm_init(nccl_unique_id, nranks, rank);
+        } catch (...) {
+            if (t_off) cudaFree(t_off);
+            if (t_nbr) cudaFree(t_nbr);
+            if (g) cpg_graph_destroy(g);
+            throw;
+        }
+        if (t_off) cudaFree(t_off);
+        if (t_nbr) cudaFree(t_nbr);
+        *out = g;
+    });
+}
+
+int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info) {
+    return guarded([&] {
+        require(g && info, "null argument");
+        info->n = g->n;
+        info->nnz = g->nnz;
+        info->n_local = g->n_loc;
+        info->nnz_local = g->nnz_loc;
+        info->row_begin = g->row0;
+        info->n_padded = g->n_pad;
+        info->n_hubs = g->n_hubs;
+        info->n_items = g->n_items;
+        info->max_degree = g->max_degree;
+        info->rank = g->rank;
+        info->nranks = g->nranks;
+        info->device = g->device;
+        info->structure_hash = g->hash;
+    });
+}
+
+int cpg_graph_destroy(cpg_graph* g) {
+    if (!g) return CPG_OK;
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        cudaDeviceSynchronize();
+        if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
+        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->gdeg, (void*)g->new_of_old, (void*)g->items,
+                        (void*)g->bitems, (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
+                        (void*)g->bhub_count, (void*)g->w_a, (void*)g->w_b, (void*)g->acc, (void*)g->full,
+                        (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial, (void*)g->d_mass_err,
+                        (void*)g->d_step_mass, (void*)g->d_stage})
+            if (p) cudaFree(p);
+        for (auto e : g->ev)
+            if (e) cudaEventDestroy(e);
+        if (g->stream) cudaStreamDestroy(g->stream);
+        if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+        delete g;
+    });
+}
+
+int cpg_chebypower(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t n_sources,
+                   double* out, cpg_stats* stats) {
+    return drive(g, coeffs, K, sources, nullptr, n_sources, 1, 0, out, false, nullptr, stats);
+}
+
+int cpg_chebypower_device(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                          uint32_t n_sources, double* d_out, void* stream, cpg_stats* stats) {
+    return drive(g, coeffs, K, sources, nullptr, n_sources, 1, 0, d_out, true, stream, stats);
+}
+
+int cpg_chebypower_vec(cpg_graph* g, const double* coeffs, uint32_t K, const double* seeds, uint32_t n_seeds,
+                       double* out, cpg_stats* stats) {
+    return drive(g, coeffs, K, nullptr, seeds, n_seeds, 1, 1, out, false, nullptr, stats);
+}
+
+int cpg_chebypower_batched(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                           uint32_t n_sources, uint32_t tile, double* out, cpg_stats* stats) {
+    return drive(g, coeffs, K, sources, nullptr, n_sources, tile, 2, out, false, nullptr, stats);
+}
+
+int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                                  uint32_t n_sources, uint32_t tile, double* d_out, void* stream, cpg_stats* stats) {
+    return drive(g, coeffs, K, sources, nullptr, n_sources, tile, 2, d_out, true, stream, stats);
+}
+
+int cpg_apply_walk(cpg_graph* g, const double* x, double* y) {
+    const double c[2] = {0.0, 1.0};  // c0 T0 + c1 T1 = P x
+    return cpg_chebypower_vec(g, c, 1, x, 1, y, nullptr);
+}
+
+int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source, double* out,
+                         double* r_trace, double* est_trace) {
+    return guarded([&] {
+        check_query(g, coeffs, K, &source, 1);
+        require(g->nranks == 1, "trace is single-GPU only");
+        std::lock_guard<std::mutex> lock(g->mu);
+        DeviceGuard dg(g->device);
+        cudaStream_t st = g->stream;
+        ensure_ws(g, 1);
+        upload_params(g, coeffs, K, &source, 1, st);
+        const size_t n = g->n, np = g->n_pad;
+        std::vector<uint32_t> no(n), gdeg(np);
+        CPG_CUDA(cudaMemcpy(no.data(), g->new_of_old, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+        CPG_CUDA(cudaMemcpy(gdeg.data(), g->gdeg, sizeof(uint32_t) * np, cudaMemcpyDeviceToHost));
+        std::vector<double> w(np), acc(np);
+        auto emit = [&](uint32_t k, const double* wv, const double* av, double a_scale) {
+            for (size_t v = 0; v < n; ++v) {
+                const uint32_t gv = no[v];
+                const double d = static_cast<double>(gdeg[gv]);
+                if (r_trace) r_trace[k * n + v] = d * wv[gv];
+                if (est_trace) est_trace[k * n + v] = a_scale * d * av[gv];
+            }
+        };
+        // k = 0: T_0 = e_s, est = c0 e_s (solvers.cpp:209, 215)
+        for (size_t v = 0; v < n; ++v) {
+            if (r_trace) r_trace[v] = v == source ? 1.0 : 0.0;
+            if (est_trace) est_trace[v] = v == source ? coeffs[0] : 0.0;
+        }
+        CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * np, st));
+        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, 0, st);
+        for (uint32_t k = 1; k <= K; ++k) {
+            StepArgs a;
+            a.rowptr = g->rowptr;
+            a.col = g->col;
+            a.items = g->items;
+            a.w_cur = (k & 1) ? g->w_a : g->w_b;
+            a.w_io = (k & 1) ? g->w_b : g->w_a;
+            a.acc = g->acc;
+            a.out = g->acc;
+            a.hub_partial = g->hub_partial;
+            a.hub_count = g->hub_count;
+            a.mass_partial = g->d_mass_partial + static_cast<size_t>(k - 1) * g->step_grid;
+            a.coeffs = g->d_coeffs;
+            a.row0 = 0;
+            a.n_items = g->n_items;
+            a.k = static_cast<int>(k);
+            a.first = k == 1;
+            a.last = 0;
+            launch_step(a, g->step_grid, st);
+            CPG_CUDA(cudaGetLastError());
+            CPG_CUDA(cudaMemcpyAsync(w.data(), a.w_io, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+            CPG_CUDA(cudaMemcpyAsync(acc.data(), g->acc, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+            CPG_CUDA(cudaStreamSynchronize(st));
+            emit(k, w.data(), acc.data(), 1.0);
+            if (k == K && out)
+                for (size_t v = 0; v < n; ++v) out[v] = static_cast<double>(gdeg[no[v]]) * acc[no[v]];
+        }
+    });
+}
+
+double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile) {
+    if (!g) return 0.0;
+    // 4 B index + 8*B B gathered row per edge, 8 B row pointer
+    // per row, 4 streams of 8*B B per row (read w_{k-1}, write w_{k+1}, read+write
+    // acc); sharded adds the received all-gather bytes 8*B*n*(R-1)/R.
+    const double B = tile <= 1 ? 1.0 : kBatchCols;
+    const double nnz = static_cast<double>(g->nnz_loc), nl = static_cast<double>(g->n_loc);
+    double bytes = nnz * (4.0 + 8.0 * B) + 8.0 * (nl + 1) + 32.0 * nl * B;
+    if (g->nranks > 1)
+        bytes += 8.0 * B * static_cast<double>(g->n_pad) * (g->nranks - 1) / g->nranks;
+    return bytes;
+}
+
+} // extern "C"

@@ -1,0 +1,91 @@
+// cpg_graph.hpp -- host-side handle behind cpg_graph* (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+#include "cpg_common.hpp"
+#include "device_graph.cuh"
+
+struct cpg_graph {
+    int device = 0;
+    int rank = 0, nranks = 1;
+    uint32_t n = 0, n_loc = 0, n_pad = 0, row0 = 0, max_degree = 0;
+    uint64_t nnz = 0, nnz_loc = 0, hash = 0;
+
+    int64_t* rowptr = nullptr;      // [n_loc+1]
+    uint32_t* col = nullptr;        // [nnz_loc]
+    uint32_t* gdeg = nullptr;       // [n_pad]
+    uint32_t* new_of_old = nullptr; // [n]
+
+    cpg::WorkItem* items = nullptr; // single-source items
+    uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0;
+    cpg::WorkItem* bitems = nullptr; // batched hub pieces
+    uint32_t n_bhubs = 0, n_bhub_items = 0;
+
+    double* hub_partial = nullptr;  // [n_hub_items]
+    unsigned int* hub_count = nullptr;  // [n_hubs]
+    double* bhub_partial = nullptr; // [n_bhub_items][64]
+    unsigned int* bhub_count = nullptr;
+
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    int sm_count = 0, step_grid = 0, batch_grid = 0;
+
+    // Query workspace (grown on demand, owned by the handle).
+    double* w_a = nullptr;
+    double* w_b = nullptr;
+    double* acc = nullptr;
+    double* full = nullptr;         // gathered final result (n_pad or n_pad*64)
+    size_t ws_cols = 0;             // 1 (single) or 64 (batched) currently sized for
+    double* d_coeffs = nullptr;
+    size_t coeff_cap = 0;
+    uint32_t* d_sources = nullptr;
+    size_t src_cap = 0;
+    double* d_mass_partial = nullptr;
+    size_t mass_cap = 0;
+    double* d_mass_err = nullptr;   // [2]: running max, scratch
+    double* d_step_mass = nullptr;  // [coeff_cap]
+    double* d_stage = nullptr;      // device result staging for host output (2 slots)
+    size_t stage_cap = 0;           // doubles per slot
+    // ev[0..1]: slot copied out; ev[2..3]: slot computed; ev[4]: caller-stream join
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+
+    void* nccl_comm = nullptr;      // ncclComm_t when sharded
+    std::mutex mu;                  // one query at a time per handle
+};
+
+namespace cpg {
+
+// graph_build.cu
+void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st);
+void ensure_batch_tables(cpg_graph* g);
+
+// step_kernels.cu
+void launch_step(const StepArgs& a, int grid, cudaStream_t st);
+int step_occupancy();
+void launch_batch(const BatchArgs& a, int grid, cudaStream_t st);
+int batch_occupancy();
+void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                        uint32_t q, cudaStream_t st);
+void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                              uint32_t q0, uint32_t count, cudaStream_t st);
+void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
+                       uint32_t n, cudaStream_t st);
+void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, cudaStream_t st);
+void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
+                            uint32_t count, cudaStream_t st);
+void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st);
+void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
+
+// nccl_dl.cpp
+void nccl_get_unique_id(void* out128);
+void* nccl_comm_init(const void* id128, int nranks, int rank);
+void nccl_allgather_f64(const double* send, double* recv, size_t count, void* comm, cudaStream_t st);
+void nccl_allreduce_sum_f64(const double* send, double* recv, size_t count, void* comm, cudaStream_t st);
+void nccl_comm_destroy(void* comm);
+
+} // namespace cpg

@@ -1,0 +1,78 @@
+// device_graph.cuh -- device-side graph layout and kernel parameter blocks.
+//
+// Layout in HBM (one handle = one GPU = one row shard):
+//   rows are relabelled by (degree desc, id asc) and dealt round-robin to the
+//   R ranks ("degree snake"), so rank r owns the contiguous global id range
+//   [r*n_loc, (r+1)*n_loc) and every rank gets ~n/R rows and ~nnz/R edges;
+//   within a rank rows stay degree-descending (hubs first: the most-gathered
+//   iterate entries share L2 lines).
+//   rowptr  int64 [n_loc+1]   local row offsets
+//   col     uint32[nnz_loc]   global (relabelled) neighbour ids, sorted per row
+//   gdeg    uint32[n_pad]     degree of every global id (0 for padding)
+//   new_of_old uint32[n]      caller id -> global id
+//   items   WorkItem[...]     hub pieces first, then row tiles (single-source)
+//   iterates: w_a, w_b fp64[n_pad] (replicated), acc fp64[n_loc]
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cpg {
+
+// Tile geometry of the single-source step (cheby_step_kernel).
+constexpr int kStepThreads = 256;
+constexpr int kTileEdges = 2048;                 // edges staged per tile (16 KB smem)
+constexpr int kTileChunk = kTileEdges / 2;       // rows with deg > chunk are hubs
+constexpr int kTileMaxRows = 2048;
+constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per thread)
+
+// Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
+constexpr int kBatchCols = 64;
+constexpr int kBatchThreads = 256;
+constexpr int kBatchHubEdges = 2048;             // rows above this are split
+
+// Work item.  Tile: {row_begin, row_end, 0, lg<<1}.  Hub piece:
+// {row, slot_base, piece, (hub<<1)|1}; pieces of one hub are consecutive
+// slots [slot_base, slot_base + P).
+struct WorkItem {
+    uint32_t a, b, c, info;
+};
+
+struct StepArgs {
+    const int64_t* rowptr;
+    const uint32_t* col;
+    const WorkItem* items;
+    const double* w_cur;   // gather source w_k (global ids, replicated)
+    double* w_io;          // in: w_{k-1}, out: w_{k+1} (global ids)
+    double* acc;           // local rows
+    double* out;           // final d*acc (local rows), used when last
+    double* hub_partial;   // per hub piece
+    unsigned int* hub_count;
+    double* mass_partial;  // [n_items] for this step
+    const double* coeffs;  // device copy of c_0..c_K
+    uint32_t row0;         // global id of local row 0
+    uint32_t n_items;
+    int k;                 // computing w_k (1..K)
+    int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
+    int last;              // write out = d * acc instead of acc
+};
+
+struct BatchArgs {
+    const int64_t* rowptr;
+    const uint32_t* col;
+    const WorkItem* hub_items;  // hub pieces (row, slot_base, piece, hub<<1|1)
+    uint32_t n_hub_items;
+    uint32_t hub_rows;          // rows [0, hub_rows) are hubs
+    uint32_t n_loc;
+    const double* w_cur;        // [n_pad][64]
+    double* w_io;               // [n_pad][64]
+    double* acc;                // [n_loc][64]
+    double* out;                // [n_loc][64] when last
+    double* hub_partial;        // [slots][64]
+    unsigned int* hub_count;
+    const double* coeffs;
+    uint32_t row0;
+    int k, first, last;
+};
+
+} // namespace cpg

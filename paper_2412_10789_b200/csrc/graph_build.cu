@@ -1,0 +1,281 @@
+// graph_build.cu -- CSR upload: degree-sorted relabel, row-shard extraction and
+// the load-balanced work tables.  One-time work per graph handle, off the timed
+// path (the reference's Graph::from_csr + inv_degree_, graph.cpp:48-104, is the
+// host analogue).  All of it runs on the device with CUB primitives.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "cpg_graph.hpp"
+
+namespace cpg {
+
+namespace {
+
+constexpr int kT = 256;
+
+inline int grid_for(uint64_t n, int cap = 148 * 16) {
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, cap)));
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+    T* p = nullptr;
+    CPG_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+    return p;
+}
+
+struct DevTemp {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b) {
+        if (b > bytes) {
+            if (p) cudaFree(p);
+            CPG_CUDA(cudaMalloc(&p, b));
+            bytes = b;
+        }
+    }
+    ~DevTemp() {
+        if (p) cudaFree(p);
+    }
+};
+
+__global__ void k_deg_ids(const uint64_t* off, uint32_t n, uint32_t* deg, uint32_t* ids) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        deg[v] = static_cast<uint32_t>(off[v + 1] - off[v]);
+        ids[v] = static_cast<uint32_t>(v);
+    }
+}
+
+// Position i of the degree order goes to rank i % R, local row i / R.
+__global__ void k_assign(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t n_loc,
+                         uint32_t* new_of_old, uint32_t* gdeg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = static_cast<uint32_t>((i % R) * n_loc + i / R);
+        new_of_old[order[i]] = g;
+        gdeg[g] = sdeg[i];
+    }
+}
+
+__global__ void k_local(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t rank,
+                        uint32_t n_loc, int64_t* ldeg, uint32_t* lold) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= n_loc; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = j * R + rank;
+        const bool real = j < n_loc && i < n;
+        ldeg[j] = real ? sdeg[i] : 0;
+        if (j < n_loc) lold[j] = real ? order[i] : 0xffffffffu;
+    }
+}
+
+// One warp per local row: relabelled neighbours keyed by (row, new id).
+__global__ void k_fill_keys(const int64_t* rowptr, const uint32_t* lold, const uint64_t* off, const uint32_t* nbr,
+                            const uint32_t* new_of_old, uint32_t n_loc, uint64_t* keys) {
+    const uint64_t lane = threadIdx.x & 31;
+    for (uint64_t j = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; j < n_loc;
+         j += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t old = lold[j];
+        if (old == 0xffffffffu) continue;
+        const uint64_t s = off[old], d = off[old + 1] - s;
+        const int64_t dst = rowptr[j];
+        for (uint64_t t = lane; t < d; t += 32)
+            keys[dst + t] = (j << 32) | new_of_old[nbr[s + t]];
+    }
+}
+
+__global__ void k_extract(const uint64_t* keys, uint64_t nnz, uint32_t* col) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz; e += (uint64_t)gridDim.x * blockDim.x)
+        col[e] = static_cast<uint32_t>(keys[e] & 0xffffffffu);
+}
+
+// Rows are degree-descending, so hubs are a prefix: count = last index with deg > thr, +1.
+__global__ void k_count_above(const int64_t* rowptr, uint32_t n_loc, int64_t thr, unsigned int* count) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc; j += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t d = rowptr[j + 1] - rowptr[j];
+        const int64_t dn = j + 1 < n_loc ? rowptr[j + 2] - rowptr[j + 1] : -1;
+        if (d > thr && dn <= thr) *count = static_cast<unsigned int>(j + 1);
+    }
+}
+
+__global__ void k_pieces(const int64_t* rowptr, uint32_t n_hub, int64_t piece, uint32_t* P) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= n_hub; j += gridDim.x * blockDim.x)
+        P[j] = j < n_hub ? static_cast<uint32_t>((rowptr[j + 1] - rowptr[j] + piece - 1) / piece) : 0u;
+}
+
+__global__ void k_hub_items(const uint32_t* P, const uint32_t* base, uint32_t n_hub, WorkItem* items) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5)
+        for (uint32_t p = lane; p < P[j]; p += 32) items[base[j] + p] = WorkItem{j, base[j], p, (j << 1) | 1u};
+}
+
+__global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, uint8_t* flags) {
+    for (uint64_t j = first + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        bool start = (j == first) || ((j - first) % kTileMaxRows == 0) ||
+                     (rowptr[j] / kTileChunk != rowptr[j - 1] / kTileChunk);
+        flags[j - first] = start ? 1 : 0;
+    }
+}
+
+__global__ void k_tile_items(const int64_t* rowptr, const uint32_t* starts, uint32_t n_tiles, uint32_t n_loc,
+                             WorkItem* items) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
+        const uint32_t rb = starts[t];
+        const uint32_t re = t + 1 < n_tiles ? starts[t + 1] : n_loc;
+        const int64_t edges = rowptr[re] - rowptr[rb];
+        const double avg = static_cast<double>(edges) / static_cast<double>(re - rb);
+        int lg = 0;
+        while (lg < 5 && static_cast<double>(2 << lg) <= avg / 2.0) ++lg;  // g <= mean/2
+        items[t] = WorkItem{rb, re, 0u, static_cast<uint32_t>(lg) << 1};
+    }
+}
+
+// Builds hub-piece items for rows with degree > thr (pieces of `piece` edges).
+// Returns (n_hub, n_items); items written to *out (allocated here).
+void build_hub_items(const int64_t* rowptr, uint32_t n_loc, int64_t thr, int64_t piece, WorkItem** out,
+                     uint32_t* n_hub_out, uint32_t* n_items_out, uint32_t reserve_tail, cudaStream_t st) {
+    unsigned int* d_cnt = dalloc<unsigned int>(1);
+    CPG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned int), st));
+    if (n_loc) k_count_above<<<grid_for(n_loc), kT, 0, st>>>(rowptr, n_loc, thr, d_cnt);
+    unsigned int n_hub = 0;
+    CPG_CUDA(cudaMemcpyAsync(&n_hub, d_cnt, sizeof(n_hub), cudaMemcpyDeviceToHost, st));
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_cnt);
+    uint32_t* P = dalloc<uint32_t>(n_hub + 1);
+    uint32_t* base = dalloc<uint32_t>(n_hub + 1);
+    k_pieces<<<grid_for(n_hub + 1), kT, 0, st>>>(rowptr, n_hub, piece, P);
+    DevTemp tmp;
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, P, base, n_hub + 1, st);
+    tmp.ensure(bytes);
+    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, P, base, n_hub + 1, st));
+    uint32_t total = 0;
+    CPG_CUDA(cudaMemcpyAsync(&total, base + n_hub, sizeof(total), cudaMemcpyDeviceToHost, st));
+    CPG_CUDA(cudaStreamSynchronize(st));
+    WorkItem* items = dalloc<WorkItem>(static_cast<size_t>(total) + reserve_tail);
+    if (n_hub) k_hub_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(P, base, n_hub, items);
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(P);
+    cudaFree(base);
+    *out = items;
+    *n_hub_out = n_hub;
+    *n_items_out = total;
+}
+
+} // namespace
+
+void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st) {
+    const uint32_t n = g->n;
+    const uint32_t R = static_cast<uint32_t>(g->nranks);
+    const uint32_t rank = static_cast<uint32_t>(g->rank);
+    g->n_loc = (n + R - 1) / R;
+    g->n_pad = g->n_loc * R;
+    g->row0 = rank * g->n_loc;
+    const uint32_t n_loc = g->n_loc;
+    DevTemp tmp;
+    size_t bytes = 0;
+
+    // 1. degree order: (degree desc, id asc) -- radix sort is stable.
+    uint32_t* deg = dalloc<uint32_t>(n);
+    uint32_t* ids = dalloc<uint32_t>(n);
+    uint32_t* sdeg = dalloc<uint32_t>(n);
+    uint32_t* order = dalloc<uint32_t>(n);
+    k_deg_ids<<<grid_for(n), kT, 0, st>>>(d_off, n, deg, ids);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, deg, sdeg, ids, order, n, 0, 32, st);
+    tmp.ensure(bytes);
+    CPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, deg, sdeg, ids, order, n, 0, 32, st));
+    CPG_CUDA(cudaMemcpyAsync(&g->max_degree, sdeg, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    cudaFree(deg);
+    cudaFree(ids);
+
+    // 2. relabel + shard assignment.
+    g->new_of_old = dalloc<uint32_t>(n);
+    g->gdeg = dalloc<uint32_t>(g->n_pad);
+    CPG_CUDA(cudaMemsetAsync(g->gdeg, 0, sizeof(uint32_t) * g->n_pad, st));
+    k_assign<<<grid_for(n), kT, 0, st>>>(order, sdeg, n, R, n_loc, g->new_of_old, g->gdeg);
+    int64_t* ldeg = dalloc<int64_t>(static_cast<size_t>(n_loc) + 1);
+    uint32_t* lold = dalloc<uint32_t>(n_loc);
+    k_local<<<grid_for(static_cast<uint64_t>(n_loc) + 1), kT, 0, st>>>(order, sdeg, n, R, rank, n_loc, ldeg, lold);
+    cudaFree(sdeg);
+    cudaFree(order);
+
+    // 3. local row pointers.
+    g->rowptr = dalloc<int64_t>(static_cast<size_t>(n_loc) + 1);
+    bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, ldeg, g->rowptr, n_loc + 1, st);
+    tmp.ensure(bytes);
+    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, ldeg, g->rowptr, n_loc + 1, st));
+    int64_t nnz_loc = 0;
+    CPG_CUDA(cudaMemcpyAsync(&nnz_loc, g->rowptr + n_loc, sizeof(nnz_loc), cudaMemcpyDeviceToHost, st));
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(ldeg);
+    g->nnz_loc = static_cast<uint64_t>(nnz_loc);
+
+    // 4. relabelled column ids, sorted within each row (64-bit (row,col) radix sort).
+    {
+        uint64_t* keys = dalloc<uint64_t>(g->nnz_loc);
+        uint64_t* keys_sorted = dalloc<uint64_t>(g->nnz_loc);
+        k_fill_keys<<<grid_for(static_cast<uint64_t>(n_loc) * 32), kT, 0, st>>>(g->rowptr, lold, d_off, d_nbr,
+                                                                                 g->new_of_old, n_loc, keys);
+        int row_bits = 1;
+        while (row_bits < 32 && (1ull << row_bits) < n_loc) ++row_bits;
+        bytes = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, keys_sorted, g->nnz_loc, 0, 32 + row_bits, st);
+        tmp.ensure(bytes);
+        CPG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, keys, keys_sorted, g->nnz_loc, 0, 32 + row_bits, st));
+        cudaFree(keys);
+        g->col = dalloc<uint32_t>(g->nnz_loc);
+        k_extract<<<grid_for(g->nnz_loc), kT, 0, st>>>(keys_sorted, g->nnz_loc, g->col);
+        CPG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(keys_sorted);
+    }
+    cudaFree(lold);
+
+    // 5. single-source work table: hub pieces, then row tiles.
+    WorkItem* hub_items = nullptr;
+    uint32_t n_hub = 0, n_hub_items = 0;
+    build_hub_items(g->rowptr, n_loc, kTileChunk, kHubPieceEdges, &hub_items, &n_hub, &n_hub_items, 0, st);
+    uint32_t n_tiles = 0;
+    uint32_t* starts = nullptr;
+    if (n_hub < n_loc) {
+        const uint32_t rows = n_loc - n_hub;
+        uint8_t* flags = dalloc<uint8_t>(rows);
+        starts = dalloc<uint32_t>(rows);
+        unsigned int* d_sel = dalloc<unsigned int>(1);
+        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(g->rowptr, n_hub, n_loc, flags);
+        cub::CountingInputIterator<uint32_t> it(n_hub);
+        bytes = 0;
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);
+        tmp.ensure(bytes);
+        CPG_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, starts, d_sel, rows, st));
+        CPG_CUDA(cudaMemcpyAsync(&n_tiles, d_sel, sizeof(n_tiles), cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(flags);
+        cudaFree(d_sel);
+    }
+    g->n_hubs = n_hub;
+    g->n_hub_items = n_hub_items;
+    g->n_tiles = n_tiles;
+    g->n_items = n_hub_items + n_tiles;
+    g->items = dalloc<WorkItem>(g->n_items);
+    if (n_hub_items)
+        CPG_CUDA(cudaMemcpyAsync(g->items, hub_items, sizeof(WorkItem) * n_hub_items, cudaMemcpyDeviceToDevice, st));
+    if (n_tiles)
+        k_tile_items<<<grid_for(n_tiles), kT, 0, st>>>(g->rowptr, starts, n_tiles, n_loc, g->items + n_hub_items);
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(hub_items);
+    if (starts) cudaFree(starts);
+    CPG_CUDA(cudaGetLastError());
+}
+
+void ensure_batch_tables(cpg_graph* g) {
+    if (g->bitems) return;
+    uint32_t n_hub = 0, n_items = 0;
+    build_hub_items(g->rowptr, g->n_loc, kBatchHubEdges, kBatchHubEdges, &g->bitems, &n_hub, &n_items, 0, g->stream);
+    g->n_bhubs = n_hub;
+    g->n_bhub_items = n_items;
+    CPG_CUDA(cudaGetLastError());
+}
+
+} // namespace cpg

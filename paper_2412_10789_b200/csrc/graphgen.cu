@@ -1,0 +1,320 @@
+// graphgen.cu -- seeded synthetic inputs for the parity tests and the bench
+// (stand-ins for the paper's SNAP datasets).  Not the hot path.
+//
+// Every edge draw is addressed by its sample index i through
+// SplitMix64::stream(seed, i) (include/chebyprop/rng.hpp:30-35 semantics), so
+// the host build (device = -1) and the device build produce the same CSR:
+// both symmetrise, drop self-loops, sort, deduplicate and compact isolated ids
+// in ascending order -- the invariants Graph::from_csr demands
+// (graph.cpp:48-104).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "cpg_common.hpp"
+
+namespace cpg {
+namespace {
+
+__host__ __device__ __forceinline__ uint64_t sm_next(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ double sm_double(uint64_t& s) {
+    return static_cast<double>(sm_next(s) >> 11) * 0x1.0p-53;
+}
+__host__ __device__ __forceinline__ uint64_t sm_stream(uint64_t seed, uint64_t tag) {
+    uint64_t s = seed ^ (0x9e3779b97f4a7c15ull * (tag + 1));
+    sm_next(s);
+    return s;
+}
+
+constexpr uint64_t kLoop = ~0ull;  // self-loop sentinel (sorts last)
+
+// R-MAT: per level pick a quadrant with probabilities (a, b, c, d).
+__host__ __device__ __forceinline__ void rmat_pair(uint64_t seed, uint64_t i, uint32_t scale, double a, double ab,
+                                                   double abc, uint64_t& k1, uint64_t& k2) {
+    uint64_t s = sm_stream(seed, i);
+    uint32_t u = 0, v = 0;
+    for (uint32_t l = 0; l < scale; ++l) {
+        const double r = sm_double(s);
+        const uint32_t bu = r >= ab ? 1u : 0u;
+        const uint32_t bv = (r >= a && r < ab) || r >= abc ? 1u : 0u;
+        u = (u << 1) | bu;
+        v = (v << 1) | bv;
+    }
+    if (u == v) {
+        k1 = k2 = kLoop;
+    } else {
+        k1 = (static_cast<uint64_t>(u) << 32) | v;
+        k2 = (static_cast<uint64_t>(v) << 32) | u;
+    }
+}
+
+// Chung-Lu: both endpoints drawn proportionally to w (inverse CDF search).
+__host__ __device__ __forceinline__ uint32_t cdf_search(const double* cdf, uint32_t n, double x) {
+    uint32_t lo = 0, hi = n - 1;  // first i with cdf[i] > x
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+__host__ __device__ __forceinline__ void chunglu_pair(uint64_t seed, uint64_t i, const double* cdf, uint32_t n,
+                                                      uint64_t& k1, uint64_t& k2) {
+    uint64_t s = sm_stream(seed, i);
+    const double total = cdf[n - 1];
+    const uint32_t u = cdf_search(cdf, n, sm_double(s) * total);
+    const uint32_t v = cdf_search(cdf, n, sm_double(s) * total);
+    if (u == v) {
+        k1 = k2 = kLoop;
+    } else {
+        k1 = (static_cast<uint64_t>(u) << 32) | v;
+        k2 = (static_cast<uint64_t>(v) << 32) | u;
+    }
+}
+
+__global__ void k_rmat(uint64_t seed, uint64_t m, uint32_t scale, double a, double ab, double abc, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        rmat_pair(seed, i, scale, a, ab, abc, keys[2 * i], keys[2 * i + 1]);
+}
+
+__global__ void k_chunglu(uint64_t seed, uint64_t m, const double* cdf, uint32_t n, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        chunglu_pair(seed, i, cdf, n, keys[2 * i], keys[2 * i + 1]);
+}
+
+__global__ void k_mark(const uint64_t* keys, uint64_t nnz, uint32_t* present) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz; e += (uint64_t)gridDim.x * blockDim.x)
+        present[keys[e] >> 32] = 1u;
+}
+
+__global__ void k_csr(const uint64_t* keys, uint64_t nnz, const uint32_t* newid, uint64_t* off, uint32_t* nbr,
+                      uint32_t n) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = static_cast<uint32_t>(keys[e] >> 32);
+        nbr[e] = newid[static_cast<uint32_t>(keys[e] & 0xffffffffu)];
+        if (e == 0 || (keys[e - 1] >> 32) != u) off[newid[u]] = e;
+        if (e == 0) off[n] = nnz;
+    }
+}
+
+int grid_for(uint64_t n) { return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 32))); }
+
+// Shared tail: keys (2m, unsorted) -> CSR.  Device path.
+void keys_to_csr_device(uint64_t* keys, uint64_t nk, uint32_t id_space, uint32_t id_bits, uint64_t** off_out,
+                        uint32_t** nbr_out, uint32_t* n_out, uint64_t* nnz_out) {
+    cudaStream_t st = 0;
+    uint64_t* sorted = nullptr;
+    CPG_CUDA(cudaMalloc(&sorted, nk * sizeof(uint64_t)));
+    void* tmp = nullptr;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, sorted, nk, 0, 64, st);
+    CPG_CUDA(cudaMalloc(&tmp, bytes));
+    CPG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, keys, sorted, nk, 0, 64, st));
+    cudaFree(tmp);
+    uint64_t* d_cnt = nullptr;
+    CPG_CUDA(cudaMalloc(&d_cnt, sizeof(uint64_t)));
+    bytes = 0;
+    cub::DeviceSelect::Unique(nullptr, bytes, sorted, keys, d_cnt, nk, st);
+    CPG_CUDA(cudaMalloc(&tmp, bytes));
+    CPG_CUDA(cub::DeviceSelect::Unique(tmp, bytes, sorted, keys, d_cnt, nk, st));
+    cudaFree(tmp);
+    cudaFree(sorted);
+    uint64_t nu = 0, last = 0;
+    CPG_CUDA(cudaMemcpy(&nu, d_cnt, sizeof(nu), cudaMemcpyDeviceToHost));
+    cudaFree(d_cnt);
+    if (nu) CPG_CUDA(cudaMemcpy(&last, keys + nu - 1, sizeof(last), cudaMemcpyDeviceToHost));
+    if (nu && last == kLoop) --nu;
+    require(nu > 0, "generator produced an empty graph");
+    uint32_t *present = nullptr, *newid = nullptr;
+    CPG_CUDA(cudaMalloc(&present, (static_cast<size_t>(id_space) + 1) * sizeof(uint32_t)));
+    CPG_CUDA(cudaMalloc(&newid, (static_cast<size_t>(id_space) + 1) * sizeof(uint32_t)));
+    CPG_CUDA(cudaMemset(present, 0, (static_cast<size_t>(id_space) + 1) * sizeof(uint32_t)));
+    k_mark<<<grid_for(nu), 256, 0, st>>>(keys, nu, present);
+    bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, present, newid, id_space + 1, st);
+    CPG_CUDA(cudaMalloc(&tmp, bytes));
+    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, present, newid, id_space + 1, st));
+    cudaFree(tmp);
+    uint32_t n = 0;
+    CPG_CUDA(cudaMemcpy(&n, newid + id_space, sizeof(n), cudaMemcpyDeviceToHost));
+    uint64_t* off = nullptr;
+    uint32_t* nbr = nullptr;
+    CPG_CUDA(cudaMalloc(&off, (static_cast<size_t>(n) + 1) * sizeof(uint64_t)));
+    CPG_CUDA(cudaMalloc(&nbr, nu * sizeof(uint32_t)));
+    k_csr<<<grid_for(nu), 256, 0, st>>>(keys, nu, newid, off, nbr, n);
+    CPG_CUDA(cudaDeviceSynchronize());
+    CPG_CUDA(cudaGetLastError());
+    cudaFree(present);
+    cudaFree(newid);
+    (void)id_bits;
+    *off_out = off;
+    *nbr_out = nbr;
+    *n_out = n;
+    *nnz_out = nu;
+}
+
+// Host path (tests / small graphs): identical keys -> identical CSR.
+void keys_to_csr_host(std::vector<uint64_t>& keys, uint32_t id_space, uint64_t** off_out, uint32_t** nbr_out,
+                      uint32_t* n_out, uint64_t* nnz_out) {
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    if (!keys.empty() && keys.back() == kLoop) keys.pop_back();
+    require(!keys.empty(), "generator produced an empty graph");
+    std::vector<uint32_t> newid(static_cast<size_t>(id_space) + 1, 0);
+    for (uint64_t k : keys) newid[k >> 32] = 1;
+    uint32_t n = 0;
+    for (size_t i = 0; i <= id_space; ++i) {
+        const uint32_t p = newid[i];
+        newid[i] = n;
+        n += p;
+    }
+    const uint64_t nnz = keys.size();
+    auto* off = static_cast<uint64_t*>(std::malloc((static_cast<size_t>(n) + 1) * sizeof(uint64_t)));
+    auto* nbr = static_cast<uint32_t*>(std::malloc(std::max<uint64_t>(1, nnz) * sizeof(uint32_t)));
+    if (!off || !nbr) fail(CPG_ENOMEM, "host generator out of memory");
+    for (uint64_t e = 0; e < nnz; ++e) {
+        const uint32_t u = static_cast<uint32_t>(keys[e] >> 32);
+        nbr[e] = newid[static_cast<uint32_t>(keys[e] & 0xffffffffu)];
+        if (e == 0 || (keys[e - 1] >> 32) != u) off[newid[u]] = e;
+    }
+    off[n] = nnz;
+    *off_out = off;
+    *nbr_out = nbr;
+    *n_out = n;
+    *nnz_out = nnz;
+}
+
+template <typename F>
+void host_fill(std::vector<uint64_t>& keys, uint64_t m, F&& pair) {
+    keys.resize(2 * m);
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (uint64_t i = t; i < m; i += nt) pair(i, keys[2 * i], keys[2 * i + 1]);
+        });
+    for (auto& x : th) x.join();
+}
+
+// Expected-degree weights w_i ~ (i + 1)^(-1/(gamma-1)), scaled to the target
+// mean degree with the cap enforced (a few rescale rounds), as a CDF.
+std::vector<double> chunglu_cdf(uint32_t n, double exponent, double mean_degree, uint32_t max_degree) {
+    require(exponent > 1.0, "chung-lu exponent must exceed 1");
+    std::vector<double> w(n);
+    const double beta = 1.0 / (exponent - 1.0);
+    for (uint32_t i = 0; i < n; ++i) w[i] = std::pow(static_cast<double>(i) + 1.0, -beta);
+    const double target = mean_degree * n;
+    for (int round = 0; round < 50; ++round) {
+        double sum = 0.0;
+        for (double x : w) sum += x;
+        const double s = target / sum;
+        bool capped = false;
+        for (double& x : w) {
+            x *= s;
+            if (max_degree && x > max_degree) {
+                x = max_degree;
+                capped = true;
+            }
+        }
+        if (!capped) break;
+    }
+    std::vector<double> cdf(n);
+    double acc = 0.0;
+    for (uint32_t i = 0; i < n; ++i) cdf[i] = (acc += w[i]);
+    return cdf;
+}
+
+} // namespace
+} // namespace cpg
+
+using namespace cpg;
+
+extern "C" {
+
+int cpg_gen_rmat(uint32_t scale, uint64_t n_samples, double a, double b, double c, uint64_t seed, int device,
+                 uint64_t** offsets, uint32_t** neighbors, uint32_t* n, uint64_t* nnz) {
+    return guarded([&] {
+        require(scale >= 1 && scale <= 31, "rmat scale must be in [1, 31]");
+        require(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0, "rmat probabilities");
+        require(offsets && neighbors && n && nnz, "null argument");
+        const double ab = a + b, abc = a + b + c;
+        const uint32_t ids = 1u << scale;
+        if (device < 0) {
+            std::vector<uint64_t> keys;
+            host_fill(keys, n_samples, [&](uint64_t i, uint64_t& k1, uint64_t& k2) {
+                rmat_pair(seed, i, scale, a, ab, abc, k1, k2);
+            });
+            keys_to_csr_host(keys, ids, offsets, neighbors, n, nnz);
+            return;
+        }
+        CPG_CUDA(cudaSetDevice(device));
+        uint64_t* keys = nullptr;
+        CPG_CUDA(cudaMalloc(&keys, 2 * n_samples * sizeof(uint64_t)));
+        k_rmat<<<grid_for(n_samples), 256>>>(seed, n_samples, scale, a, ab, abc, keys);
+        CPG_CUDA(cudaGetLastError());
+        try {
+            keys_to_csr_device(keys, 2 * n_samples, ids, scale, offsets, neighbors, n, nnz);
+        } catch (...) {
+            cudaFree(keys);
+            throw;
+        }
+        cudaFree(keys);
+    });
+}
+
+int cpg_gen_chunglu(uint32_t n_ids, uint64_t n_samples, double exponent, double mean_degree, uint32_t max_degree,
+                    uint64_t seed, int device, uint64_t** offsets, uint32_t** neighbors, uint32_t* n, uint64_t* nnz) {
+    return guarded([&] {
+        require(n_ids >= 2, "chung-lu needs at least two ids");
+        require(offsets && neighbors && n && nnz, "null argument");
+        const std::vector<double> cdf = chunglu_cdf(n_ids, exponent, mean_degree, max_degree);
+        if (device < 0) {
+            std::vector<uint64_t> keys;
+            host_fill(keys, n_samples, [&](uint64_t i, uint64_t& k1, uint64_t& k2) {
+                chunglu_pair(seed, i, cdf.data(), n_ids, k1, k2);
+            });
+            keys_to_csr_host(keys, n_ids, offsets, neighbors, n, nnz);
+            return;
+        }
+        CPG_CUDA(cudaSetDevice(device));
+        double* d_cdf = nullptr;
+        uint64_t* keys = nullptr;
+        CPG_CUDA(cudaMalloc(&d_cdf, n_ids * sizeof(double)));
+        CPG_CUDA(cudaMemcpy(d_cdf, cdf.data(), n_ids * sizeof(double), cudaMemcpyHostToDevice));
+        CPG_CUDA(cudaMalloc(&keys, 2 * n_samples * sizeof(uint64_t)));
+        k_chunglu<<<grid_for(n_samples), 256>>>(seed, n_samples, d_cdf, n_ids, keys);
+        CPG_CUDA(cudaGetLastError());
+        cudaFree(d_cdf);
+        try {
+            keys_to_csr_device(keys, 2 * n_samples, n_ids, 32, offsets, neighbors, n, nnz);
+        } catch (...) {
+            cudaFree(keys);
+            throw;
+        }
+        cudaFree(keys);
+    });
+}
+
+int cpg_free_csr(uint64_t* offsets, uint32_t* neighbors, int device) {
+    return guarded([&] {
+        if (device < 0) {
+            std::free(offsets);
+            std::free(neighbors);
+        } else {
+            CPG_CUDA(cudaSetDevice(device));
+            if (offsets) CPG_CUDA(cudaFree(offsets));
+            if (neighbors) CPG_CUDA(cudaFree(neighbors));
+        }
+    });
+}
+
+} // extern "C"

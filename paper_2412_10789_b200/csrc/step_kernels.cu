@@ -1,0 +1,422 @@
+// step_kernels.cu -- the hot path: one fused Chebyshev step per launch.
+//
+// Replaces, per step, the reference's scatter SpMV apply_walk_into
+// (graph.cpp:257-267) plus the two dense passes around it in cheby_power_vec
+// (solvers.cpp:218 accumulate, :221 recurrence, :222 swap) with ONE pull-SpMV
+// kernel in the D^-1-scaled basis  w_k = D^-1 T_k(P) s :
+//
+//   y(v)      = sum_{u in N(v)} w_k(u)                  (pattern-only A, 4 B index + 8 B gather)
+//   w_{k+1}(v)= 2 y(v)/d_v - w_{k-1}(v)                 (in place over w_{k-1})
+//   acc(v)   += c_{k+1} w_{k+1}(v)                      (acc = D^-1 yhat)
+//   mass     += d_v w_{k+1}(v)                          (= sum T_{k+1}, checks C13)
+//   last step: out(v) = d_v acc(v)                      (= yhat, solvers.cpp:225)
+//
+// Load balance for power-law degrees (rows are degree-sorted at upload):
+//   * row tiles: <= 2048 edges; indices streamed coalesced (L1 no-allocate),
+//     gathered values staged in shared memory, then each row reduced by a
+//     power-of-two lane group sized to the tile's mean degree;
+//   * hub rows (deg > 1024): split into 4096-edge pieces, one CTA each; the
+//     last-arriving piece (device-scope atomic ticket) sums the piece partials
+//     in piece order and runs the epilogue.
+// Every reduction has a fixed order, so results are bit-reproducible run to
+// run (no floating-point atomics).
+#include <cuda_runtime.h>
+
+#include "device_graph.cuh"
+
+namespace cpg {
+
+__device__ __forceinline__ uint32_t ld_index(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ double ld_gather(const double* p) { return __ldg(p); }
+
+__device__ __forceinline__ double2 ld_gather2(const double* p) {
+    return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// Deterministic CTA sum: xor butterfly per warp, warp partials summed in warp
+// order by thread 0.  Result valid in thread 0 only.
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < THREADS / 32; ++i) s += red[i];
+    }
+    return s;
+}
+
+// Recurrence + accumulation + mass for local row r with neighbour sum y.
+__device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, double y, int64_t d,
+                                              double& mass) {
+    const uint32_t gr = a.row0 + r;
+    double w_new = 0.0, acc_new = 0.0;
+    if (d > 0) {
+        const double dd = static_cast<double>(d);
+        if (a.first) {
+            w_new = y / dd;  // w_1 = D^-1 A w_0   (T_1 = P T_0, solvers.cpp:212)
+            acc_new = a.coeffs[0] * a.w_cur[gr] + a.coeffs[1] * w_new;
+        } else {
+            w_new = 2.0 * y / dd - a.w_io[gr];  // solvers.cpp:221
+            acc_new = a.acc[r] + a.coeffs[a.k] * w_new;  // solvers.cpp:218 (for k+1)
+        }
+        mass += dd * w_new;
+    }
+    a.w_io[gr] = w_new;
+    if (a.last)
+        a.out[r] = static_cast<double>(d) * acc_new;
+    else
+        a.acc[r] = acc_new;
+}
+
+template <int THREADS, int TILE>
+__device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, double* vals,
+                                             double& mass) {
+    constexpr int PER = TILE / THREADS;
+    const uint32_t rb = it.a, re = it.b;
+    const int lg = (it.info >> 1) & 7;
+    const int64_t e0 = a.rowptr[rb];
+    const int cnt = static_cast<int>(a.rowptr[re] - e0);
+    const uint32_t* colp = a.col + e0;
+
+    // Phase 1: coalesced index stream, independent gathers (PER in flight per thread).
+    uint32_t idx[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int j = i * THREADS + threadIdx.x;
+        idx[i] = j < cnt ? ld_index(colp + j) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int j = i * THREADS + threadIdx.x;
+        if (j < cnt) vals[j] = ld_gather(a.w_cur + idx[i]);
+    }
+    __syncthreads();
+
+    // Phase 2: per-row reduction by lane groups of g = 2^lg, then epilogue.
+    const int g = 1 << lg;
+    const int sub = threadIdx.x & (g - 1);
+    const int grp = threadIdx.x >> lg;
+    const int ngrp = THREADS >> lg;
+    const uint32_t nrows = re - rb;
+    for (uint32_t base = 0; base < nrows; base += ngrp) {
+        const uint32_t r = rb + base + grp;
+        double s = 0.0;
+        int64_t d = 0;
+        if (r < re) {
+            const int64_t rs = a.rowptr[r];
+            d = a.rowptr[r + 1] - rs;
+            const double* v = vals + (rs - e0);
+            for (int j = sub; j < d; j += g) s += v[j];
+        }
+        for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (r < re && sub == 0) step_epilogue(a, r, s, d, mass);
+    }
+    __syncthreads();  // vals is reused by the next item
+}
+
+template <int THREADS>
+__device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it, double* red,
+                                            int* flag, double& mass) {
+    constexpr int PER = kHubPieceEdges / THREADS;
+    const uint32_t r = it.a, slot_base = it.b, piece = it.c, hub = it.info >> 1;
+    const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
+    const int64_t d = re - rs;
+    const int64_t p0 = rs + static_cast<int64_t>(piece) * kHubPieceEdges;
+    const int64_t p1 = min(p0 + kHubPieceEdges, re);
+    const uint32_t P = static_cast<uint32_t>((d + kHubPieceEdges - 1) / kHubPieceEdges);
+
+    uint32_t idx[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int64_t e = p0 + i * THREADS + threadIdx.x;
+        idx[i] = e < p1 ? ld_index(a.col + e) : 0u;
+    }
+    double vals[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int64_t e = p0 + i * THREADS + threadIdx.x;
+        vals[i] = e < p1 ? ld_gather(a.w_cur + idx[i]) : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) s += vals[i];
+    s = block_sum<THREADS>(s, red);
+
+    if (P == 1) {
+        if (threadIdx.x == 0) step_epilogue(a, r, s, d, mass);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        a.hub_partial[slot_base + piece] = s;
+        __threadfence();
+        const unsigned prev = atomicAdd(&a.hub_count[hub], 1u);
+        *flag = (prev == P - 1);
+    }
+    __syncthreads();
+    if (*flag && threadIdx.x < 32) {  // last piece: ordered sum of the P partials
+        __threadfence();
+        double y = 0.0;
+        for (uint32_t p = threadIdx.x; p < P; p += 32) y += __ldcg(a.hub_partial + slot_base + p);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+        if (threadIdx.x == 0) {
+            a.hub_count[hub] = 0u;  // re-arm for the next step
+            step_epilogue(a, r, y, d, mass);
+        }
+    }
+    __syncthreads();
+}
+
+template <int THREADS, int TILE>
+__global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
+    __shared__ double vals[TILE];
+    __shared__ double red[THREADS / 32];
+    __shared__ int flag;
+    double mass = 0.0;
+    for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+        const WorkItem it = a.items[i];
+        if (it.info & 1u)
+            process_hub<THREADS>(a, it, red, &flag, mass);
+        else
+            process_tile<THREADS, TILE>(a, it, vals, mass);
+    }
+    mass = block_sum<THREADS>(mass, red);
+    if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
+}
+
+// ---------------------------------------------------------------------------
+// Batched step: 64 sources per tile, iterate rows [n_pad][64] fp64 row-major.
+// One warp per row job; each lane owns two columns (one double2 per gathered
+// 512-B row).  Rows above kBatchHubEdges are split into pieces with the same
+// ordered last-arriver reduction.  Edge order within a row is sequential, so
+// each column is bit-identical to a single-source run with the same sum order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d,
+                                               int lane) {
+    const uint32_t gr = a.row0 + r;
+    double2* wio = reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * kBatchCols) + lane;
+    double2* accp = reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * kBatchCols) + lane;
+    double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
+    if (d > 0) {
+        const double dd = static_cast<double>(d);
+        if (a.first) {
+            const double2 w0 =
+                reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * kBatchCols)[lane];
+            w_new.x = y.x / dd;
+            w_new.y = y.y / dd;
+            acc_new.x = a.coeffs[0] * w0.x + a.coeffs[1] * w_new.x;
+            acc_new.y = a.coeffs[0] * w0.y + a.coeffs[1] * w_new.y;
+        } else {
+            const double2 wp = *wio;
+            const double2 ac = *accp;
+            const double ck = a.coeffs[a.k];
+            w_new.x = 2.0 * y.x / dd - wp.x;
+            w_new.y = 2.0 * y.y / dd - wp.y;
+            acc_new.x = ac.x + ck * w_new.x;
+            acc_new.y = ac.y + ck * w_new.y;
+        }
+    }
+    *wio = w_new;
+    if (a.last) {
+        const double dd = static_cast<double>(d);
+        reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * kBatchCols)[lane] =
+            make_double2(dd * acc_new.x, dd * acc_new.y);
+    } else {
+        *accp = acc_new;
+    }
+}
+
+__device__ __forceinline__ double2 batch_row_sum(const BatchArgs& a, int64_t e0, int64_t e1, int lane) {
+    constexpr int U = 8;
+    double2 s = {0.0, 0.0};
+    for (int64_t base = e0; base < e1; base += 32) {
+        const int m = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
+        const uint32_t c = lane < m ? ld_index(a.col + base + lane) : 0u;
+        int j = 0;
+        for (; j + U <= m; j += U) {
+            double2 v[U];
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                const uint32_t u = __shfl_sync(0xffffffffu, c, j + t);
+                v[t] = ld_gather2(a.w_cur + static_cast<size_t>(u) * kBatchCols + 2 * lane);
+            }
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                s.x += v[t].x;
+                s.y += v[t].y;
+            }
+        }
+        for (; j < m; ++j) {
+            const uint32_t u = __shfl_sync(0xffffffffu, c, j);
+            const double2 v = ld_gather2(a.w_cur + static_cast<size_t>(u) * kBatchCols + 2 * lane);
+            s.x += v.x;
+            s.y += v.y;
+        }
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(kBatchThreads) cheby_batch_kernel(const BatchArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_jobs = a.n_hub_items + (a.n_loc - a.hub_rows);
+    for (uint32_t job = wg; job < n_jobs; job += nw) {
+        if (job < a.n_hub_items) {
+            const WorkItem it = a.hub_items[job];
+            const uint32_t r = it.a, slot_base = it.b, piece = it.c, hub = it.info >> 1;
+            const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
+            const int64_t d = re - rs;
+            const int64_t p0 = rs + static_cast<int64_t>(piece) * kBatchHubEdges;
+            const int64_t p1 = min(p0 + kBatchHubEdges, re);
+            const uint32_t P = static_cast<uint32_t>((d + kBatchHubEdges - 1) / kBatchHubEdges);
+            const double2 s = batch_row_sum(a, p0, p1, lane);
+            reinterpret_cast<double2*>(a.hub_partial +
+                                       static_cast<size_t>(slot_base + piece) * kBatchCols)[lane] = s;
+            __threadfence();
+            __syncwarp();
+            unsigned prev = 0;
+            if (lane == 0) prev = atomicAdd(&a.hub_count[hub], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == P - 1) {
+                __threadfence();
+                double2 y = {0.0, 0.0};
+                for (uint32_t p = 0; p < P; ++p) {
+                    const double2 v = __ldcg(reinterpret_cast<const double2*>(
+                                                 a.hub_partial + static_cast<size_t>(slot_base + p) * kBatchCols) +
+                                             lane);
+                    y.x += v.x;
+                    y.y += v.y;
+                }
+                if (lane == 0) a.hub_count[hub] = 0u;
+                batch_epilogue(a, r, y, d, lane);
+            }
+        } else {
+            const uint32_t r = a.hub_rows + (job - a.n_hub_items);
+            const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
+            const double2 s = batch_row_sum(a, rs, re, lane);
+            batch_epilogue(a, r, s, re - rs, lane);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Small kernels around the steps.
+// ---------------------------------------------------------------------------
+
+// w_0 = D^-1 e_s in the global (relabelled) ids; vector pre-zeroed.
+__global__ void init_onehot_kernel(double* w, const uint32_t* gdeg, const uint32_t* new_of_old,
+                                   const uint32_t* sources, uint32_t q) {
+    const uint32_t s = new_of_old[sources[q]];
+    w[s] = 1.0 / static_cast<double>(gdeg[s]);
+}
+
+// Batched: column j of W_0 = D^-1 e_{s_j}; matrix pre-zeroed.
+__global__ void init_onehot_batch_kernel(double* W, const uint32_t* gdeg, const uint32_t* new_of_old,
+                                         const uint32_t* sources, uint32_t q0, uint32_t count) {
+    const uint32_t j = threadIdx.x;
+    if (j < count) {
+        const uint32_t s = new_of_old[sources[q0 + j]];
+        W[static_cast<size_t>(s) * kBatchCols + j] = 1.0 / static_cast<double>(gdeg[s]);
+    }
+}
+
+// w_0 = D^-1 seed for a dense seed given in caller ids.
+__global__ void init_dense_kernel(double* w, const uint32_t* gdeg, const uint32_t* new_of_old,
+                                  const double* seed, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t s = new_of_old[v];
+        w[s] = seed[v] / static_cast<double>(gdeg[s]);
+    }
+}
+
+// out[v] = full[new_of_old[v]]  (back to the caller's ids).
+__global__ void unpermute_kernel(double* out, const double* full, const uint32_t* new_of_old, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        out[v] = full[new_of_old[v]];
+}
+
+// Batched: out[j][v] = full[new_of_old[v]][j] for j < count.
+__global__ void unpermute_batch_kernel(double* out, const double* full, const uint32_t* new_of_old,
+                                       uint32_t n, uint32_t count) {
+    const uint32_t lane = threadIdx.x & 63;
+    for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 6; v < n;
+         v += (gridDim.x * blockDim.x) >> 6) {
+        if (lane < count)
+            out[static_cast<size_t>(lane) * n + v] =
+                full[static_cast<size_t>(new_of_old[v]) * kBatchCols + lane];
+    }
+}
+
+// steps[k] = sum_b mass_partial[k][b]  (ordered, one CTA per step).
+__global__ void mass_steps_kernel(const double* mass_partial, uint32_t n_part, double* steps) {
+    __shared__ double red[kStepThreads / 32];
+    const uint32_t k = blockIdx.x;
+    double s = 0.0;
+    for (uint32_t b = threadIdx.x; b < n_part; b += blockDim.x) s += mass_partial[static_cast<size_t>(k) * n_part + b];
+    s = block_sum<kStepThreads>(s, red);
+    if (threadIdx.x == 0) steps[k] = s;
+}
+
+// err = max(err, max_k |steps[k] - mass0|).
+__global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, double* err) {
+    double worst = *err;
+    for (uint32_t k = 0; k < K; ++k) worst = fmax(worst, fabs(steps[k] - mass0));
+    *err = worst;
+}
+
+// Host-side launch wrappers ---------------------------------------------------
+void launch_step(const StepArgs& a, int grid, cudaStream_t st) {
+    cheby_step_kernel<kStepThreads, kTileEdges><<<grid, kStepThreads, 0, st>>>(a);
+}
+int step_occupancy() {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileEdges>,
+                                                  kStepThreads, 0);
+    return blocks;
+}
+void launch_batch(const BatchArgs& a, int grid, cudaStream_t st) {
+    cheby_batch_kernel<<<grid, kBatchThreads, 0, st>>>(a);
+}
+int batch_occupancy() {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel, kBatchThreads, 0);
+    return blocks;
+}
+void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                        uint32_t q, cudaStream_t st) {
+    init_onehot_kernel<<<1, 1, 0, st>>>(w, gdeg, no, src, q);
+}
+void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                              uint32_t q0, uint32_t count, cudaStream_t st) {
+    init_onehot_batch_kernel<<<1, kBatchCols, 0, st>>>(W, gdeg, no, src, q0, count);
+}
+void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
+                       uint32_t n, cudaStream_t st) {
+    init_dense_kernel<<<1184, 256, 0, st>>>(w, gdeg, no, seed, n);
+}
+void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, cudaStream_t st) {
+    unpermute_kernel<<<1184, 256, 0, st>>>(out, full, no, n);
+}
+void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
+                            uint32_t count, cudaStream_t st) {
+    unpermute_batch_kernel<<<1184, 256, 0, st>>>(out, full, no, n, count);
+}
+void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st) {
+    mass_steps_kernel<<<K, kStepThreads, 0, st>>>(mp, n_part, steps);
+}
+void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st) {
+    mass_err_kernel<<<1, 1, 0, st>>>(steps, K, mass0, err);
+}
+
+} // namespace cpg

@@ -1,0 +1,239 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference library.
+
+The checker is the UNMODIFIED reference (oracle/_ref/libchebyprop_ref.so, built
+from /root/reference sources), whose restatement oracle/cheby_oracle.c is
+pinned bit-for-bit in tests/test_oracle_pin.py.  Tolerance (north star):
+per score vector max-abs <= 1e-12, L1 <= 1e-10, identical top-100 set.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+PPR, HKPR = 0, 1
+
+
+def _ref_graph(off, nb):
+    from oracle import RefGraph
+
+    return RefGraph.from_csr(off, nb)
+
+
+def _graphs():
+    from oracle import Port
+
+    gs = {
+        "star": Port.edges_to_csr([[0, 1], [0, 2], [0, 3]]),          # tests/oracles.hpp:181-184
+        "path3": Port.edges_to_csr([[0, 1], [1, 2]]),                 # oracles.hpp:186-189
+        "ring_chord_200": Port.make_graph(200, 300, 1),               # acceptance.cpp:139-157 (C4)
+        "ring_chord_1000": Port.make_graph(1000, 1500, 5),
+        "big_star": Port.edges_to_csr([[0, i] for i in range(1, 9001)] + [[i, i + 1] for i in range(1, 9000)]),
+    }
+    return gs
+
+
+@pytest.fixture(scope="module")
+def graphs(gpu):
+    import paper_2412_10789_b200 as P
+
+    gs = _graphs()
+    gs["rmat12"] = P.gen_rmat(12, 8 * 4096, seed=3)
+    gs["chunglu"] = P.gen_chunglu(20000, 200000, 2.1, 20.0, 12000, seed=4)  # hubs split in pieces
+    return gs
+
+
+@pytest.mark.parametrize("name", ["star", "path3", "ring_chord_200", "ring_chord_1000", "big_star", "rmat12",
+                                  "chunglu"])
+@pytest.mark.parametrize("family,param", [(PPR, 0.2), (HKPR, 5.0)])
+def test_cheby_power_matches_reference(graphs, cpg, name, family, param):
+    off, nb = graphs[name]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    kernel = cpg.Kernel.ppr(param) if family == PPR else cpg.Kernel.hkpr(param)
+    K = cpg.plan_truncation(kernel, 1e-8).cheby_steps
+    n = g.node_count()
+    sources = sorted({0, n // 2, n - 1, min(n - 1, 7)})
+    for s in sources:
+        est = cpg.cheby_power(g, kernel, s, K)
+        want, mass, rst = ref.cheby_power(family, param, s, K)
+        assert_parity(est.values, want)
+        assert est.stats.iterations == rst["iterations"] == K
+        assert est.stats.push_work == rst["push_work"]
+        assert est.stats.mass_err_max <= 1e-9  # acceptance.cpp:349-360 (C13)
+
+
+def test_k1_two_term(graphs, cpg):
+    """test_solvers.cpp:89-100: K = 1 is c0 e_s + c1 P e_s."""
+    off, nb = graphs["star"]
+    g = cpg.Graph.from_csr(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    c = k.cheby_coeffs(1)
+    est = cpg.cheby_power(g, k, 1, 1)
+    e = np.zeros(4)
+    e[1] = 1
+    pe = cpg.apply_walk(g, e)
+    np.testing.assert_allclose(est.values, c[0] * e + c[1] * pe, rtol=1e-14, atol=0)
+
+
+def test_star_r3_lands_on_hub(graphs, cpg):
+    """test_solvers.cpp:101-113 through the observer slow path."""
+    off, nb = graphs["star"]
+    g = cpg.Graph.from_csr(off, nb)
+    seen = {}
+    cpg.cheby_power(g, cpg.Kernel.ppr(0.2), 1, 3, observer=lambda k, r, e: seen.__setitem__(k, r.copy()))
+    r3 = seen[3]
+    assert abs(r3[0] - 1.0) <= 1e-14
+    assert np.all(np.abs(r3[1:]) < 1e-14)
+
+
+def test_observer_trace_matches_reference(graphs, cpg):
+    off, nb = graphs["ring_chord_200"]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    K = 12
+    rs, es = [], []
+    est = cpg.cheby_power(g, cpg.Kernel.hkpr(5.0), 17, K, observer=lambda k, r, e: (rs.append(r.copy()),
+                                                                                    es.append(e.copy())))
+    want, rt, et = ref.cheby_power_trace(HKPR, 5.0, 17, K)
+    assert len(rs) == K + 1
+    for k in range(K + 1):
+        assert np.abs(rs[k] - rt[k]).max() <= 1e-12
+        assert np.abs(es[k] - et[k]).max() <= 1e-12
+    assert_parity(est.values, want)
+
+
+def test_mass_conservation_every_step(graphs, cpg):
+    """test_solvers.cpp:122-128 / acceptance C13: |sum r_k - 1| <= 1e-9."""
+    from oracle import Port
+
+    off, nb = Port.make_graph(50, 80, 17)
+    g = cpg.Graph.from_csr(off, nb)
+    sums = []
+    cpg.cheby_power(g, cpg.Kernel.ppr(0.2), 7, 30, observer=lambda k, r, e: sums.append(r.sum()))
+    assert len(sums) == 31
+    assert max(abs(s - 1.0) for s in sums) <= 1e-9
+
+
+def test_cheby_power_vec_matches_reference(graphs, cpg):
+    from oracle import Port
+
+    for name in ("ring_chord_1000", "rmat12", "chunglu"):
+        off, nb = graphs[name]
+        g = cpg.Graph.from_csr(off, nb)
+        ref = _ref_graph(off, nb)
+        x = Port.random_vector(g.node_count(), 92, 0.0, 1.0)
+        est = cpg.cheby_power_vec(g, cpg.Kernel.ppr(0.2), x, 40)
+        want = ref.cheby_power_vec(PPR, 0.2, x, 40)
+        assert np.abs(est.values - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+        assert np.abs(est.values - want).sum() <= 1e-10 * max(1.0, np.abs(want).sum())
+
+
+def test_apply_walk_matches_reference(graphs, cpg):
+    from oracle import Port
+
+    for name in ("star", "path3", "rmat12", "big_star"):
+        off, nb = graphs[name]
+        g = cpg.Graph.from_csr(off, nb)
+        ref = _ref_graph(off, nb)
+        x = Port.random_vector(g.node_count(), 5, 0.0, 1.0)
+        np.testing.assert_allclose(cpg.apply_walk(g, x), ref.apply_walk(x), rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("nsrc", [1, 10, 64, 70])
+def test_batched_matches_single_source(graphs, cpg, nsrc):
+    off, nb = graphs["chunglu"]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    kernel = cpg.Kernel.hkpr(5.0)
+    K = cpg.plan_truncation(kernel, 1e-8).cheby_steps
+    src = ref.select_sources_uniform(nsrc, 11)
+    got, st = cpg.cheby_power_many(g, kernel, src, K, batched=True)
+    assert got.shape == (nsrc, g.node_count())
+    for j in range(0, nsrc, max(1, nsrc // 5)):
+        want, _, _ = ref.cheby_power(HKPR, 5.0, int(src[j]), K)
+        assert_parity(got[j], want)
+    assert st.push_work == K * g.volume() * nsrc
+
+
+def test_many_single_source_pinned_output(graphs, cpg):
+    import torch
+
+    off, nb = graphs["rmat12"]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    kernel = cpg.Kernel.ppr(0.2)
+    K = 26
+    src = ref.select_sources_uniform(9, 1)
+    pinned = torch.empty((len(src), g.node_count()), dtype=torch.float64, pin_memory=True)
+    got, st = cpg.cheby_power_many(g, kernel, src, K, out=pinned.numpy())
+    for j, s in enumerate(src):
+        want, _, _ = ref.cheby_power(PPR, 0.2, int(s), K)
+        assert_parity(got[j], want)
+    assert st.mass_err_max <= 1e-9
+
+
+def test_sum_property(graphs, cpg):
+    """Property 1: sum yhat = sum_k c_k."""
+    off, nb = graphs["chunglu"]
+    g = cpg.Graph.from_csr(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    est = cpg.cheby_power(g, k, 3, 26)
+    assert abs(est.values.sum() - k.cheby_coeffs(26).sum()) <= 1e-12
+
+
+def test_bit_reproducible(graphs, cpg):
+    off, nb = graphs["chunglu"]
+    g = cpg.Graph.from_csr(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    a = cpg.cheby_power(g, k, 5, 26).values
+    b = cpg.cheby_power(g, k, 5, 26).values
+    assert np.array_equal(a, b)
+
+
+def test_errors(graphs, cpg):
+    off, nb = graphs["path3"]
+    g = cpg.Graph.from_csr(off, nb)
+    with pytest.raises(cpg.ParameterError):
+        cpg.cheby_power(g, cpg.Kernel.ppr(0.2), 99, 5)  # solvers.cpp:28-29
+    with pytest.raises(cpg.ParameterError):
+        cpg.cheby_power(g, cpg.Kernel.ppr(0.2), 0, 0)  # solvers.cpp:201
+    with pytest.raises(cpg.ParameterError):
+        cpg.cheby_power_vec(g, cpg.Kernel.ppr(0.2), np.zeros(2), 5)  # solvers.cpp:36-37
+
+
+def test_general_gp_vector_a_half(graphs, cpg):
+    """acceptance.cpp:317-347 (C12) style: a = 1/2 against the reference wrapper."""
+    from oracle import Port
+
+    off, nb = Port.make_graph(10, 12, 63)
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    x = Port.random_vector(g.node_count(), 64, 0.0, 1.0)
+    steps = cpg.plan_truncation(cpg.Kernel.ppr(0.2), 1e-13).cheby_steps
+    z = cpg.general_gp_vector(g, cpg.Kernel.ppr(0.2), 0.5, x, steps)
+    want = ref.general_gp_vector(PPR, 0.2, 0.5, x, steps)
+    assert np.abs(z - want).max() <= 1e-12
+
+
+def test_device_generator_matches_host(cpg, gpu):
+    dev = cpg.gen_rmat(14, 8 << 14, seed=9, device=0)
+    off, nb = dev.to_host()
+    hoff, hnb = cpg.gen_rmat(14, 8 << 14, seed=9)
+    assert np.array_equal(off, hoff) and np.array_equal(nb, hnb)
+    dev.close()
+    dev = cpg.gen_chunglu(30000, 150000, 2.3, 10.0, 2000, seed=5, device=0)
+    off, nb = dev.to_host()
+    hoff, hnb = cpg.gen_chunglu(30000, 150000, 2.3, 10.0, 2000, seed=5)
+    assert np.array_equal(off, hoff) and np.array_equal(nb, hnb)
+
+
+def test_graph_from_device_csr(cpg, gpu):
+    dev = cpg.gen_rmat(13, 8 << 13, seed=21, device=0)
+    off, nb = dev.to_host()
+    dg = cpg.DeviceGraph.from_device(dev)
+    ref = _ref_graph(off, nb)
+    est = cpg.cheby_power(dg, cpg.Kernel.ppr(0.2), 11, 26)
+    want, _, _ = ref.cheby_power(PPR, 0.2, 11, 26)
+    assert_parity(est.values, want)
