@@ -235,10 +235,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default=None, choices=["single", "batched"], help="override the config's path")
+    ap.add_argument("--tile", type=int, default=None, help="sources per batched tile (1..64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.mode:
+        cfg["mode"] = args.mode
+    if args.tile:
+        cfg["tile"] = args.tile
     if args.impl == "reference":
         return run_reference(args, cfg)
     run_ours(args, cfg)
@@ -283,7 +289,7 @@ def run_ours(args, cfg):
 
     sources = P.select_sources_uniform(n, cfg["sources"], 1)
     batched = cfg["mode"] == "batched"
-    tile = 64
+    tile = int(cfg.get("tile", min(64, len(sources))))
     L = P._lib.lib()
     import ctypes
 
@@ -396,6 +402,7 @@ def run_ours(args, cfg):
             "queries_per_s": queries / (ms / 1e3),
             "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": nnz, "K": K,
                        "sources_per_step": len(sources), "mode": cfg["mode"],
+                       "tile": tile if batched else 1,
                        "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

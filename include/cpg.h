@@ -184,6 +184,9 @@ int cpg_gen_chunglu(uint32_t n_ids, uint64_t n_samples, double exponent, double 
                     uint32_t max_degree, uint64_t seed, int device, uint64_t** offsets,
                     uint32_t** neighbors, uint32_t* n, uint64_t* nnz);
 int cpg_free_csr(uint64_t* offsets, uint32_t* neighbors, int device);
+/* Copy a device-resident CSR (e.g. from the generator) into caller host arrays. */
+int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint32_t n, uint64_t nnz,
+                    int device, uint64_t* offsets, uint32_t* neighbors);
 
 #ifdef __cplusplus
 }

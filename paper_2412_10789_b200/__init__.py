@@ -452,15 +452,10 @@ class DeviceCSR:
             self.offsets_ptr = self.neighbors_ptr = 0
 
     def to_host(self):
-        import torch  # plumbing only: device->host copy of the generated CSR
-
         off = np.empty(self.n + 1, dtype=np.uint64)
         nbr = np.empty(self.nnz, dtype=np.uint32)
-        cudart = torch.cuda.cudart()
-        torch.cuda.synchronize(self.device)
-        # cudaMemcpy(dst, src, bytes, DeviceToHost=2)
-        cudart.cudaMemcpy(off.ctypes.data, self.offsets_ptr, off.nbytes, 2)
-        cudart.cudaMemcpy(nbr.ctypes.data, self.neighbors_ptr, nbr.nbytes, 2)
+        _check(L.lib().cpg_csr_to_host(ctypes.c_void_p(self.offsets_ptr), ctypes.c_void_p(self.neighbors_ptr),
+                                       self.n, self.nnz, self.device, _u64p(off), _u32p(nbr)), "csr_to_host")
         return off, nbr
 
     def __del__(self):

@@ -97,7 +97,7 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     g->hub_partial = dalloc<double>(g->n_hub_items);
     g->hub_count = dalloc<unsigned int>(g->n_hubs);
     CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_hubs)));
-    const int occ = std::max(1, step_occupancy());
+    const int occ = std::max(1, step_occupancy(g->tile));
     g->step_grid = static_cast<int>(std::max<uint32_t>(
         1, std::min<uint64_t>(g->n_items, static_cast<uint64_t>(occ) * g->sm_count)));
     g->batch_grid = std::max(1, batch_occupancy()) * g->sm_count;
@@ -106,8 +106,15 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     return g.release();
 }
 
+// Column width of the batched step for a tile of `tile` sources.
+uint32_t batch_width(uint32_t tile) {
+    uint32_t B = 4;
+    while (B < tile) B <<= 1;
+    return B;
+}
+
 void ensure_ws(cpg_graph* g, size_t cols) {
-    if (g->ws_cols >= cols) return;
+    if (g->ws_cols == cols) return;
     dfree(g->w_a);
     dfree(g->w_b);
     dfree(g->acc);
@@ -184,6 +191,7 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
         a.coeffs = g->d_coeffs;
         a.row0 = g->row0;
         a.n_items = g->n_items;
+        a.tile = g->tile;
         a.k = static_cast<int>(k);
         a.first = k == 1;
         a.last = k == K;
@@ -212,12 +220,12 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
 }
 
 // One tile of up to 64 sources (q0 .. q0+count) through the batched step.
-uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t count, double* d_dst, cudaStream_t st,
-                   StepProf* prof) {
+uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
+                   cudaStream_t st, StepProf* prof) {
     uint32_t launches = 0;
-    const size_t cols = kBatchCols;
+    const size_t cols = B;
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
-    launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, st);
+    launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
     ++launches;
     for (uint32_t k = 1; k <= K; ++k) {
         BatchArgs b;
@@ -239,7 +247,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t count, double
         b.first = k == 1;
         b.last = k == K;
         if (prof) prof->before(st);
-        launch_batch(b, g->batch_grid, st);
+        launch_batch(b, static_cast<int>(B), g->batch_grid, st);
         if (prof) prof->after(st);
         ++launches;
         if (g->nranks > 1)
@@ -252,7 +260,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t count, double
             nccl_allgather_f64(g->acc, g->full, g->n_loc * cols, g->nccl_comm, st);
             src = g->full;
         }
-        launch_unpermute_batch(d_dst, src, g->new_of_old, g->n, count, st);
+        launch_unpermute_batch(d_dst, src, g->new_of_old, g->n, count, B, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -308,12 +316,17 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             CPG_CUDA(cudaEventRecord(g->ev[4], static_cast<cudaStream_t>(user_stream)));
             CPG_CUDA(cudaStreamWaitEvent(st, g->ev[4], 0));
         }
-        const size_t cols = mode == 2 ? kBatchCols : 1;
+        const uint32_t B = mode == 2 ? batch_width(tile) : 1;
+        const size_t cols = B;
         if (mode == 2) {
             require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
             ensure_batch_tables(g);
-            if (!g->bhub_partial) {
-                g->bhub_partial = dalloc<double>(static_cast<size_t>(g->n_bhub_items) * kBatchCols);
+            if (g->bhub_cols < B) {
+                dfree(g->bhub_partial);
+                g->bhub_partial = dalloc<double>(static_cast<size_t>(g->n_bhub_items) * B);
+                g->bhub_cols = B;
+            }
+            if (!g->bhub_count) {
                 g->bhub_count = dalloc<unsigned int>(g->n_bhubs);
                 CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_bhubs)));
             }
@@ -349,7 +362,7 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
                 CPG_CUDA(cudaMemcpyAsync(seed_dev, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
                 launches += run_single(g, K, q0, seed_dev, mass0, dst, st, prof.get());
             } else {
-                launches += run_batch(g, K, q0, count, dst, st, prof.get());
+                launches += run_batch(g, K, B, q0, count, dst, st, prof.get());
             }
             if (out && !out_on_device) {
                 // compute of batch b is queued; now drain batch b-1 (overlaps b's steps)
@@ -385,7 +398,7 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (seed_dev) cudaFree(seed_dev);
-        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, static_cast<uint32_t>(cols));
+        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, mode == 2 ? tile : 1u);
         if (stats && prof) {
             stats->step_ms = prof->total_ms();
             stats->step_launches = static_cast<uint32_t>(prof->ev.size() / 2);
@@ -594,6 +607,7 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
             a.coeffs = g->d_coeffs;
             a.row0 = 0;
             a.n_items = g->n_items;
+        a.tile = g->tile;
             a.k = static_cast<int>(k);
             a.first = k == 1;
             a.last = 0;
@@ -614,7 +628,7 @@ double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile) {
     // 4 B index + 8*B B gathered row per edge, 8 B row pointer
     // per row, 4 streams of 8*B B per row (read w_{k-1}, write w_{k+1}, read+write
     // acc); sharded adds the received all-gather bytes 8*B*n*(R-1)/R.
-    const double B = tile <= 1 ? 1.0 : kBatchCols;
+    const double B = tile <= 1 ? 1.0 : static_cast<double>(batch_width(tile));
     const double nnz = static_cast<double>(g->nnz_loc), nl = static_cast<double>(g->n_loc);
     double bytes = nnz * (4.0 + 8.0 * B) + 8.0 * (nl + 1) + 32.0 * nl * B;
     if (g->nranks > 1)

@@ -23,6 +23,7 @@ struct cpg_graph {
 
     cpg::WorkItem* items = nullptr; // single-source items
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0;
+    int tile = 0;                   // kTileSmall / kTileLarge
     cpg::WorkItem* bitems = nullptr; // batched hub pieces
     uint32_t n_bhubs = 0, n_bhub_items = 0;
 
@@ -40,7 +41,8 @@ struct cpg_graph {
     double* w_b = nullptr;
     double* acc = nullptr;
     double* full = nullptr;         // gathered final result (n_pad or n_pad*64)
-    size_t ws_cols = 0;             // 1 (single) or 64 (batched) currently sized for
+    size_t ws_cols = 0;             // columns the workspace is sized for (1 or B)
+    size_t bhub_cols = 0;           // columns bhub_partial is sized for
     double* d_coeffs = nullptr;
     size_t coeff_cap = 0;
     uint32_t* d_sources = nullptr;
@@ -66,18 +68,18 @@ void ensure_batch_tables(cpg_graph* g);
 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st);
-int step_occupancy();
-void launch_batch(const BatchArgs& a, int grid, cudaStream_t st);
+int step_occupancy(int tile);
+void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int batch_occupancy();
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                              uint32_t q0, uint32_t count, cudaStream_t st);
+                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st);
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
                        uint32_t n, cudaStream_t st);
 void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, cudaStream_t st);
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
-                            uint32_t count, cudaStream_t st);
+                            uint32_t count, uint32_t B, cudaStream_t st);
 void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st);
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
 

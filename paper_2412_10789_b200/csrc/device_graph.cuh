@@ -19,11 +19,13 @@
 
 namespace cpg {
 
-// Tile geometry of the single-source step (cheby_step_kernel).
+// Tile geometry of the single-source step (cheby_step_kernel).  The tile
+// width is chosen per graph at upload: kTileLarge when there are enough edges
+// to give every SM several tiles, kTileSmall otherwise.
 constexpr int kStepThreads = 256;
-constexpr int kTileEdges = 2048;                 // edges staged per tile (16 KB smem)
-constexpr int kTileChunk = kTileEdges / 2;       // rows with deg > chunk are hubs
-constexpr int kTileMaxRows = 2048;
+constexpr int kTileSmall = 1024;                 // edges staged per tile ( 8 KB smem)
+constexpr int kTileLarge = 4096;                 // edges staged per tile (32 KB smem)
+constexpr int kTileMaxRows = 512;                // rows per tile (2 epilogue rows per thread)
 constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per thread)
 
 // Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
@@ -31,12 +33,19 @@ constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
 constexpr int kBatchHubEdges = 2048;             // rows above this are split
 
-// Work item.  Tile: {row_begin, row_end, 0, lg<<1}.  Hub piece:
-// {row, slot_base, piece, (hub<<1)|1}; pieces of one hub are consecutive
-// slots [slot_base, slot_base + P).
-struct WorkItem {
-    uint32_t a, b, c, info;
+// Work item (16 B, one vector load).
+//   tile: a = first row, b = end row,
+//         c = first edge | edge count << 40 | lg(lane group) << 54
+//   hub piece (bit 63 of c set): a = row (== hub index, hubs are the row
+//         prefix), b = first partial slot of this hub, c = piece | 1 << 63
+struct __align__(16) WorkItem {
+    uint32_t a, b;
+    uint64_t c;
 };
+constexpr uint64_t kHubBit = 1ull << 63;
+__host__ __device__ inline uint64_t tile_code(uint64_t e0, uint32_t cnt, uint32_t lg) {
+    return e0 | (static_cast<uint64_t>(cnt) << 40) | (static_cast<uint64_t>(lg) << 54);
+}
 
 struct StepArgs {
     const int64_t* rowptr;
@@ -52,6 +61,7 @@ struct StepArgs {
     const double* coeffs;  // device copy of c_0..c_K
     uint32_t row0;         // global id of local row 0
     uint32_t n_items;
+    int tile;              // kTileSmall or kTileLarge (must match the table)
     int k;                 // computing w_k (1..K)
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
     int last;              // write out = d * acc instead of acc

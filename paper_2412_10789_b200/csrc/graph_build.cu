@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "cpg_graph.hpp"
@@ -106,14 +107,17 @@ __global__ void k_pieces(const int64_t* rowptr, uint32_t n_hub, int64_t piece, u
 __global__ void k_hub_items(const uint32_t* P, const uint32_t* base, uint32_t n_hub, WorkItem* items) {
     const int lane = threadIdx.x & 31;
     for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5)
-        for (uint32_t p = lane; p < P[j]; p += 32) items[base[j] + p] = WorkItem{j, base[j], p, (j << 1) | 1u};
+        for (uint32_t p = lane; p < P[j]; p += 32) items[base[j] + p] = WorkItem{j, base[j], p | kHubBit};
 }
 
-__global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, uint8_t* flags) {
+// A row starts a tile when its first edge falls in a new chunk of tile/2 edges
+// (or every kTileMaxRows rows).  All rows of a tile start inside one chunk and
+// non-hub rows have <= tile/2 edges, so a tile holds <= tile edges.
+__global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, int64_t chunk, uint8_t* flags) {
     for (uint64_t j = first + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc;
          j += (uint64_t)gridDim.x * blockDim.x) {
         bool start = (j == first) || ((j - first) % kTileMaxRows == 0) ||
-                     (rowptr[j] / kTileChunk != rowptr[j - 1] / kTileChunk);
+                     (rowptr[j] / chunk != rowptr[j - 1] / chunk);
         flags[j - first] = start ? 1 : 0;
     }
 }
@@ -127,7 +131,8 @@ __global__ void k_tile_items(const int64_t* rowptr, const uint32_t* starts, uint
         const double avg = static_cast<double>(edges) / static_cast<double>(re - rb);
         int lg = 0;
         while (lg < 5 && static_cast<double>(2 << lg) <= avg / 2.0) ++lg;  // g <= mean/2
-        items[t] = WorkItem{rb, re, 0u, static_cast<uint32_t>(lg) << 1};
+        items[t] = WorkItem{rb, re, tile_code(static_cast<uint64_t>(rowptr[rb]), static_cast<uint32_t>(edges),
+                                               static_cast<uint32_t>(lg))};
     }
 }
 
@@ -232,10 +237,17 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
     }
     cudaFree(lold);
 
-    // 5. single-source work table: hub pieces, then row tiles.
+    // 5. single-source work table: hub pieces, then row tiles.  Large tiles
+    //    when every SM gets >= 8 of them, small tiles otherwise.
+    g->tile = g->nnz_loc >= static_cast<uint64_t>(kTileLarge) * g->sm_count * 8 ? kTileLarge : kTileSmall;
+    if (const char* force = std::getenv("CPG_TILE")) {  // test hook: exercise either width
+        const int t = std::atoi(force);
+        if (t == kTileSmall || t == kTileLarge) g->tile = t;
+    }
+    const int64_t chunk = g->tile / 2;
     WorkItem* hub_items = nullptr;
     uint32_t n_hub = 0, n_hub_items = 0;
-    build_hub_items(g->rowptr, n_loc, kTileChunk, kHubPieceEdges, &hub_items, &n_hub, &n_hub_items, 0, st);
+    build_hub_items(g->rowptr, n_loc, chunk, kHubPieceEdges, &hub_items, &n_hub, &n_hub_items, 0, st);
     uint32_t n_tiles = 0;
     uint32_t* starts = nullptr;
     if (n_hub < n_loc) {
@@ -243,7 +255,7 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
         uint8_t* flags = dalloc<uint8_t>(rows);
         starts = dalloc<uint32_t>(rows);
         unsigned int* d_sel = dalloc<unsigned int>(1);
-        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(g->rowptr, n_hub, n_loc, flags);
+        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(g->rowptr, n_hub, n_loc, chunk, flags);
         cub::CountingInputIterator<uint32_t> it(n_hub);
         bytes = 0;
         cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);

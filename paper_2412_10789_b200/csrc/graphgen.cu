@@ -304,6 +304,16 @@ int cpg_gen_chunglu(uint32_t n_ids, uint64_t n_samples, double exponent, double 
     });
 }
 
+int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint32_t n, uint64_t nnz, int device,
+                    uint64_t* offsets, uint32_t* neighbors) {
+    return guarded([&] {
+        require(d_offsets && d_neighbors && offsets && neighbors, "null argument");
+        CPG_CUDA(cudaSetDevice(device));
+        CPG_CUDA(cudaMemcpy(offsets, d_offsets, (static_cast<size_t>(n) + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CPG_CUDA(cudaMemcpy(neighbors, d_neighbors, nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
 int cpg_free_csr(uint64_t* offsets, uint32_t* neighbors, int device) {
     return guarded([&] {
         if (device < 0) {

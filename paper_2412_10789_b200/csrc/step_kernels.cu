@@ -56,18 +56,20 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // Recurrence + accumulation + mass for local row r with neighbour sum y.
-__device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, double y, int64_t d,
-                                              double& mass) {
+// w_prev = w_{k-1}(v) (for the first step: w_0(v)), acc_old = acc(v) (unused
+// in the first step).
+__device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, double y, int64_t d, double w_prev,
+                                              double acc_old, double& mass) {
     const uint32_t gr = a.row0 + r;
     double w_new = 0.0, acc_new = 0.0;
     if (d > 0) {
         const double dd = static_cast<double>(d);
         if (a.first) {
             w_new = y / dd;  // w_1 = D^-1 A w_0   (T_1 = P T_0, solvers.cpp:212)
-            acc_new = a.coeffs[0] * a.w_cur[gr] + a.coeffs[1] * w_new;
+            acc_new = a.coeffs[0] * w_prev + a.coeffs[1] * w_new;
         } else {
-            w_new = 2.0 * y / dd - a.w_io[gr];  // solvers.cpp:221
-            acc_new = a.acc[r] + a.coeffs[a.k] * w_new;  // solvers.cpp:218 (for k+1)
+            w_new = 2.0 * y / dd - w_prev;  // solvers.cpp:221
+            acc_new = acc_old + a.coeffs[a.k] * w_new;  // solvers.cpp:218 (for k+1)
         }
         mass += dd * w_new;
     }
@@ -78,57 +80,91 @@ __device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, dou
         a.acc[r] = acc_new;
 }
 
+__device__ __forceinline__ void load_prev(const StepArgs& a, uint32_t r, double& w_prev, double& acc_old) {
+    const uint32_t gr = a.row0 + r;
+    if (a.first) {
+        w_prev = a.w_cur[gr];
+        acc_old = 0.0;
+    } else {
+        w_prev = a.w_io[gr];
+        acc_old = a.acc[r];
+    }
+}
+
+template <int TILE>
+struct TileSmem {
+    double vals[TILE];            // gathered w_k(col) of the tile's edges
+    double ysum[kTileMaxRows];    // per-row neighbour sums
+    int rp[kTileMaxRows + 1];     // row offsets relative to the tile's first edge
+};
+
+// One row tile: every global load is issued up front (row offsets, the index
+// stream, the epilogue operands of the rows this thread finalises), then the
+// gathers; one barrier; lane-group row sums from shared memory; one barrier;
+// the fused epilogue with thread t owning rows t and t + 256.
 template <int THREADS, int TILE>
-__device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, double* vals,
+__device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, TileSmem<TILE>& sm,
                                              double& mass) {
     constexpr int PER = TILE / THREADS;
-    const uint32_t rb = it.a, re = it.b;
-    const int lg = (it.info >> 1) & 7;
-    const int64_t e0 = a.rowptr[rb];
-    const int cnt = static_cast<int>(a.rowptr[re] - e0);
+    constexpr int RPT = kTileMaxRows / THREADS;
+    const uint32_t rb = it.a;
+    const int nrows = static_cast<int>(it.b - it.a);
+    const int64_t e0 = static_cast<int64_t>(it.c & ((1ull << 40) - 1));
+    const int cnt = static_cast<int>((it.c >> 40) & 0x3fff);
+    const int lg = static_cast<int>((it.c >> 54) & 7);
     const uint32_t* colp = a.col + e0;
 
-    // Phase 1: coalesced index stream, independent gathers (PER in flight per thread).
     uint32_t idx[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int j = i * THREADS + threadIdx.x;
         idx[i] = j < cnt ? ld_index(colp + j) : 0u;
     }
+    for (int j = threadIdx.x; j <= nrows; j += THREADS) sm.rp[j] = static_cast<int>(a.rowptr[rb + j] - e0);
+    double w_prev[RPT], acc_old[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = q * THREADS + threadIdx.x;
+        if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
+    }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int j = i * THREADS + threadIdx.x;
-        if (j < cnt) vals[j] = ld_gather(a.w_cur + idx[i]);
+        if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[i]);
     }
     __syncthreads();
 
-    // Phase 2: per-row reduction by lane groups of g = 2^lg, then epilogue.
     const int g = 1 << lg;
     const int sub = threadIdx.x & (g - 1);
     const int grp = threadIdx.x >> lg;
     const int ngrp = THREADS >> lg;
-    const uint32_t nrows = re - rb;
-    for (uint32_t base = 0; base < nrows; base += ngrp) {
-        const uint32_t r = rb + base + grp;
+    for (int base = 0; base < nrows; base += ngrp) {
+        const int r = base + grp;
         double s = 0.0;
-        int64_t d = 0;
-        if (r < re) {
-            const int64_t rs = a.rowptr[r];
-            d = a.rowptr[r + 1] - rs;
-            const double* v = vals + (rs - e0);
-            for (int j = sub; j < d; j += g) s += v[j];
+        if (r < nrows) {
+            const int b1 = sm.rp[r + 1];
+            for (int j = sm.rp[r] + sub; j < b1; j += g) s += sm.vals[j];
         }
         for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (r < re && sub == 0) step_epilogue(a, r, s, d, mass);
+        if (r < nrows && sub == 0) sm.ysum[r] = s;
     }
-    __syncthreads();  // vals is reused by the next item
+    __syncthreads();
+
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = q * THREADS + threadIdx.x;
+        if (r < nrows)
+            step_epilogue(a, rb + r, sm.ysum[r], sm.rp[r + 1] - sm.rp[r], w_prev[q], acc_old[q], mass);
+    }
+    __syncthreads();  // shared memory is reused by the next item
 }
 
 template <int THREADS>
 __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it, double* red,
                                             int* flag, double& mass) {
     constexpr int PER = kHubPieceEdges / THREADS;
-    const uint32_t r = it.a, slot_base = it.b, piece = it.c, hub = it.info >> 1;
+    const uint32_t r = it.a, slot_base = it.b;
+    const uint32_t piece = static_cast<uint32_t>(it.c & 0xffffffffu), hub = it.a;
     const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
     const int64_t d = re - rs;
     const int64_t p0 = rs + static_cast<int64_t>(piece) * kHubPieceEdges;
@@ -153,7 +189,11 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
     s = block_sum<THREADS>(s, red);
 
     if (P == 1) {
-        if (threadIdx.x == 0) step_epilogue(a, r, s, d, mass);
+        if (threadIdx.x == 0) {
+            double wp, ao;
+            load_prev(a, r, wp, ao);
+            step_epilogue(a, r, s, d, wp, ao, mass);
+        }
         return;
     }
     if (threadIdx.x == 0) {
@@ -171,7 +211,9 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
         for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
         if (threadIdx.x == 0) {
             a.hub_count[hub] = 0u;  // re-arm for the next step
-            step_epilogue(a, r, y, d, mass);
+            double wp, ao;
+            load_prev(a, r, wp, ao);
+            step_epilogue(a, r, y, d, wp, ao, mass);
         }
     }
     __syncthreads();
@@ -179,39 +221,45 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
 
 template <int THREADS, int TILE>
 __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
-    __shared__ double vals[TILE];
+    __shared__ TileSmem<TILE> sm;
     __shared__ double red[THREADS / 32];
     __shared__ int flag;
     double mass = 0.0;
     for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
-        const WorkItem it = a.items[i];
-        if (it.info & 1u)
+        WorkItem it;
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
+        it.a = raw.x;
+        it.b = raw.y;
+        it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        if (it.c & kHubBit)
             process_hub<THREADS>(a, it, red, &flag, mass);
         else
-            process_tile<THREADS, TILE>(a, it, vals, mass);
+            process_tile<THREADS, TILE>(a, it, sm, mass);
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
 // ---------------------------------------------------------------------------
-// Batched step: 64 sources per tile, iterate rows [n_pad][64] fp64 row-major.
-// One warp per row job; each lane owns two columns (one double2 per gathered
-// 512-B row).  Rows above kBatchHubEdges are split into pieces with the same
-// ordered last-arriver reduction.  Edge order within a row is sequential, so
-// each column is bit-identical to a single-source run with the same sum order.
+// Batched step: B sources per tile (B in {4,8,16,32,64}), iterates row-major
+// [n_pad][B] fp64.  One warp per row job.  L = B/2 lanes cover one gathered
+// row (a double2 each), so one warp instruction gathers EPW = 32/L neighbour
+// rows: every edge costs ONE B*8-byte row fetch shared by B queries (vs one
+// 8-byte fetch per query in the single-source step).  Lane sub-group s sums
+// edges s, s+EPW, ... in order; sub-groups are combined by a fixed xor tree,
+// so results are bit-reproducible.  Rows above kBatchHubEdges are split into
+// pieces with the ordered last-arriver reduction.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d,
-                                               int lane) {
+template <int B>
+__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d, int cl) {
     const uint32_t gr = a.row0 + r;
-    double2* wio = reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * kBatchCols) + lane;
-    double2* accp = reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * kBatchCols) + lane;
+    double2* wio = reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B) + cl;
+    double2* accp = reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * B) + cl;
     double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
     if (d > 0) {
         const double dd = static_cast<double>(d);
         if (a.first) {
-            const double2 w0 =
-                reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * kBatchCols)[lane];
+            const double2 w0 = reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl];
             w_new.x = y.x / dd;
             w_new.y = y.y / dd;
             acc_new.x = a.coeffs[0] * w0.x + a.coeffs[1] * w_new.x;
@@ -229,26 +277,31 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, d
     *wio = w_new;
     if (a.last) {
         const double dd = static_cast<double>(d);
-        reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * kBatchCols)[lane] =
-            make_double2(dd * acc_new.x, dd * acc_new.y);
+        reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * B)[cl] = make_double2(dd * acc_new.x, dd * acc_new.y);
     } else {
         *accp = acc_new;
     }
 }
 
+// Sum of W_k rows over edges [e0, e1), for this lane's two columns, reduced
+// over the EPW lane sub-groups (result valid in every lane).
+template <int B>
 __device__ __forceinline__ double2 batch_row_sum(const BatchArgs& a, int64_t e0, int64_t e1, int lane) {
-    constexpr int U = 8;
+    constexpr int L = B / 2;
+    constexpr int EPW = 32 / L;
+    constexpr int U = (EPW >= 8) ? 4 : 8;  // gathers in flight per lane
+    const int sub = lane / L, cl = lane % L;
     double2 s = {0.0, 0.0};
     for (int64_t base = e0; base < e1; base += 32) {
         const int m = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
         const uint32_t c = lane < m ? ld_index(a.col + base + lane) : 0u;
-        int j = 0;
-        for (; j + U <= m; j += U) {
+        for (int j = 0; j < m; j += EPW * U) {
             double2 v[U];
 #pragma unroll
             for (int t = 0; t < U; ++t) {
-                const uint32_t u = __shfl_sync(0xffffffffu, c, j + t);
-                v[t] = ld_gather2(a.w_cur + static_cast<size_t>(u) * kBatchCols + 2 * lane);
+                const int jj = j + t * EPW + sub;
+                const uint32_t u = __shfl_sync(0xffffffffu, c, jj & 31);
+                v[t] = jj < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int t = 0; t < U; ++t) {
@@ -256,33 +309,37 @@ __device__ __forceinline__ double2 batch_row_sum(const BatchArgs& a, int64_t e0,
                 s.y += v[t].y;
             }
         }
-        for (; j < m; ++j) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, j);
-            const double2 v = ld_gather2(a.w_cur + static_cast<size_t>(u) * kBatchCols + 2 * lane);
-            s.x += v.x;
-            s.y += v.y;
-        }
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
     }
     return s;
 }
 
+template <int B>
 __global__ void __launch_bounds__(kBatchThreads) cheby_batch_kernel(const BatchArgs a) {
+    constexpr int L = B / 2;
     const int lane = threadIdx.x & 31;
+    const int cl = lane % L;
+    const bool writer = lane < L;
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_jobs = a.n_hub_items + (a.n_loc - a.hub_rows);
     for (uint32_t job = wg; job < n_jobs; job += nw) {
         if (job < a.n_hub_items) {
             const WorkItem it = a.hub_items[job];
-            const uint32_t r = it.a, slot_base = it.b, piece = it.c, hub = it.info >> 1;
+            const uint32_t r = it.a, slot_base = it.b, hub = it.a;
+            const uint32_t piece = static_cast<uint32_t>(it.c & 0xffffffffu);
             const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
             const int64_t d = re - rs;
             const int64_t p0 = rs + static_cast<int64_t>(piece) * kBatchHubEdges;
             const int64_t p1 = min(p0 + kBatchHubEdges, re);
             const uint32_t P = static_cast<uint32_t>((d + kBatchHubEdges - 1) / kBatchHubEdges);
-            const double2 s = batch_row_sum(a, p0, p1, lane);
-            reinterpret_cast<double2*>(a.hub_partial +
-                                       static_cast<size_t>(slot_base + piece) * kBatchCols)[lane] = s;
+            const double2 s = batch_row_sum<B>(a, p0, p1, lane);
+            if (writer)
+                reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(slot_base + piece) * B)[cl] = s;
             __threadfence();
             __syncwarp();
             unsigned prev = 0;
@@ -292,20 +349,19 @@ __global__ void __launch_bounds__(kBatchThreads) cheby_batch_kernel(const BatchA
                 __threadfence();
                 double2 y = {0.0, 0.0};
                 for (uint32_t p = 0; p < P; ++p) {
-                    const double2 v = __ldcg(reinterpret_cast<const double2*>(
-                                                 a.hub_partial + static_cast<size_t>(slot_base + p) * kBatchCols) +
-                                             lane);
+                    const double2 v = __ldcg(
+                        reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(slot_base + p) * B) + cl);
                     y.x += v.x;
                     y.y += v.y;
                 }
                 if (lane == 0) a.hub_count[hub] = 0u;
-                batch_epilogue(a, r, y, d, lane);
+                if (writer) batch_epilogue<B>(a, r, y, d, cl);
             }
         } else {
             const uint32_t r = a.hub_rows + (job - a.n_hub_items);
             const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
-            const double2 s = batch_row_sum(a, rs, re, lane);
-            batch_epilogue(a, r, s, re - rs, lane);
+            const double2 s = batch_row_sum<B>(a, rs, re, lane);
+            if (writer) batch_epilogue<B>(a, r, s, re - rs, cl);
         }
     }
 }
@@ -321,13 +377,13 @@ __global__ void init_onehot_kernel(double* w, const uint32_t* gdeg, const uint32
     w[s] = 1.0 / static_cast<double>(gdeg[s]);
 }
 
-// Batched: column j of W_0 = D^-1 e_{s_j}; matrix pre-zeroed.
+// Batched: column j of W_0 = D^-1 e_{s_j}; matrix [n_pad][B] pre-zeroed.
 __global__ void init_onehot_batch_kernel(double* W, const uint32_t* gdeg, const uint32_t* new_of_old,
-                                         const uint32_t* sources, uint32_t q0, uint32_t count) {
+                                         const uint32_t* sources, uint32_t q0, uint32_t count, uint32_t B) {
     const uint32_t j = threadIdx.x;
     if (j < count) {
         const uint32_t s = new_of_old[sources[q0 + j]];
-        W[static_cast<size_t>(s) * kBatchCols + j] = 1.0 / static_cast<double>(gdeg[s]);
+        W[static_cast<size_t>(s) * B + j] = 1.0 / static_cast<double>(gdeg[s]);
     }
 }
 
@@ -346,15 +402,14 @@ __global__ void unpermute_kernel(double* out, const double* full, const uint32_t
         out[v] = full[new_of_old[v]];
 }
 
-// Batched: out[j][v] = full[new_of_old[v]][j] for j < count.
+// Batched: out[j][v] = full[new_of_old[v]][j] for j < count (full is [n_pad][B]).
 __global__ void unpermute_batch_kernel(double* out, const double* full, const uint32_t* new_of_old,
-                                       uint32_t n, uint32_t count) {
-    const uint32_t lane = threadIdx.x & 63;
-    for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 6; v < n;
-         v += (gridDim.x * blockDim.x) >> 6) {
-        if (lane < count)
-            out[static_cast<size_t>(lane) * n + v] =
-                full[static_cast<size_t>(new_of_old[v]) * kBatchCols + lane];
+                                       uint32_t n, uint32_t count, uint32_t B) {
+    const uint64_t total = static_cast<uint64_t>(n) * count;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t j = static_cast<uint32_t>(i / n), v = static_cast<uint32_t>(i % n);
+        out[i] = full[static_cast<size_t>(new_of_old[v]) * B + j];
     }
 }
 
@@ -377,20 +432,33 @@ __global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, d
 
 // Host-side launch wrappers ---------------------------------------------------
 void launch_step(const StepArgs& a, int grid, cudaStream_t st) {
-    cheby_step_kernel<kStepThreads, kTileEdges><<<grid, kStepThreads, 0, st>>>(a);
+    if (a.tile == kTileLarge)
+        cheby_step_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a);
+    else
+        cheby_step_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a);
 }
-int step_occupancy() {
+int step_occupancy(int tile) {
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileEdges>,
-                                                  kStepThreads, 0);
+    if (tile == kTileLarge)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileLarge>,
+                                                      kStepThreads, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileSmall>,
+                                                      kStepThreads, 0);
     return blocks;
 }
-void launch_batch(const BatchArgs& a, int grid, cudaStream_t st) {
-    cheby_batch_kernel<<<grid, kBatchThreads, 0, st>>>(a);
+void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    switch (B) {
+    case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 16: cheby_batch_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 32: cheby_batch_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
+    default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    }
 }
 int batch_occupancy() {
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel, kBatchThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel<64>, kBatchThreads, 0);
     return blocks;
 }
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
@@ -398,8 +466,8 @@ void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, con
     init_onehot_kernel<<<1, 1, 0, st>>>(w, gdeg, no, src, q);
 }
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                              uint32_t q0, uint32_t count, cudaStream_t st) {
-    init_onehot_batch_kernel<<<1, kBatchCols, 0, st>>>(W, gdeg, no, src, q0, count);
+                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st) {
+    init_onehot_batch_kernel<<<1, 64, 0, st>>>(W, gdeg, no, src, q0, count, B);
 }
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
                        uint32_t n, cudaStream_t st) {
@@ -409,8 +477,8 @@ void launch_unpermute(double* out, const double* full, const uint32_t* no, uint3
     unpermute_kernel<<<1184, 256, 0, st>>>(out, full, no, n);
 }
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
-                            uint32_t count, cudaStream_t st) {
-    unpermute_batch_kernel<<<1184, 256, 0, st>>>(out, full, no, n, count);
+                            uint32_t count, uint32_t B, cudaStream_t st) {
+    unpermute_batch_kernel<<<2368, 256, 0, st>>>(out, full, no, n, count, B);
 }
 void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st) {
     mass_steps_kernel<<<K, kStepThreads, 0, st>>>(mp, n_part, steps);

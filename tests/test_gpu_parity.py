@@ -141,15 +141,16 @@ def test_apply_walk_matches_reference(graphs, cpg):
         np.testing.assert_allclose(cpg.apply_walk(g, x), ref.apply_walk(x), rtol=1e-13, atol=1e-15)
 
 
-@pytest.mark.parametrize("nsrc", [1, 10, 64, 70])
-def test_batched_matches_single_source(graphs, cpg, nsrc):
+@pytest.mark.parametrize("nsrc,tile", [(1, 64), (10, 64), (64, 64), (70, 64), (3, 3), (9, 8), (20, 16),
+                                       (40, 32)])
+def test_batched_matches_single_source(graphs, cpg, nsrc, tile):
     off, nb = graphs["chunglu"]
     g = cpg.Graph.from_csr(off, nb)
     ref = _ref_graph(off, nb)
     kernel = cpg.Kernel.hkpr(5.0)
     K = cpg.plan_truncation(kernel, 1e-8).cheby_steps
     src = ref.select_sources_uniform(nsrc, 11)
-    got, st = cpg.cheby_power_many(g, kernel, src, K, batched=True)
+    got, st = cpg.cheby_power_many(g, kernel, src, K, batched=True, tile=tile)
     assert got.shape == (nsrc, g.node_count())
     for j in range(0, nsrc, max(1, nsrc // 5)):
         want, _, _ = ref.cheby_power(HKPR, 5.0, int(src[j]), K)
@@ -237,3 +238,33 @@ def test_graph_from_device_csr(cpg, gpu):
     est = cpg.cheby_power(dg, cpg.Kernel.ppr(0.2), 11, 26)
     want, _, _ = ref.cheby_power(PPR, 0.2, 11, 26)
     assert_parity(est.values, want)
+
+
+@pytest.mark.parametrize("tile", ["1024", "4096"])
+def test_both_tile_widths(cpg, gpu, tile, monkeypatch):
+    """Force each tile width (CPG_TILE) on a graph with hubs split into pieces."""
+    monkeypatch.setenv("CPG_TILE", tile)
+    off, nb = cpg.gen_chunglu(60000, 900000, 2.1, 30.0, 20000, seed=8)
+    dg = cpg.DeviceGraph.from_host(off, nb, 0)
+    ref = _ref_graph(off, nb)
+    assert dg.info.n_hubs > 0
+    for fam, par, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15)):
+        kern = cpg.Kernel.ppr(par) if fam == PPR else cpg.Kernel.hkpr(par)
+        for s in (0, 1, 12345, dg.n - 1):
+            est = cpg.cheby_power(dg, kern, s, K)
+            want, _, _ = ref.cheby_power(fam, par, s, K)
+            assert_parity(est.values, want)
+
+
+def test_large_graph_default_tiles(cpg, gpu):
+    """A graph big enough for the large-tile table (>= 4096*148*8 edges)."""
+    off, nb = cpg.gen_rmat(18, 16 << 18, seed=12)
+    assert len(nb) >= 4096 * 148 * 8
+    dg = cpg.DeviceGraph.from_host(off, nb, 0)
+    ref = _ref_graph(off, nb)
+    src = ref.select_sources_uniform(3, 1)
+    got, st = cpg.cheby_power_many(dg, cpg.Kernel.ppr(0.2), src, 26)
+    for j, s in enumerate(src):
+        want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
+        assert_parity(got[j], want)
+    assert st.mass_err_max <= 1e-9
