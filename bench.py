@@ -39,15 +39,15 @@ PPR, HKPR = 0, 1
 CONFIGS = {
     1: dict(name="rmat-s16-ef8 ppr", gen="rmat", scale=16, samples=8 << 16, seed=1,
             family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
-    2: dict(name="chunglu-dblp-size hkpr", gen="chunglu", n_ids=317_080, samples=1_052_000, exponent=2.5,
+    2: dict(name="chunglu-dblp-size hkpr", gen="chunglu", n_ids=317_080, samples=1_050_000, exponent=2.5,
             mean=6.6, cap=0, seed=2, family=HKPR, param=5.0, eps=1e-8, sources=64, mode="single"),
-    3: dict(name="chunglu-livejournal-size ppr", gen="chunglu", n_ids=4_846_609, samples=44_200_000,
+    3: dict(name="chunglu-livejournal-size ppr", gen="chunglu", n_ids=4_846_609, samples=43_200_000,
             exponent=2.3, mean=17.8, cap=20_000, seed=3, family=PPR, param=0.2, eps=1e-8, sources=64,
             mode="single"),
     4: dict(name="chunglu-orkut-size hkpr batched", gen="chunglu", n_ids=3_072_626, samples=121_000_000,
             exponent=2.1, mean=76.0, cap=33_000, seed=4, family=HKPR, param=5.0, eps=1e-8, sources=64,
             mode="batched"),
-    5: dict(name="rmat-friendster-size ppr", gen="rmat", scale=26, samples=2_280_000_000, seed=5,
+    5: dict(name="rmat-friendster-size ppr", gen="rmat", scale=27, samples=1_840_000_000, seed=5,
             family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
 }
 DEFAULT_CONFIG = 3

@@ -320,14 +320,17 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         const size_t cols = B;
         if (mode == 2) {
             require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
-            ensure_batch_tables(g);
-            if (g->bhub_cols < B) {
+            ensure_batch_tables(g, static_cast<int>(B));
+            const size_t need = static_cast<size_t>(g->n_bhub_items) * B;
+            if (g->bhub_items_cap < need || !g->bhub_partial) {
                 dfree(g->bhub_partial);
-                g->bhub_partial = dalloc<double>(static_cast<size_t>(g->n_bhub_items) * B);
-                g->bhub_cols = B;
+                g->bhub_partial = dalloc<double>(need);
+                g->bhub_items_cap = need;
             }
-            if (!g->bhub_count) {
+            if (g->bhub_count_cap < g->n_bhubs || !g->bhub_count) {
+                dfree(g->bhub_count);
                 g->bhub_count = dalloc<unsigned int>(g->n_bhubs);
+                g->bhub_count_cap = g->n_bhubs;
                 CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_bhubs)));
             }
         }

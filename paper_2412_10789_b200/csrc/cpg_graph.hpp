@@ -26,6 +26,8 @@ struct cpg_graph {
     int tile = 0;                   // kTileSmall / kTileLarge
     cpg::WorkItem* bitems = nullptr; // batched hub pieces
     uint32_t n_bhubs = 0, n_bhub_items = 0;
+    int bitems_width = 0;           // B the batched hub table was built for
+    size_t bhub_items_cap = 0, bhub_count_cap = 0;
 
     double* hub_partial = nullptr;  // [n_hub_items]
     unsigned int* hub_count = nullptr;  // [n_hubs]
@@ -64,7 +66,7 @@ namespace cpg {
 
 // graph_build.cu
 void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st);
-void ensure_batch_tables(cpg_graph* g);
+void ensure_batch_tables(cpg_graph* g, int B);
 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st);

@@ -281,12 +281,16 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
     CPG_CUDA(cudaGetLastError());
 }
 
-void ensure_batch_tables(cpg_graph* g) {
-    if (g->bitems) return;
+void ensure_batch_tables(cpg_graph* g, int B) {
+    if (g->bitems && g->bitems_width == B) return;
+    if (g->bitems) cudaFree(g->bitems);
+    g->bitems = nullptr;
     uint32_t n_hub = 0, n_items = 0;
-    build_hub_items(g->rowptr, g->n_loc, kBatchHubEdges, kBatchHubEdges, &g->bitems, &n_hub, &n_items, 0, g->stream);
+    const int64_t hb = batch_hub_edges(B);
+    build_hub_items(g->rowptr, g->n_loc, hb, hb, &g->bitems, &n_hub, &n_items, 0, g->stream);
     g->n_bhubs = n_hub;
     g->n_bhub_items = n_items;
+    g->bitems_width = B;
     CPG_CUDA(cudaGetLastError());
 }
 

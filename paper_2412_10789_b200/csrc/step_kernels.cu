@@ -242,31 +242,67 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
 
 // ---------------------------------------------------------------------------
 // Batched step: B sources per tile (B in {4,8,16,32,64}), iterates row-major
-// [n_pad][B] fp64.  One warp per row job.  L = B/2 lanes cover one gathered
-// row (a double2 each), so one warp instruction gathers EPW = 32/L neighbour
-// rows: every edge costs ONE B*8-byte row fetch shared by B queries (vs one
-// 8-byte fetch per query in the single-source step).  Lane sub-group s sums
-// edges s, s+EPW, ... in order; sub-groups are combined by a fixed xor tree,
-// so results are bit-reproducible.  Rows above kBatchHubEdges are split into
-// pieces with the ordered last-arriver reduction.
+// [n_pad][B] fp64.  A row is owned by a lane sub-group of L = B/2 lanes (one
+// double2 each), so a warp works on RPW = 32/L rows at once and every edge
+// costs ONE B*8-byte row fetch shared by the B queries (vs one 8-byte fetch per
+// query in the single-source step).  Per row: the epilogue operands are
+// prefetched with the first index chunk, then 32-edge chunks: each lane loads
+// 32/L indices (coalesced within the sub-group), and U row gathers per lane are
+// kept in flight.  Edge order within a row is sequential, so results are
+// bit-reproducible.  Rows above kBatchHubEdges are split into pieces combined
+// by the ordered last-arriver reduction.
 // ---------------------------------------------------------------------------
 template <int B>
-__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d, int cl) {
+struct BatchJob {
+    uint32_t r;
+    int64_t e0, e1, d;
+    uint32_t slot, piece, P;
+    bool valid, hub;
+};
+
+template <int B>
+__device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t job, uint32_t n_jobs) {
+    BatchJob<B> j;
+    j.valid = job < n_jobs;
+    j.hub = false;
+    j.r = 0;
+    j.e0 = j.e1 = j.d = 0;
+    j.slot = j.piece = j.P = 0;
+    if (!j.valid) return j;
+    if (job < a.n_hub_items) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + job);
+        j.hub = true;
+        j.r = raw.x;
+        j.slot = raw.y;
+        j.piece = raw.z;
+        const int64_t rs = a.rowptr[j.r], re = a.rowptr[j.r + 1];
+        j.d = re - rs;
+        constexpr int HB = batch_hub_edges(B);
+        j.e0 = rs + static_cast<int64_t>(j.piece) * HB;
+        j.e1 = min(j.e0 + HB, re);
+        j.P = static_cast<uint32_t>((j.d + HB - 1) / HB);
+    } else {
+        j.r = a.hub_rows + (job - a.n_hub_items);
+        j.e0 = a.rowptr[j.r];
+        j.e1 = a.rowptr[j.r + 1];
+        j.d = j.e1 - j.e0;
+    }
+    return j;
+}
+
+template <int B>
+__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d, int cl,
+                                               double2 wp, double2 ac) {
     const uint32_t gr = a.row0 + r;
-    double2* wio = reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B) + cl;
-    double2* accp = reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * B) + cl;
     double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
     if (d > 0) {
         const double dd = static_cast<double>(d);
-        if (a.first) {
-            const double2 w0 = reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl];
+        if (a.first) {  // wp holds w_0 of this row
             w_new.x = y.x / dd;
             w_new.y = y.y / dd;
-            acc_new.x = a.coeffs[0] * w0.x + a.coeffs[1] * w_new.x;
-            acc_new.y = a.coeffs[0] * w0.y + a.coeffs[1] * w_new.y;
+            acc_new.x = a.coeffs[0] * wp.x + a.coeffs[1] * w_new.x;
+            acc_new.y = a.coeffs[0] * wp.y + a.coeffs[1] * w_new.y;
         } else {
-            const double2 wp = *wio;
-            const double2 ac = *accp;
             const double ck = a.coeffs[a.k];
             w_new.x = 2.0 * y.x / dd - wp.x;
             w_new.y = 2.0 * y.y / dd - wp.y;
@@ -274,95 +310,95 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, d
             acc_new.y = ac.y + ck * w_new.y;
         }
     }
-    *wio = w_new;
+    reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl] = w_new;
     if (a.last) {
         const double dd = static_cast<double>(d);
         reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * B)[cl] = make_double2(dd * acc_new.x, dd * acc_new.y);
     } else {
-        *accp = acc_new;
+        reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * B)[cl] = acc_new;
     }
 }
 
-// Sum of W_k rows over edges [e0, e1), for this lane's two columns, reduced
-// over the EPW lane sub-groups (result valid in every lane).
 template <int B>
-__device__ __forceinline__ double2 batch_row_sum(const BatchArgs& a, int64_t e0, int64_t e1, int lane) {
-    constexpr int L = B / 2;
-    constexpr int EPW = 32 / L;
-    constexpr int U = (EPW >= 8) ? 4 : 8;  // gathers in flight per lane
-    const int sub = lane / L, cl = lane % L;
-    double2 s = {0.0, 0.0};
-    for (int64_t base = e0; base < e1; base += 32) {
-        const int m = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
-        const uint32_t c = lane < m ? ld_index(a.col + base + lane) : 0u;
-        for (int j = 0; j < m; j += EPW * U) {
-            double2 v[U];
-#pragma unroll
-            for (int t = 0; t < U; ++t) {
-                const int jj = j + t * EPW + sub;
-                const uint32_t u = __shfl_sync(0xffffffffu, c, jj & 31);
-                v[t] = jj < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int t = 0; t < U; ++t) {
-                s.x += v[t].x;
-                s.y += v[t].y;
-            }
-        }
+__device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, int cl, double2& wp, double2& ac) {
+    const uint32_t gr = a.row0 + r;
+    if (a.first) {
+        wp = reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl];
+        ac = make_double2(0.0, 0.0);
+    } else {
+        wp = reinterpret_cast<const double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl];
+        ac = reinterpret_cast<const double2*>(a.acc + static_cast<size_t>(r) * B)[cl];
     }
-#pragma unroll
-    for (int o = L; o < 32; o <<= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-    }
-    return s;
 }
 
 template <int B>
-__global__ void __launch_bounds__(kBatchThreads) cheby_batch_kernel(const BatchArgs a) {
-    constexpr int L = B / 2;
+__global__ void __launch_bounds__(kBatchThreads, B == 64 ? 4 : 3) cheby_batch_kernel(const BatchArgs a) {
+    constexpr int L = B / 2;      // lanes per row slot
+    constexpr int RPW = 32 / L;   // row slots per warp
+    constexpr int V = 32 / L;     // indices per lane per 32-edge chunk
+    constexpr int U = 8;          // row gathers in flight per lane
     const int lane = threadIdx.x & 31;
-    const int cl = lane % L;
-    const bool writer = lane < L;
+    const int slot = lane / L, cl = lane % L;
+    const unsigned smask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_jobs = a.n_hub_items + (a.n_loc - a.hub_rows);
-    for (uint32_t job = wg; job < n_jobs; job += nw) {
-        if (job < a.n_hub_items) {
-            const WorkItem it = a.hub_items[job];
-            const uint32_t r = it.a, slot_base = it.b, hub = it.a;
-            const uint32_t piece = static_cast<uint32_t>(it.c & 0xffffffffu);
-            const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
-            const int64_t d = re - rs;
-            const int64_t p0 = rs + static_cast<int64_t>(piece) * kBatchHubEdges;
-            const int64_t p1 = min(p0 + kBatchHubEdges, re);
-            const uint32_t P = static_cast<uint32_t>((d + kBatchHubEdges - 1) / kBatchHubEdges);
-            const double2 s = batch_row_sum<B>(a, p0, p1, lane);
-            if (writer)
-                reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(slot_base + piece) * B)[cl] = s;
+    for (uint32_t base_job = wg * RPW; base_job < n_jobs; base_job += nw * RPW) {
+        const BatchJob<B> j = batch_job<B>(a, base_job + slot, n_jobs);
+        double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
+        if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
+        double2 s = {0.0, 0.0};
+        for (int64_t e = j.e0; __any_sync(0xffffffffu, e < j.e1); e += 32) {
+            const int m = static_cast<int>(e < j.e1 ? (j.e1 - e < 32 ? j.e1 - e : 32) : 0);
+            uint32_t c[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int t = v * L + cl;
+                c[v] = t < m ? ld_index(a.col + e + t) : 0u;
+            }
+#pragma unroll
+            for (int t0 = 0; t0 < 32; t0 += U) {
+                if (!__any_sync(0xffffffffu, t0 < m)) break;
+                double2 val[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int t = t0 + q;
+                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    s.x += val[q].x;
+                    s.y += val[q].y;
+                }
+            }
+        }
+        bool do_epi = j.valid && !j.hub;
+        double2 y = s;
+        if (__any_sync(0xffffffffu, j.hub)) {
+            if (j.hub)
+                reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(j.slot + j.piece) * B)[cl] = s;
             __threadfence();
             __syncwarp();
             unsigned prev = 0;
-            if (lane == 0) prev = atomicAdd(&a.hub_count[hub], 1u);
-            prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev == P - 1) {
+            if (j.hub && cl == 0) prev = atomicAdd(&a.hub_count[j.r], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, slot * L);
+            if (j.hub && prev == j.P - 1) {
                 __threadfence();
-                double2 y = {0.0, 0.0};
-                for (uint32_t p = 0; p < P; ++p) {
-                    const double2 v = __ldcg(
-                        reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(slot_base + p) * B) + cl);
+                y = make_double2(0.0, 0.0);
+                for (uint32_t p = 0; p < j.P; ++p) {
+                    const double2 v =
+                        __ldcg(reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(j.slot + p) * B) + cl);
                     y.x += v.x;
                     y.y += v.y;
                 }
-                if (lane == 0) a.hub_count[hub] = 0u;
-                if (writer) batch_epilogue<B>(a, r, y, d, cl);
+                if (cl == 0) a.hub_count[j.r] = 0u;
+                batch_prefetch<B>(a, j.r, cl, wp, ac);
+                do_epi = true;
             }
-        } else {
-            const uint32_t r = a.hub_rows + (job - a.n_hub_items);
-            const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
-            const double2 s = batch_row_sum<B>(a, rs, re, lane);
-            if (writer) batch_epilogue<B>(a, r, s, re - rs, cl);
         }
+        (void)smask;
+        if (do_epi) batch_epilogue<B>(a, j.r, y, j.d, cl, wp, ac);
     }
 }
 
