@@ -287,6 +287,18 @@ class DeviceGraph:
             pass
 
 
+def shard_plan(offsets, nranks: int):
+    """Host restatement of the device relabel + row partition: (new_of_old[n], n_local).
+
+    Node order (degree desc, id asc); order position i -> rank i % R, local row i // R."""
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = len(off) - 1
+    out = np.empty(n, dtype=np.uint32)
+    nl = ctypes.c_uint32()
+    _check(L.lib().cpg_shard_plan(_u64p(off), n, nranks, _u32p(out), ctypes.byref(nl)))
+    return out, int(nl.value)
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(L.lib().cpg_nccl_unique_id(buf))
