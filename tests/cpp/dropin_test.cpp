@@ -77,8 +77,8 @@ int main() {
         const auto plan = plan_truncation(k, 1e-8);
         const auto est = cuda::cheby_power(path3, k, 1, plan.cheby_steps);
         // exact: (I - 0.8 P) y = 0.2 e_1 on the path 0-1-2  =>  y = [0.25, 0.5, 0.25] * ... solve:
-        // P = A D^-1: y0 = 0.8*0.5*y1, y2 = 0.8*0.5*y1, y1 = 0.2 + 0.8*(y0 + y2) => y1 = 0.2/(1-0.32)
-        const double y1 = 0.2 / (1.0 - 0.32), y0 = 0.4 * y1;
+        // P = A D^-1: y0 = 0.8*0.5*y1, y2 = 0.8*0.5*y1, y1 = 0.2 + 0.8*(y0 + y2) => y1 = 0.2/(1-0.64)
+        const double y1 = 0.2 / (1.0 - 0.64), y0 = 0.4 * y1;
         const double l2 = std::sqrt(std::pow(est.values[0] - y0, 2) + std::pow(est.values[1] - y1, 2) +
                                     std::pow(est.values[2] - y0, 2));
         CHECK(l2 < 1e-8);
