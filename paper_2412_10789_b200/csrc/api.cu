@@ -233,6 +233,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.col = g->col;
         b.hub_items = g->bitems;
         b.n_hub_items = g->n_bhub_items;
+        b.n_items = g->n_bitems;
         b.hub_rows = g->n_bhubs;
         b.n_loc = g->n_loc;
         b.w_cur = (k & 1) ? g->w_a : g->w_b;
@@ -247,7 +248,11 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.first = k == 1;
         b.last = k == K;
         if (prof) prof->before(st);
-        launch_batch(b, static_cast<int>(B), g->batch_grid, st);
+        const int grid = batch_uses_tiles(static_cast<int>(B))
+                             ? std::max<int>(1, std::min<int>(static_cast<int>(g->n_bitems),
+                                                              batch_staged_occupancy(static_cast<int>(B)) * g->sm_count))
+                             : g->batch_grid;
+        launch_batch(b, static_cast<int>(B), grid, st);
         if (prof) prof->after(st);
         ++launches;
         if (g->nranks > 1)

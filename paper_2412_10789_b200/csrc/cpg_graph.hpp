@@ -27,6 +27,7 @@ struct cpg_graph {
     cpg::WorkItem* bitems = nullptr; // batched hub pieces
     uint32_t n_bhubs = 0, n_bhub_items = 0;
     int bitems_width = 0;           // B the batched hub table was built for
+    uint32_t n_bitems = 0;          // batched items (hub pieces + tiles when tiled)
     size_t bhub_items_cap = 0, bhub_count_cap = 0;
 
     double* hub_partial = nullptr;  // [n_hub_items]
@@ -73,6 +74,7 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st);
 int step_occupancy(int tile);
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int batch_occupancy();
+int batch_staged_occupancy(int B);
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,

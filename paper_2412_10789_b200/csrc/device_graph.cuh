@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 namespace cpg {
 
@@ -32,6 +33,25 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
 constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
+// Staged (cp.async) batched tiles for B <= 32: a tile stages the gathered
+// rows of <= batch_tile_edges(B) edges (kBatchTileBytes of shared memory per
+// buffer, double-buffered) and has <= batch_tile_rows(B) rows (2 epilogue rows
+// per row slot of B/2 lanes).
+constexpr int kBatchTileBytes = 32768;
+// Measured on B200 (profiles/r01): the register-pipelined slot kernel beats the
+// staged kernel at every width on configs 3 and 5, so staging is opt-in
+// (CPG_BATCH_STAGED=1) and only wins on tiny graphs (config 1).
+__host__ inline bool batch_uses_tiles(int B) {
+    static const bool staged = [] {
+        const char* e = std::getenv("CPG_BATCH_STAGED");
+        return e && e[0] == '1';
+    }();
+    return staged && B <= 32;
+}
+__host__ __device__ constexpr int batch_tile_edges(int B) { return kBatchTileBytes / (8 * B); }
+__host__ __device__ constexpr int batch_tile_rows(int B) {
+    return (2 * kBatchThreads / (B / 2)) < 256 ? (2 * kBatchThreads / (B / 2)) : 256;
+}
 // Hub piece for width B: one row slot (B/2 lanes) handles a piece, so the
 // piece shrinks with the slot width to keep pieces equally long in time.
 __host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges * B / 64; }
@@ -40,7 +60,9 @@ __host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges
 //   tile: a = first row, b = end row,
 //         c = first edge | edge count << 40 | lg(lane group) << 54
 //   hub piece (bit 63 of c set): a = row (== hub index, hubs are the row
-//         prefix), b = first partial slot of this hub, c = piece | 1 << 63
+//         prefix), b = first partial slot of this hub,
+//         c = first edge | edge count << 40 | 1 << 63
+//         (piece index = (first edge - rowptr[row]) / piece size)
 struct __align__(16) WorkItem {
     uint32_t a, b;
     uint64_t c;
@@ -49,6 +71,8 @@ constexpr uint64_t kHubBit = 1ull << 63;
 __host__ __device__ inline uint64_t tile_code(uint64_t e0, uint32_t cnt, uint32_t lg) {
     return e0 | (static_cast<uint64_t>(cnt) << 40) | (static_cast<uint64_t>(lg) << 54);
 }
+__host__ __device__ inline int64_t code_e0(uint64_t c) { return static_cast<int64_t>(c & ((1ull << 40) - 1)); }
+__host__ __device__ inline int code_cnt(uint64_t c) { return static_cast<int>((c >> 40) & 0x3fff); }
 
 struct StepArgs {
     const int64_t* rowptr;
@@ -73,8 +97,9 @@ struct StepArgs {
 struct BatchArgs {
     const int64_t* rowptr;
     const uint32_t* col;
-    const WorkItem* hub_items;  // hub pieces (row, slot_base, piece, hub<<1|1)
+    const WorkItem* hub_items;  // hub pieces (row, slot_base, piece | hub bit); tiled: + row tiles
     uint32_t n_hub_items;
+    uint32_t n_items;           // tiled kernel: hub pieces + tiles
     uint32_t hub_rows;          // rows [0, hub_rows) are hubs
     uint32_t n_loc;
     const double* w_cur;        // [n_pad][64]

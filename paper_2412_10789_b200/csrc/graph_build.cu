@@ -104,19 +104,28 @@ __global__ void k_pieces(const int64_t* rowptr, uint32_t n_hub, int64_t piece, u
         P[j] = j < n_hub ? static_cast<uint32_t>((rowptr[j + 1] - rowptr[j] + piece - 1) / piece) : 0u;
 }
 
-__global__ void k_hub_items(const uint32_t* P, const uint32_t* base, uint32_t n_hub, WorkItem* items) {
+// Hub piece p of hub row j: {row, first partial slot of the hub, first edge | edge count | hub bit}.
+__global__ void k_hub_items(const int64_t* rowptr, const uint32_t* P, const uint32_t* base, uint32_t n_hub,
+                            int64_t piece, WorkItem* items) {
     const int lane = threadIdx.x & 31;
-    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5)
-        for (uint32_t p = lane; p < P[j]; p += 32) items[base[j] + p] = WorkItem{j, base[j], p | kHubBit};
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t rs = rowptr[j], d = rowptr[j + 1] - rs;
+        for (uint32_t p = lane; p < P[j]; p += 32) {
+            const int64_t e0 = rs + static_cast<int64_t>(p) * piece;
+            const uint32_t cnt = static_cast<uint32_t>(min(piece, d - static_cast<int64_t>(p) * piece));
+            items[base[j] + p] = WorkItem{j, base[j], tile_code(static_cast<uint64_t>(e0), cnt, 0) | kHubBit};
+        }
+    }
 }
 
 // A row starts a tile when its first edge falls in a new chunk of tile/2 edges
 // (or every kTileMaxRows rows).  All rows of a tile start inside one chunk and
 // non-hub rows have <= tile/2 edges, so a tile holds <= tile edges.
-__global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, int64_t chunk, uint8_t* flags) {
+__global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, int64_t chunk, uint32_t max_rows,
+                             uint8_t* flags) {
     for (uint64_t j = first + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        bool start = (j == first) || ((j - first) % kTileMaxRows == 0) ||
+        bool start = (j == first) || ((j - first) % max_rows == 0) ||
                      (rowptr[j] / chunk != rowptr[j - 1] / chunk);
         flags[j - first] = start ? 1 : 0;
     }
@@ -159,13 +168,54 @@ void build_hub_items(const int64_t* rowptr, uint32_t n_loc, int64_t thr, int64_t
     CPG_CUDA(cudaMemcpyAsync(&total, base + n_hub, sizeof(total), cudaMemcpyDeviceToHost, st));
     CPG_CUDA(cudaStreamSynchronize(st));
     WorkItem* items = dalloc<WorkItem>(static_cast<size_t>(total) + reserve_tail);
-    if (n_hub) k_hub_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(P, base, n_hub, items);
+    if (n_hub)
+        k_hub_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(rowptr, P, base, n_hub, piece, items);
     CPG_CUDA(cudaStreamSynchronize(st));
     cudaFree(P);
     cudaFree(base);
     *out = items;
     *n_hub_out = n_hub;
     *n_items_out = total;
+}
+
+// Work table over local rows: hub pieces (rows with deg > chunk, split into
+// `piece`-edge pieces) then row tiles (<= 2*chunk edges, <= max_rows rows).
+void build_item_table(const int64_t* rowptr, uint32_t n_loc, int64_t chunk, uint32_t max_rows, int64_t piece,
+                      WorkItem** items_out, uint32_t* n_items_out, uint32_t* n_hubs_out, uint32_t* n_hub_items_out,
+                      cudaStream_t st) {
+    DevTemp tmp;
+    size_t bytes = 0;
+    WorkItem* hub_items = nullptr;
+    uint32_t n_hub = 0, n_hub_items = 0;
+    build_hub_items(rowptr, n_loc, chunk, piece, &hub_items, &n_hub, &n_hub_items, 0, st);
+    uint32_t n_tiles = 0;
+    uint32_t* starts = nullptr;
+    if (n_hub < n_loc) {
+        const uint32_t rows = n_loc - n_hub;
+        uint8_t* flags = dalloc<uint8_t>(rows);
+        starts = dalloc<uint32_t>(rows);
+        unsigned int* d_sel = dalloc<unsigned int>(1);
+        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(rowptr, n_hub, n_loc, chunk, max_rows, flags);
+        cub::CountingInputIterator<uint32_t> it(n_hub);
+        cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);
+        tmp.ensure(bytes);
+        CPG_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, starts, d_sel, rows, st));
+        CPG_CUDA(cudaMemcpyAsync(&n_tiles, d_sel, sizeof(n_tiles), cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(flags);
+        cudaFree(d_sel);
+    }
+    WorkItem* items = dalloc<WorkItem>(static_cast<size_t>(n_hub_items) + n_tiles);
+    if (n_hub_items)
+        CPG_CUDA(cudaMemcpyAsync(items, hub_items, sizeof(WorkItem) * n_hub_items, cudaMemcpyDeviceToDevice, st));
+    if (n_tiles) k_tile_items<<<grid_for(n_tiles), kT, 0, st>>>(rowptr, starts, n_tiles, n_loc, items + n_hub_items);
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(hub_items);
+    if (starts) cudaFree(starts);
+    *items_out = items;
+    *n_items_out = n_hub_items + n_tiles;
+    *n_hubs_out = n_hub;
+    *n_hub_items_out = n_hub_items;
 }
 
 } // namespace
@@ -244,40 +294,9 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
         const int t = std::atoi(force);
         if (t == kTileSmall || t == kTileLarge) g->tile = t;
     }
-    const int64_t chunk = g->tile / 2;
-    WorkItem* hub_items = nullptr;
-    uint32_t n_hub = 0, n_hub_items = 0;
-    build_hub_items(g->rowptr, n_loc, chunk, kHubPieceEdges, &hub_items, &n_hub, &n_hub_items, 0, st);
-    uint32_t n_tiles = 0;
-    uint32_t* starts = nullptr;
-    if (n_hub < n_loc) {
-        const uint32_t rows = n_loc - n_hub;
-        uint8_t* flags = dalloc<uint8_t>(rows);
-        starts = dalloc<uint32_t>(rows);
-        unsigned int* d_sel = dalloc<unsigned int>(1);
-        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(g->rowptr, n_hub, n_loc, chunk, flags);
-        cub::CountingInputIterator<uint32_t> it(n_hub);
-        bytes = 0;
-        cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);
-        tmp.ensure(bytes);
-        CPG_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, starts, d_sel, rows, st));
-        CPG_CUDA(cudaMemcpyAsync(&n_tiles, d_sel, sizeof(n_tiles), cudaMemcpyDeviceToHost, st));
-        CPG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(flags);
-        cudaFree(d_sel);
-    }
-    g->n_hubs = n_hub;
-    g->n_hub_items = n_hub_items;
-    g->n_tiles = n_tiles;
-    g->n_items = n_hub_items + n_tiles;
-    g->items = dalloc<WorkItem>(g->n_items);
-    if (n_hub_items)
-        CPG_CUDA(cudaMemcpyAsync(g->items, hub_items, sizeof(WorkItem) * n_hub_items, cudaMemcpyDeviceToDevice, st));
-    if (n_tiles)
-        k_tile_items<<<grid_for(n_tiles), kT, 0, st>>>(g->rowptr, starts, n_tiles, n_loc, g->items + n_hub_items);
-    CPG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(hub_items);
-    if (starts) cudaFree(starts);
+    build_item_table(g->rowptr, n_loc, g->tile / 2, kTileMaxRows, kHubPieceEdges, &g->items, &g->n_items, &g->n_hubs,
+                     &g->n_hub_items, st);
+    g->n_tiles = g->n_items - g->n_hub_items;
     CPG_CUDA(cudaGetLastError());
 }
 
@@ -285,11 +304,22 @@ void ensure_batch_tables(cpg_graph* g, int B) {
     if (g->bitems && g->bitems_width == B) return;
     if (g->bitems) cudaFree(g->bitems);
     g->bitems = nullptr;
-    uint32_t n_hub = 0, n_items = 0;
-    const int64_t hb = batch_hub_edges(B);
-    build_hub_items(g->rowptr, g->n_loc, hb, hb, &g->bitems, &n_hub, &n_items, 0, g->stream);
-    g->n_bhubs = n_hub;
-    g->n_bhub_items = n_items;
+    if (batch_uses_tiles(B)) {
+        // staged tiles: <= E(B) edges and <= R(B) rows, hubs split in E-edge pieces
+        uint32_t n_items = 0, n_hub = 0, n_hub_items = 0;
+        build_item_table(g->rowptr, g->n_loc, batch_tile_edges(B) / 2, batch_tile_rows(B), batch_tile_edges(B),
+                         &g->bitems, &n_items, &n_hub, &n_hub_items, g->stream);
+        g->n_bitems = n_items;
+        g->n_bhubs = n_hub;
+        g->n_bhub_items = n_hub_items;
+    } else {
+        uint32_t n_hub = 0, n_items = 0;
+        const int64_t hb = batch_hub_edges(B);
+        build_hub_items(g->rowptr, g->n_loc, hb, hb, &g->bitems, &n_hub, &n_items, 0, g->stream);
+        g->n_bhubs = n_hub;
+        g->n_bhub_items = n_items;
+        g->n_bitems = n_items;
+    }
     g->bitems_width = B;
     CPG_CUDA(cudaGetLastError());
 }

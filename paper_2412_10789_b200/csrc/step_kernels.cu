@@ -163,12 +163,12 @@ template <int THREADS>
 __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it, double* red,
                                             int* flag, double& mass) {
     constexpr int PER = kHubPieceEdges / THREADS;
-    const uint32_t r = it.a, slot_base = it.b;
-    const uint32_t piece = static_cast<uint32_t>(it.c & 0xffffffffu), hub = it.a;
+    const uint32_t r = it.a, slot_base = it.b, hub = it.a;
+    const int64_t p0 = code_e0(it.c);
+    const int64_t p1 = p0 + code_cnt(it.c);
     const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
     const int64_t d = re - rs;
-    const int64_t p0 = rs + static_cast<int64_t>(piece) * kHubPieceEdges;
-    const int64_t p1 = min(p0 + kHubPieceEdges, re);
+    const uint32_t piece = static_cast<uint32_t>((p0 - rs) / kHubPieceEdges);
     const uint32_t P = static_cast<uint32_t>((d + kHubPieceEdges - 1) / kHubPieceEdges);
 
     uint32_t idx[PER];
@@ -274,12 +274,13 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
         j.hub = true;
         j.r = raw.x;
         j.slot = raw.y;
-        j.piece = raw.z;
+        const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        j.e0 = code_e0(c);
+        j.e1 = j.e0 + code_cnt(c);
         const int64_t rs = a.rowptr[j.r], re = a.rowptr[j.r + 1];
         j.d = re - rs;
         constexpr int HB = batch_hub_edges(B);
-        j.e0 = rs + static_cast<int64_t>(j.piece) * HB;
-        j.e1 = min(j.e0 + HB, re);
+        j.piece = static_cast<uint32_t>((j.e0 - rs) / HB);
         j.P = static_cast<uint32_t>((j.d + HB - 1) / HB);
     } else {
         j.r = a.hub_rows + (job - a.n_hub_items);
@@ -403,6 +404,229 @@ __global__ void __launch_bounds__(kBatchThreads, B == 64 ? 4 : 3) cheby_batch_ke
 }
 
 // ---------------------------------------------------------------------------
+// Staged batched step (B <= 32): persistent CTAs walk the batched item table
+// (hub pieces, then row tiles).  For each item the gathered neighbour rows
+// (E = 32 KB / (8B) edges x B columns) are copied HBM/L2 -> shared memory with
+// cp.async (16 B per copy, no register staging), double-buffered so the copies
+// of item t+1 are in flight while item t is reduced.  In-flight bytes are
+// bounded by shared memory (2 x 32 KB per CTA), not by registers.  Row slots of
+// L = B/2 lanes then sum their rows' staged vectors in edge order
+// (deterministic) and run the fused epilogue.  Hub pieces reduce over their E
+// edges (fixed slot order) and use the ordered last-arriver combine.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+template <int B>
+struct StagedTile {
+    static constexpr int L = B / 2;                  // lanes (double2 columns) per row slot
+    static constexpr int SLOTS = kBatchThreads / L;  // row slots per CTA
+    static constexpr int E = batch_tile_edges(B);    // staged edges per item
+    static constexpr int R = batch_tile_rows(B);     // rows per tile
+    static constexpr int RPS = R / SLOTS;            // epilogue rows per slot
+    static constexpr int PER = E * L / kBatchThreads; // 16-B copies per thread per item
+    double2 buf[2][E][L];
+    int64_t rp[2][R + 1];
+    double2 red[SLOTS][L];
+    int flag;
+};
+
+// Raw 16-B work item; fields decoded on use (keeps the 3-deep pipeline in registers).
+struct ItemInfo {
+    uint32_t a, b;
+    uint64_t c;
+    __device__ __forceinline__ bool hub() const { return (c & kHubBit) != 0; }
+    __device__ __forceinline__ uint32_t rb() const { return a; }
+    __device__ __forceinline__ uint32_t re() const { return hub() ? a + 1 : b; }
+    __device__ __forceinline__ uint32_t slot() const { return b; }
+    __device__ __forceinline__ int64_t e0() const { return code_e0(c); }
+    __device__ __forceinline__ int cnt() const { return code_cnt(c); }
+};
+
+template <int B>
+__device__ __forceinline__ ItemInfo decode_item(const BatchArgs& a, uint32_t i) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + i);
+    ItemInfo it;
+    it.a = raw.x;
+    it.b = raw.y;
+    it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+    return it;
+}
+
+// Issue the cp.async copies of one item into buffer `b`, given its column ids.
+template <int B>
+__device__ __forceinline__ void stage_item(const BatchArgs& a, StagedTile<B>& sm, int b, const ItemInfo& it,
+                                           const uint32_t (&cols)[StagedTile<B>::PER]) {
+    using T = StagedTile<B>;
+    const int cnt = it.cnt();
+#pragma unroll
+    for (int i = 0; i < T::PER; ++i) {
+        const int k = i * kBatchThreads + threadIdx.x;
+        const int e = k / T::L, part = k % T::L;
+        if (e < cnt) cp_async16(&sm.buf[b][e][part], a.w_cur + static_cast<size_t>(cols[i]) * B + 2 * part);
+    }
+    if (!it.hub()) {
+        const int nr = static_cast<int>(it.re() - it.rb());
+        for (int j = threadIdx.x; j <= nr; j += kBatchThreads) cp_async8(&sm.rp[b][j], a.rowptr + it.rb() + j);
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void load_cols(const BatchArgs& a, const ItemInfo& it,
+                                          uint32_t (&cols)[StagedTile<B>::PER]) {
+    using T = StagedTile<B>;
+    const int cnt = it.cnt();
+    const uint32_t* colp = a.col + it.e0();
+#pragma unroll
+    for (int i = 0; i < T::PER; ++i) {
+        const int e = (i * kBatchThreads + static_cast<int>(threadIdx.x)) / T::L;
+        cols[i] = e < cnt ? ld_index(colp + e) : 0u;
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void reduce_item(const BatchArgs& a, StagedTile<B>& sm, int b, const ItemInfo& it) {
+    using T = StagedTile<B>;
+    const int slot = threadIdx.x / T::L, cl = threadIdx.x % T::L;
+    const uint32_t rb = it.rb();
+    if (!it.hub()) {
+        const int nr = static_cast<int>(it.re() - rb);
+        const int64_t e0 = sm.rp[b][0];
+        // prefetch epilogue operands of this slot's rows, then sum staged rows
+        double2 wp[T::RPS], ac[T::RPS];
+#pragma unroll
+        for (int q = 0; q < T::RPS; ++q) {
+            const int r = q * T::SLOTS + slot;
+            if (r < nr) batch_prefetch<B>(a, rb + r, cl, wp[q], ac[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < T::RPS; ++q) {
+            const int r = q * T::SLOTS + slot;
+            if (r < nr) {
+                const int b0 = static_cast<int>(sm.rp[b][r] - e0), b1 = static_cast<int>(sm.rp[b][r + 1] - e0);
+                double2 s = {0.0, 0.0};
+                for (int e = b0; e < b1; ++e) {
+                    const double2 v = sm.buf[b][e][cl];
+                    s.x += v.x;
+                    s.y += v.y;
+                }
+                batch_epilogue<B>(a, rb + r, s, b1 - b0, cl, wp[q], ac[q]);
+            }
+        }
+        return;
+    }
+    // hub piece: slot s sums edges s, s+SLOTS, ...; slots combined in order.
+    double2 s = {0.0, 0.0};
+    const int cnt = it.cnt();
+    for (int e = slot; e < cnt; e += T::SLOTS) {
+        const double2 v = sm.buf[b][e][cl];
+        s.x += v.x;
+        s.y += v.y;
+    }
+    sm.red[slot][cl] = s;
+    __syncthreads();
+    if (slot == 0) {
+        double2 t = {0.0, 0.0};
+        for (int q = 0; q < T::SLOTS; ++q) {
+            t.x += sm.red[q][cl].x;
+            t.y += sm.red[q][cl].y;
+        }
+        const int64_t rs = a.rowptr[rb];
+        const int64_t d = a.rowptr[rb + 1] - rs;
+        const uint32_t P = static_cast<uint32_t>((d + T::E - 1) / T::E);
+        const uint32_t piece = static_cast<uint32_t>((it.e0() - rs) / T::E);
+        if (P == 1) {
+            double2 wp, ac;
+            batch_prefetch<B>(a, rb, cl, wp, ac);
+            batch_epilogue<B>(a, rb, t, d, cl, wp, ac);
+        } else {
+            reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(it.slot() + piece) * B)[cl] = t;
+            __threadfence();
+            if (T::L < 32) __syncwarp((1u << T::L) - 1u);
+            else __syncwarp();
+            if (cl == 0) {
+                const unsigned prev = atomicAdd(&a.hub_count[rb], 1u);
+                sm.flag = prev == P - 1;
+            }
+            if (T::L < 32) __syncwarp((1u << T::L) - 1u);
+            else __syncwarp();
+            if (sm.flag) {
+                __threadfence();
+                double2 y = {0.0, 0.0};
+                for (uint32_t p = 0; p < P; ++p) {
+                    const double2 v = __ldcg(
+                        reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(it.slot() + p) * B) + cl);
+                    y.x += v.x;
+                    y.y += v.y;
+                }
+                if (cl == 0) a.hub_count[rb] = 0u;
+                double2 wp, ac;
+                batch_prefetch<B>(a, rb, cl, wp, ac);
+                batch_epilogue<B>(a, rb, y, d, cl, wp, ac);
+            }
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kBatchThreads, 3) cheby_batch_staged_kernel(const BatchArgs a) {
+    using T = StagedTile<B>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T& sm = *reinterpret_cast<T*>(smem_raw);
+    uint32_t i = blockIdx.x;
+    if (i >= a.n_items) return;
+    // software pipeline: item i reduced while the rows of i+G are in flight
+    // (cp.async) and the column ids of i+2G are being loaded (registers).
+    uint32_t cols[T::PER];
+    ItemInfo cur = decode_item<B>(a, i);
+    load_cols<B>(a, cur, cols);
+    stage_item<B>(a, sm, 0, cur, cols);
+    cp_async_commit();
+    ItemInfo nxt{0u, 0u, 0ull};
+    if (i + gridDim.x < a.n_items) {
+        nxt = decode_item<B>(a, i + gridDim.x);
+        load_cols<B>(a, nxt, cols);
+    }
+    int b = 0;
+    for (; i < a.n_items; i += gridDim.x) {
+        const bool has_next = i + gridDim.x < a.n_items;
+        if (has_next) stage_item<B>(a, sm, b ^ 1, nxt, cols);
+        cp_async_commit();
+        ItemInfo nn{0u, 0u, 0ull};
+        const uint32_t i2 = i + 2 * gridDim.x;
+        if (i2 < a.n_items) {
+            nn = decode_item<B>(a, i2);
+            load_cols<B>(a, nn, cols);
+        }
+        cp_async_wait<1>();  // the copies of item i have landed
+        __syncthreads();
+        reduce_item<B>(a, sm, b, cur);
+        __syncthreads();  // buffer b is free again
+        cur = nxt;
+        nxt = nn;
+        b ^= 1;
+    }
+    cp_async_wait<0>();
+}
+
+template <int B>
+size_t staged_smem() {
+    return sizeof(StagedTile<B>);
+}
+
+// ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
 
@@ -483,7 +707,46 @@ int step_occupancy(int tile) {
                                                       kStepThreads, 0);
     return blocks;
 }
+template <int B>
+void launch_staged(const BatchArgs& a, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t bytes = staged_smem<B>();
+    if (!configured) {
+        cudaFuncSetAttribute(cheby_batch_staged_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+        configured = true;
+    }
+    cheby_batch_staged_kernel<B><<<grid, kBatchThreads, bytes, st>>>(a);
+}
+
+template <int B>
+int staged_occupancy() {
+    const size_t bytes = staged_smem<B>();
+    cudaFuncSetAttribute(cheby_batch_staged_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bytes));
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_staged_kernel<B>, kBatchThreads, bytes);
+    return blocks;
+}
+
+int batch_staged_occupancy(int B) {
+    switch (B) {
+    case 4: return staged_occupancy<4>();
+    case 8: return staged_occupancy<8>();
+    case 16: return staged_occupancy<16>();
+    default: return staged_occupancy<32>();
+    }
+}
+
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    if (batch_uses_tiles(B)) {
+        switch (B) {
+        case 4: launch_staged<4>(a, grid, st); return;
+        case 8: launch_staged<8>(a, grid, st); return;
+        case 16: launch_staged<16>(a, grid, st); return;
+        default: launch_staged<32>(a, grid, st); return;
+        }
+    }
     switch (B) {
     case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
     case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
