@@ -126,10 +126,12 @@ int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors,
                              const void* nccl_unique_id, cpg_graph** out);
 
 /* Host restatement of the device relabel/partition (graph_build.cu): nodes
- * ordered by (degree desc, id asc); position i goes to rank i % nranks, local
- * row i / nranks, i.e. global id (i % nranks) * ceil(n/nranks) + i / nranks.
- * Fills new_of_old[n]; returns rows per rank in *n_local. */
-int cpg_shard_plan(const uint64_t* offsets, uint32_t n, int nranks, uint32_t* new_of_old, uint32_t* n_local);
+ * ordered by (degree desc, id asc); with cr = ceil(n / (nranks*chunks)),
+ * position i goes to rank = i % nranks, t = i / nranks, chunk = t % chunks,
+ * j = t / chunks: global id = chunk*nranks*cr + rank*cr + j, local row
+ * chunk*cr + j.  Fills new_of_old[n]; returns cr in *rows_per_chunk. */
+int cpg_shard_plan(const uint64_t* offsets, uint32_t n, int nranks, int chunks, uint32_t* new_of_old,
+                   uint32_t* rows_per_chunk);
 
 int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info);
 int cpg_graph_destroy(cpg_graph* g);

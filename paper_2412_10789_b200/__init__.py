@@ -287,16 +287,18 @@ class DeviceGraph:
             pass
 
 
-def shard_plan(offsets, nranks: int):
-    """Host restatement of the device relabel + row partition: (new_of_old[n], n_local).
+def shard_plan(offsets, nranks: int, chunks: int = 1):
+    """Host restatement of the device relabel + row partition: (new_of_old[n], cr).
 
-    Node order (degree desc, id asc); order position i -> rank i % R, local row i // R."""
+    Node order (degree desc, id asc); position i -> rank i % R, t = i // R,
+    chunk t % C, j = t // C; global id chunk*R*cr + rank*cr + j (cr rows per
+    rank and chunk; local row chunk*cr + j)."""
     off = np.ascontiguousarray(offsets, dtype=np.uint64)
     n = len(off) - 1
     out = np.empty(n, dtype=np.uint32)
-    nl = ctypes.c_uint32()
-    _check(L.lib().cpg_shard_plan(_u64p(off), n, nranks, _u32p(out), ctypes.byref(nl)))
-    return out, int(nl.value)
+    cr = ctypes.c_uint32()
+    _check(L.lib().cpg_shard_plan(_u64p(off), n, nranks, chunks, _u32p(out), ctypes.byref(cr)))
+    return out, int(cr.value)
 
 
 def nccl_unique_id() -> bytes:

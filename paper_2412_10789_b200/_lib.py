@@ -54,7 +54,7 @@ SIGNATURES = {
     "cpg_nccl_unique_id": (c_int, [c_void_p]),
     "cpg_graph_create_sharded": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, c_int, c_int,
                                          c_int, c_void_p, POINTER(_G)]),
-    "cpg_shard_plan": (c_int, [_u64p, c_uint32, c_int, _u32p, _u32p]),
+    "cpg_shard_plan": (c_int, [_u64p, c_uint32, c_int, c_int, _u32p, _u32p]),
     "cpg_graph_info_get": (c_int, [_G, POINTER(cpg_graph_info)]),
     "cpg_graph_destroy": (c_int, [_G]),
     "cpg_chebypower": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_void_p, POINTER(cpg_stats)]),

@@ -81,26 +81,42 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Row chunks per rank: one all-gather per chunk, overlapped with the next
+// chunk's step kernel.  1 on a single GPU; CPG_CHUNKS overrides (tests).
+int default_chunks(int nranks) {
+    int c = nranks > 1 ? 4 : 1;
+    if (const char* e = std::getenv("CPG_CHUNKS")) c = std::max(1, std::min(64, std::atoi(e)));
+    return c;
+}
+
+int table_grid(const cpg_graph* g, uint32_t n_items, int occ) {
+    return static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>(n_items, static_cast<uint64_t>(occ) * g->sm_count)));
+}
+
 cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t n, uint64_t nnz, int device,
                          int rank, int nranks) {
     auto g = std::make_unique<cpg_graph>();
     g->device = device;
     g->rank = rank;
     g->nranks = nranks;
+    g->chunks = default_chunks(nranks);
     g->n = n;
     g->nnz = nnz;
     CPG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     CPG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    CPG_CUDA(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
     for (auto& e : g->ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g->chunk_ev.resize(2 * static_cast<size_t>(g->chunks));
+    for (auto& e : g->chunk_ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CPG_CUDA(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device));
     build_device_graph(g.get(), d_off, d_nbr, g->stream);
-    g->hub_partial = dalloc<double>(g->n_hub_items);
-    g->hub_count = dalloc<unsigned int>(g->n_hubs);
-    CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_hubs)));
+    g->hub_partial = dalloc<double>(g->n_partials);
+    g->hub_count = dalloc<unsigned int>(g->n_loc);
+    CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
     const int occ = std::max(1, step_occupancy(g->tile));
-    g->step_grid = static_cast<int>(std::max<uint32_t>(
-        1, std::min<uint64_t>(g->n_items, static_cast<uint64_t>(occ) * g->sm_count)));
-    g->batch_grid = std::max(1, batch_occupancy()) * g->sm_count;
+    g->step_grid = 1;  // max over chunks: the mass-partial stride
+    for (const auto& t : g->tables) g->step_grid = std::max(g->step_grid, table_grid(g.get(), t.n_items, occ));
     g->d_mass_err = dalloc<double>(2);
     CPG_CUDA(cudaDeviceSynchronize());
     return g.release();
@@ -122,7 +138,7 @@ void ensure_ws(cpg_graph* g, size_t cols) {
     g->w_a = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
     g->w_b = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
     g->acc = dalloc<double>(static_cast<size_t>(g->n_loc) * cols);
-    if (g->nranks > 1) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    if (g->nccl_comm) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
     CPG_CUDA(cudaMemset(g->w_a, 0, sizeof(double) * g->n_pad * cols));
     CPG_CUDA(cudaMemset(g->w_b, 0, sizeof(double) * g->n_pad * cols));
     g->ws_cols = cols;
@@ -141,7 +157,7 @@ void ensure_params(cpg_graph* g, uint32_t K, uint32_t n_sources) {
         g->d_sources = dalloc<uint32_t>(n_sources);
         g->src_cap = n_sources;
     }
-    const size_t need = static_cast<size_t>(K) * g->step_grid;
+    const size_t need = static_cast<size_t>(K) * g->chunks * g->step_grid;
     if (g->mass_cap < need) {
         dfree(g->d_mass_partial);
         g->d_mass_partial = dalloc<double>(need);
@@ -165,65 +181,120 @@ void check_query(const cpg_graph* g, const double* coeffs, uint32_t K, const uin
         require(sources[i] < g->n, "source node " + std::to_string(sources[i]) + " out of range");  // :28-29
 }
 
-// One single-source (or dense-seed, when seed_dev != null) query into
-// local acc; then d_dst[n] (caller ids) if non-null.
-uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
-                    cudaStream_t st, StepProf* prof) {
+// Global id of local row 0 of chunk c (cpg_graph layout, graph_build.cu):
+// gid(l) = l + chunk_row0(c) for l in chunk c.
+uint32_t chunk_row0(const cpg_graph* g, uint32_t c) {
+    return c * (static_cast<uint32_t>(g->nranks) - 1) * g->cr + static_cast<uint32_t>(g->rank) * g->cr;
+}
+
+// In-place all-gather of chunk c of a replicated [n_pad][cols] iterate on the
+// comm stream, after the chunk's step kernel (event chunk_ev[c]); the next use
+// of the iterate waits for chunk_ev[C + C-1] (the comm stream is in order).
+void gather_chunk(cpg_graph* g, double* w, uint32_t c, size_t cols, cudaStream_t st) {
+    if (!g->nccl_comm) return;
+    const size_t C = static_cast<size_t>(g->chunks);
+    const size_t R = static_cast<size_t>(g->nranks);
+    double* base = w + static_cast<size_t>(c) * R * g->cr * cols;
+    CPG_CUDA(cudaEventRecord(g->chunk_ev[c], st));
+    CPG_CUDA(cudaStreamWaitEvent(g->comm_stream, g->chunk_ev[c], 0));
+    nccl_allgather_f64(base + static_cast<size_t>(g->rank) * g->cr * cols, base, g->cr * cols, g->nccl_comm,
+                       g->comm_stream);
+    if (c + 1 == C) CPG_CUDA(cudaEventRecord(g->chunk_ev[C + c], g->comm_stream));
+}
+
+void wait_gathers(cpg_graph* g, cudaStream_t st) {
+    if (!g->nccl_comm) return;
+    const size_t C = static_cast<size_t>(g->chunks);
+    CPG_CUDA(cudaStreamWaitEvent(st, g->chunk_ev[C + C - 1], 0));
+}
+
+// Final d*acc (local rows) -> full [n_pad][cols] replicated, chunk by chunk.
+const double* gather_result(cpg_graph* g, size_t cols, cudaStream_t st) {
+    if (!g->nccl_comm) return g->acc;
+    const size_t R = static_cast<size_t>(g->nranks);
+    for (uint32_t c = 0; c < static_cast<uint32_t>(g->chunks); ++c)
+        nccl_allgather_f64(g->acc + static_cast<size_t>(c) * g->cr * cols,
+                           g->full + static_cast<size_t>(c) * R * g->cr * cols, g->cr * cols, g->nccl_comm, st);
+    return g->full;
+}
+
+// The K fused steps of one query, chunk by chunk (last = write d*acc).
+uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
+                   cudaStream_t st, StepProf* prof) {
     uint32_t launches = 0;
-    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
-    if (seed_dev)
-        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, st);
-    else
-        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
-    ++launches;
-    for (uint32_t k = 1; k <= K; ++k) {
+    const int occ = std::max(1, step_occupancy(g->tile));
+    const uint32_t C = static_cast<uint32_t>(g->chunks);
+    for (uint32_t k = k_first; k <= k_last; ++k) {
         StepArgs a;
         a.rowptr = g->rowptr;
         a.col = g->col;
-        a.items = g->items;
         a.w_cur = (k & 1) ? g->w_a : g->w_b;
         a.w_io = (k & 1) ? g->w_b : g->w_a;
         a.acc = g->acc;
         a.out = g->acc;
         a.hub_partial = g->hub_partial;
         a.hub_count = g->hub_count;
-        a.mass_partial = g->d_mass_partial + static_cast<size_t>(k - 1) * g->step_grid;
         a.coeffs = g->d_coeffs;
-        a.row0 = g->row0;
-        a.n_items = g->n_items;
         a.tile = g->tile;
         a.k = static_cast<int>(k);
         a.first = k == 1;
-        a.last = k == K;
-        if (prof) prof->before(st);
-        launch_step(a, g->step_grid, st);
-        if (prof) prof->after(st);
-        ++launches;
-        if (g->nranks > 1) nccl_allgather_f64(a.w_io + g->row0, a.w_io, g->n_loc, g->nccl_comm, st);
+        a.last = last_writes_out && k == K;
+        if (k > 1) wait_gathers(g, st);
+        for (uint32_t c = 0; c < C; ++c) {
+            const ItemTable& t = g->tables[c];
+            a.items = t.items;
+            a.n_items = t.n_items;
+            a.row0 = chunk_row0(g, c);
+            a.mass_partial = g->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * g->step_grid;
+            if (t.n_items) {
+                const int grid = table_grid(g, t.n_items, occ);
+                if (prof) prof->before(st);
+                launch_step(a, grid, st);
+                if (prof) prof->after(st);
+                ++launches;
+            }
+            gather_chunk(g, a.w_io, c, 1, st);
+        }
     }
-    launch_mass_steps(g->d_mass_partial, g->step_grid, K, g->d_step_mass, st);
+    wait_gathers(g, st);
+    return launches;
+}
+
+// One single-source (or dense-seed, when seed_dev != null) query; result
+// d*acc unpermuted into d_dst[n] (caller ids) if non-null.
+uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
+                    cudaStream_t st, StepProf* prof) {
+    uint32_t launches = 0;
+    const uint32_t C = static_cast<uint32_t>(g->chunks);
+    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
+    CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * C * g->step_grid, st));
+    if (seed_dev)
+        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, st);
+    else
+        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
     ++launches;
-    if (g->nranks > 1) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
+    launches += run_steps(g, 1, K, K, true, st, prof);
+    launch_mass_steps(g->d_mass_partial, C * g->step_grid, K, g->d_step_mass, st);
+    ++launches;
+    if (g->nccl_comm) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
     launch_mass_err(g->d_step_mass, K, mass0, g->d_mass_err, st);
     ++launches;
     if (d_dst) {
-        const double* src = g->acc;
-        if (g->nranks > 1) {
-            nccl_allgather_f64(g->acc, g->full, g->n_loc, g->nccl_comm, st);
-            src = g->full;
-        }
-        launch_unpermute(d_dst, src, g->new_of_old, g->n, st);
+        launch_unpermute(d_dst, gather_result(g, 1, st), g->new_of_old, g->n, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
     return launches;
 }
 
-// One tile of up to 64 sources (q0 .. q0+count) through the batched step.
+// One tile of up to B sources (q0 .. q0+count) through the batched step.
 uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
                    cudaStream_t st, StepProf* prof) {
     uint32_t launches = 0;
     const size_t cols = B;
+    const uint32_t C = static_cast<uint32_t>(g->chunks);
+    const bool staged = batch_uses_tiles(static_cast<int>(B));
+    const int occ = staged ? batch_staged_occupancy(static_cast<int>(B)) : batch_occupancy();
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
     launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
     ++launches;
@@ -231,11 +302,6 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         BatchArgs b;
         b.rowptr = g->rowptr;
         b.col = g->col;
-        b.hub_items = g->bitems;
-        b.n_hub_items = g->n_bhub_items;
-        b.n_items = g->n_bitems;
-        b.hub_rows = g->n_bhubs;
-        b.n_loc = g->n_loc;
         b.w_cur = (k & 1) ? g->w_a : g->w_b;
         b.w_io = (k & 1) ? g->w_b : g->w_a;
         b.acc = g->acc;
@@ -243,29 +309,32 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.hub_partial = g->bhub_partial;
         b.hub_count = g->bhub_count;
         b.coeffs = g->d_coeffs;
-        b.row0 = g->row0;
         b.k = static_cast<int>(k);
         b.first = k == 1;
         b.last = k == K;
-        if (prof) prof->before(st);
-        const int grid = batch_uses_tiles(static_cast<int>(B))
-                             ? std::max<int>(1, std::min<int>(static_cast<int>(g->n_bitems),
-                                                              batch_staged_occupancy(static_cast<int>(B)) * g->sm_count))
-                             : g->batch_grid;
-        launch_batch(b, static_cast<int>(B), grid, st);
-        if (prof) prof->after(st);
-        ++launches;
-        if (g->nranks > 1)
-            nccl_allgather_f64(b.w_io + static_cast<size_t>(g->row0) * cols, b.w_io, g->n_loc * cols, g->nccl_comm,
-                               st);
-    }
-    if (d_dst) {
-        const double* src = g->acc;
-        if (g->nranks > 1) {
-            nccl_allgather_f64(g->acc, g->full, g->n_loc * cols, g->nccl_comm, st);
-            src = g->full;
+        if (k > 1) wait_gathers(g, st);
+        for (uint32_t c = 0; c < C; ++c) {
+            const ItemTable& t = g->btables[c];
+            b.hub_items = t.items;
+            b.n_hub_items = t.n_hub_items;
+            b.n_items = t.n_items;
+            b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
+            b.n_loc = t.row_end;                  // end row of the chunk
+            b.row0 = chunk_row0(g, c);
+            const uint32_t jobs = staged ? t.n_items : t.n_hub_items + (t.row_end - b.hub_rows);
+            if (jobs) {
+                const int grid = staged ? table_grid(g, t.n_items, occ) : occ * g->sm_count;
+                if (prof) prof->before(st);
+                launch_batch(b, static_cast<int>(B), grid, st);
+                if (prof) prof->after(st);
+                ++launches;
+            }
+            gather_chunk(g, b.w_io, c, cols, st);
         }
-        launch_unpermute_batch(d_dst, src, g->new_of_old, g->n, count, B, st);
+    }
+    wait_gathers(g, st);
+    if (d_dst) {
+        launch_unpermute_batch(d_dst, gather_result(g, cols, st), g->new_of_old, g->n, count, B, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -326,17 +395,15 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         if (mode == 2) {
             require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
             ensure_batch_tables(g, static_cast<int>(B));
-            const size_t need = static_cast<size_t>(g->n_bhub_items) * B;
+            const size_t need = static_cast<size_t>(g->n_bpartials) * B;
             if (g->bhub_items_cap < need || !g->bhub_partial) {
                 dfree(g->bhub_partial);
                 g->bhub_partial = dalloc<double>(need);
                 g->bhub_items_cap = need;
             }
-            if (g->bhub_count_cap < g->n_bhubs || !g->bhub_count) {
-                dfree(g->bhub_count);
-                g->bhub_count = dalloc<unsigned int>(g->n_bhubs);
-                g->bhub_count_cap = g->n_bhubs;
-                CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_bhubs)));
+            if (!g->bhub_count) {
+                g->bhub_count = dalloc<unsigned int>(g->n_loc);
+                CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
             }
         }
         ensure_ws(g, cols);
@@ -488,7 +555,8 @@ int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors,
         cpg_graph* g = nullptr;
         try {
             g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks);
-            if (nranks > 1) g->nccl_comm = nccl_comm_init(nccl_unique_id, nranks, rank);
+            // NCCL whenever an id is given (also for one rank: exercises the collective path)
+            if (nccl_unique_id) g->nccl_comm = nccl_comm_init(nccl_unique_id, nranks, rank);
         } catch (...) {
             if (t_off) cudaFree(t_off);
             if (t_nbr) cudaFree(t_nbr);
@@ -526,8 +594,13 @@ int cpg_graph_destroy(cpg_graph* g) {
         DeviceGuard dg(g->device);
         cudaDeviceSynchronize();
         if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
-        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->gdeg, (void*)g->new_of_old, (void*)g->items,
-                        (void*)g->bitems, (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
+        for (auto& t : g->tables) cudaFree(t.items);
+        for (auto& t : g->btables) cudaFree(t.items);
+        for (auto e : g->chunk_ev)
+            if (e) cudaEventDestroy(e);
+        if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->gdeg, (void*)g->new_of_old,
+                        (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
                         (void*)g->bhub_count, (void*)g->w_a, (void*)g->w_b, (void*)g->acc, (void*)g->full,
                         (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial, (void*)g->d_mass_err,
                         (void*)g->d_step_mass, (void*)g->d_stage})
@@ -600,28 +673,12 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
         }
         CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * np, st));
         launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, 0, st);
+        CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * g->chunks * g->step_grid, st));
         for (uint32_t k = 1; k <= K; ++k) {
-            StepArgs a;
-            a.rowptr = g->rowptr;
-            a.col = g->col;
-            a.items = g->items;
-            a.w_cur = (k & 1) ? g->w_a : g->w_b;
-            a.w_io = (k & 1) ? g->w_b : g->w_a;
-            a.acc = g->acc;
-            a.out = g->acc;
-            a.hub_partial = g->hub_partial;
-            a.hub_count = g->hub_count;
-            a.mass_partial = g->d_mass_partial + static_cast<size_t>(k - 1) * g->step_grid;
-            a.coeffs = g->d_coeffs;
-            a.row0 = 0;
-            a.n_items = g->n_items;
-        a.tile = g->tile;
-            a.k = static_cast<int>(k);
-            a.first = k == 1;
-            a.last = 0;
-            launch_step(a, g->step_grid, st);
+            run_steps(g, k, k, K, false, st, nullptr);
             CPG_CUDA(cudaGetLastError());
-            CPG_CUDA(cudaMemcpyAsync(w.data(), a.w_io, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+            const double* w_io = (k & 1) ? g->w_b : g->w_a;
+            CPG_CUDA(cudaMemcpyAsync(w.data(), w_io, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
             CPG_CUDA(cudaMemcpyAsync(acc.data(), g->acc, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
             CPG_CUDA(cudaStreamSynchronize(st));
             emit(k, w.data(), acc.data(), 1.0);

@@ -10,9 +10,20 @@
 #include "cpg_common.hpp"
 #include "device_graph.cuh"
 
+namespace cpg {
+// Work table for one chunk of local rows [row_begin, row_end).
+struct ItemTable {
+    WorkItem* items = nullptr;
+    uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0;
+    uint32_t row_begin = 0, row_end = 0;
+};
+} // namespace cpg
+
 struct cpg_graph {
     int device = 0;
     int rank = 0, nranks = 1;
+    int chunks = 1;                 // row chunks per rank (one all-gather each)
+    uint32_t cr = 0;                // rows per (rank, chunk)
     uint32_t n = 0, n_loc = 0, n_pad = 0, row0 = 0, max_degree = 0;
     uint64_t nnz = 0, nnz_loc = 0, hash = 0;
 
@@ -21,22 +32,23 @@ struct cpg_graph {
     uint32_t* gdeg = nullptr;       // [n_pad]
     uint32_t* new_of_old = nullptr; // [n]
 
-    cpg::WorkItem* items = nullptr; // single-source items
-    uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0;
+    std::vector<cpg::ItemTable> tables;   // single-source items, one table per chunk
+    uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0, n_partials = 0;
     int tile = 0;                   // kTileSmall / kTileLarge
-    cpg::WorkItem* bitems = nullptr; // batched hub pieces
-    uint32_t n_bhubs = 0, n_bhub_items = 0;
-    int bitems_width = 0;           // B the batched hub table was built for
-    uint32_t n_bitems = 0;          // batched items (hub pieces + tiles when tiled)
-    size_t bhub_items_cap = 0, bhub_count_cap = 0;
+    std::vector<cpg::ItemTable> btables;  // batched items per chunk
+    int bitems_width = 0;           // B the batched tables were built for
+    uint32_t n_bpartials = 0;
+    size_t bhub_items_cap = 0;
 
-    double* hub_partial = nullptr;  // [n_hub_items]
-    unsigned int* hub_count = nullptr;  // [n_hubs]
-    double* bhub_partial = nullptr; // [n_bhub_items][64]
-    unsigned int* bhub_count = nullptr;
+    double* hub_partial = nullptr;  // [n_partials]
+    unsigned int* hub_count = nullptr;  // [n_loc], indexed by local row
+    double* bhub_partial = nullptr; // [n_bpartials][B]
+    unsigned int* bhub_count = nullptr; // [n_loc]
 
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t comm_stream = nullptr;  // per-chunk all-gathers (sharded)
+    std::vector<cudaEvent_t> chunk_ev;   // chunk computed / chunk gathered
     int sm_count = 0, step_grid = 0, batch_grid = 0;
 
     // Query workspace (grown on demand, owned by the handle).
@@ -68,6 +80,8 @@ namespace cpg {
 // graph_build.cu
 void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st);
 void ensure_batch_tables(cpg_graph* g, int B);
+ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t chunk, uint32_t max_rows,
+                           int64_t piece, uint32_t slot_off, cudaStream_t st);
 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st);

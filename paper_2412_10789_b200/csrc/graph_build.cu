@@ -50,23 +50,29 @@ __global__ void k_deg_ids(const uint64_t* off, uint32_t n, uint32_t* deg, uint32
     }
 }
 
-// Position i of the degree order goes to rank i % R, local row i / R.
-__global__ void k_assign(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t n_loc,
-                         uint32_t* new_of_old, uint32_t* gdeg) {
+// Layout for R ranks x C chunks, cr = ceil(n / (R*C)) rows per (rank, chunk):
+// position i of the degree order -> rank = i % R, t = i / R, chunk = t % C,
+// j = t / C; global id = chunk*R*cr + rank*cr + j; local row = chunk*cr + j.
+// Every (rank, chunk) gets every (R*C)-th node of the degree order (balanced
+// rows and edges), and the rows of chunk c of all ranks are one contiguous
+// block of the replicated iterate, so each chunk is one in-place all-gather.
+__global__ void k_assign(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t C,
+                         uint32_t cr, uint32_t* new_of_old, uint32_t* gdeg) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t g = static_cast<uint32_t>((i % R) * n_loc + i / R);
+        const uint64_t t = i / R;
+        const uint32_t g = static_cast<uint32_t>((t % C) * R * cr + (i % R) * cr + t / C);
         new_of_old[order[i]] = g;
         gdeg[g] = sdeg[i];
     }
 }
 
-__global__ void k_local(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t rank,
-                        uint32_t n_loc, int64_t* ldeg, uint32_t* lold) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= n_loc; j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = j * R + rank;
-        const bool real = j < n_loc && i < n;
-        ldeg[j] = real ? sdeg[i] : 0;
-        if (j < n_loc) lold[j] = real ? order[i] : 0xffffffffu;
+__global__ void k_local(const uint32_t* order, const uint32_t* sdeg, uint32_t n, uint32_t R, uint32_t C, uint32_t cr,
+                        uint32_t rank, uint32_t n_loc, int64_t* ldeg, uint32_t* lold) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l <= n_loc; l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = ((l % cr) * C + l / cr) * R + rank;
+        const bool real = l < n_loc && i < n;
+        ldeg[l] = real ? sdeg[i] : 0;
+        if (l < n_loc) lold[l] = real ? order[i] : 0xffffffffu;
     }
 }
 
@@ -90,11 +96,12 @@ __global__ void k_extract(const uint64_t* keys, uint64_t nnz, uint32_t* col) {
         col[e] = static_cast<uint32_t>(keys[e] & 0xffffffffu);
 }
 
-// Rows are degree-descending, so hubs are a prefix: count = last index with deg > thr, +1.
-__global__ void k_count_above(const int64_t* rowptr, uint32_t n_loc, int64_t thr, unsigned int* count) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc; j += (uint64_t)gridDim.x * blockDim.x) {
+// Rows of a range are degree-descending, so hubs are a prefix: count = last
+// index with deg > thr, +1 (rowptr points at the range's first row).
+__global__ void k_count_above(const int64_t* rowptr, uint32_t n_rows, int64_t thr, unsigned int* count) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_rows; j += (uint64_t)gridDim.x * blockDim.x) {
         const int64_t d = rowptr[j + 1] - rowptr[j];
-        const int64_t dn = j + 1 < n_loc ? rowptr[j + 2] - rowptr[j + 1] : -1;
+        const int64_t dn = j + 1 < n_rows ? rowptr[j + 2] - rowptr[j + 1] : -1;
         if (d > thr && dn <= thr) *count = static_cast<unsigned int>(j + 1);
     }
 }
@@ -102,18 +109,20 @@ __global__ void k_count_above(const int64_t* rowptr, uint32_t n_loc, int64_t thr
 __global__ void k_pieces(const int64_t* rowptr, uint32_t n_hub, int64_t piece, uint32_t* P) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= n_hub; j += gridDim.x * blockDim.x)
         P[j] = j < n_hub ? static_cast<uint32_t>((rowptr[j + 1] - rowptr[j] + piece - 1) / piece) : 0u;
-}
+}  // rowptr points at the range's first row
 
-// Hub piece p of hub row j: {row, first partial slot of the hub, first edge | edge count | hub bit}.
-__global__ void k_hub_items(const int64_t* rowptr, const uint32_t* P, const uint32_t* base, uint32_t n_hub,
-                            int64_t piece, WorkItem* items) {
+// Hub piece p of hub row row0+j: {row, first partial slot of the hub (+ slot
+// offset), first edge | edge count | hub bit}.
+__global__ void k_hub_items(const int64_t* rowptr, uint32_t row0, const uint32_t* P, const uint32_t* base,
+                            uint32_t n_hub, int64_t piece, uint32_t slot_off, WorkItem* items) {
     const int lane = threadIdx.x & 31;
     for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5) {
-        const int64_t rs = rowptr[j], d = rowptr[j + 1] - rs;
+        const int64_t rs = rowptr[row0 + j], d = rowptr[row0 + j + 1] - rs;
         for (uint32_t p = lane; p < P[j]; p += 32) {
             const int64_t e0 = rs + static_cast<int64_t>(p) * piece;
             const uint32_t cnt = static_cast<uint32_t>(min(piece, d - static_cast<int64_t>(p) * piece));
-            items[base[j] + p] = WorkItem{j, base[j], tile_code(static_cast<uint64_t>(e0), cnt, 0) | kHubBit};
+            items[base[j] + p] =
+                WorkItem{row0 + j, slot_off + base[j], tile_code(static_cast<uint64_t>(e0), cnt, 0) | kHubBit};
         }
     }
 }
@@ -145,20 +154,22 @@ __global__ void k_tile_items(const int64_t* rowptr, const uint32_t* starts, uint
     }
 }
 
-// Builds hub-piece items for rows with degree > thr (pieces of `piece` edges).
-// Returns (n_hub, n_items); items written to *out (allocated here).
-void build_hub_items(const int64_t* rowptr, uint32_t n_loc, int64_t thr, int64_t piece, WorkItem** out,
-                     uint32_t* n_hub_out, uint32_t* n_items_out, uint32_t reserve_tail, cudaStream_t st) {
+// Hub-piece items for rows [row0, row1) with degree > thr (pieces of `piece`
+// edges; the hubs are a prefix of the range).  Items are allocated here.
+void build_hub_items(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t thr, int64_t piece,
+                     uint32_t slot_off, WorkItem** out, uint32_t* n_hub_out, uint32_t* n_items_out,
+                     uint32_t reserve_tail, cudaStream_t st) {
+    const uint32_t n_rows = row1 - row0;
     unsigned int* d_cnt = dalloc<unsigned int>(1);
     CPG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned int), st));
-    if (n_loc) k_count_above<<<grid_for(n_loc), kT, 0, st>>>(rowptr, n_loc, thr, d_cnt);
+    if (n_rows) k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, thr, d_cnt);
     unsigned int n_hub = 0;
     CPG_CUDA(cudaMemcpyAsync(&n_hub, d_cnt, sizeof(n_hub), cudaMemcpyDeviceToHost, st));
     CPG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_cnt);
     uint32_t* P = dalloc<uint32_t>(n_hub + 1);
     uint32_t* base = dalloc<uint32_t>(n_hub + 1);
-    k_pieces<<<grid_for(n_hub + 1), kT, 0, st>>>(rowptr, n_hub, piece, P);
+    k_pieces<<<grid_for(n_hub + 1), kT, 0, st>>>(rowptr + row0, n_hub, piece, P);
     DevTemp tmp;
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, P, base, n_hub + 1, st);
@@ -169,7 +180,8 @@ void build_hub_items(const int64_t* rowptr, uint32_t n_loc, int64_t thr, int64_t
     CPG_CUDA(cudaStreamSynchronize(st));
     WorkItem* items = dalloc<WorkItem>(static_cast<size_t>(total) + reserve_tail);
     if (n_hub)
-        k_hub_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(rowptr, P, base, n_hub, piece, items);
+        k_hub_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(rowptr, row0, P, base, n_hub, piece,
+                                                                                 slot_off, items);
     CPG_CUDA(cudaStreamSynchronize(st));
     cudaFree(P);
     cudaFree(base);
@@ -178,25 +190,28 @@ void build_hub_items(const int64_t* rowptr, uint32_t n_loc, int64_t thr, int64_t
     *n_items_out = total;
 }
 
-// Work table over local rows: hub pieces (rows with deg > chunk, split into
-// `piece`-edge pieces) then row tiles (<= 2*chunk edges, <= max_rows rows).
-void build_item_table(const int64_t* rowptr, uint32_t n_loc, int64_t chunk, uint32_t max_rows, int64_t piece,
-                      WorkItem** items_out, uint32_t* n_items_out, uint32_t* n_hubs_out, uint32_t* n_hub_items_out,
-                      cudaStream_t st) {
+} // namespace
+
+// Work table over local rows [row0, row1): hub pieces (rows with deg > chunk,
+// split into `piece`-edge pieces, partial slots from slot_off) then row tiles
+// (<= 2*chunk edges, <= max_rows rows).
+ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t chunk, uint32_t max_rows,
+                           int64_t piece, uint32_t slot_off, cudaStream_t st) {
     DevTemp tmp;
     size_t bytes = 0;
     WorkItem* hub_items = nullptr;
     uint32_t n_hub = 0, n_hub_items = 0;
-    build_hub_items(rowptr, n_loc, chunk, piece, &hub_items, &n_hub, &n_hub_items, 0, st);
+    build_hub_items(rowptr, row0, row1, chunk, piece, slot_off, &hub_items, &n_hub, &n_hub_items, 0, st);
     uint32_t n_tiles = 0;
     uint32_t* starts = nullptr;
-    if (n_hub < n_loc) {
-        const uint32_t rows = n_loc - n_hub;
+    const uint32_t first = row0 + n_hub;
+    if (first < row1) {
+        const uint32_t rows = row1 - first;
         uint8_t* flags = dalloc<uint8_t>(rows);
         starts = dalloc<uint32_t>(rows);
         unsigned int* d_sel = dalloc<unsigned int>(1);
-        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(rowptr, n_hub, n_loc, chunk, max_rows, flags);
-        cub::CountingInputIterator<uint32_t> it(n_hub);
+        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(rowptr, first, row1, chunk, max_rows, flags);
+        cub::CountingInputIterator<uint32_t> it(first);
         cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);
         tmp.ensure(bytes);
         CPG_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, starts, d_sel, rows, st));
@@ -205,28 +220,32 @@ void build_item_table(const int64_t* rowptr, uint32_t n_loc, int64_t chunk, uint
         cudaFree(flags);
         cudaFree(d_sel);
     }
-    WorkItem* items = dalloc<WorkItem>(static_cast<size_t>(n_hub_items) + n_tiles);
+    ItemTable t;
+    t.items = dalloc<WorkItem>(static_cast<size_t>(n_hub_items) + n_tiles);
     if (n_hub_items)
-        CPG_CUDA(cudaMemcpyAsync(items, hub_items, sizeof(WorkItem) * n_hub_items, cudaMemcpyDeviceToDevice, st));
-    if (n_tiles) k_tile_items<<<grid_for(n_tiles), kT, 0, st>>>(rowptr, starts, n_tiles, n_loc, items + n_hub_items);
+        CPG_CUDA(cudaMemcpyAsync(t.items, hub_items, sizeof(WorkItem) * n_hub_items, cudaMemcpyDeviceToDevice, st));
+    if (n_tiles) k_tile_items<<<grid_for(n_tiles), kT, 0, st>>>(rowptr, starts, n_tiles, row1, t.items + n_hub_items);
     CPG_CUDA(cudaStreamSynchronize(st));
     cudaFree(hub_items);
     if (starts) cudaFree(starts);
-    *items_out = items;
-    *n_items_out = n_hub_items + n_tiles;
-    *n_hubs_out = n_hub;
-    *n_hub_items_out = n_hub_items;
+    t.n_items = n_hub_items + n_tiles;
+    t.n_hubs = n_hub;
+    t.n_hub_items = n_hub_items;
+    t.row_begin = row0;
+    t.row_end = row1;
+    return t;
 }
-
-} // namespace
 
 void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st) {
     const uint32_t n = g->n;
     const uint32_t R = static_cast<uint32_t>(g->nranks);
     const uint32_t rank = static_cast<uint32_t>(g->rank);
-    g->n_loc = (n + R - 1) / R;
+    const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
+    const uint64_t RC = static_cast<uint64_t>(R) * C;
+    g->cr = static_cast<uint32_t>((n + RC - 1) / RC);
+    g->n_loc = g->cr * C;
     g->n_pad = g->n_loc * R;
-    g->row0 = rank * g->n_loc;
+    g->row0 = rank * g->cr;  // global id of local row 0 (chunk 0)
     const uint32_t n_loc = g->n_loc;
     DevTemp tmp;
     size_t bytes = 0;
@@ -248,10 +267,11 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
     g->new_of_old = dalloc<uint32_t>(n);
     g->gdeg = dalloc<uint32_t>(g->n_pad);
     CPG_CUDA(cudaMemsetAsync(g->gdeg, 0, sizeof(uint32_t) * g->n_pad, st));
-    k_assign<<<grid_for(n), kT, 0, st>>>(order, sdeg, n, R, n_loc, g->new_of_old, g->gdeg);
+    k_assign<<<grid_for(n), kT, 0, st>>>(order, sdeg, n, R, C, g->cr, g->new_of_old, g->gdeg);
     int64_t* ldeg = dalloc<int64_t>(static_cast<size_t>(n_loc) + 1);
     uint32_t* lold = dalloc<uint32_t>(n_loc);
-    k_local<<<grid_for(static_cast<uint64_t>(n_loc) + 1), kT, 0, st>>>(order, sdeg, n, R, rank, n_loc, ldeg, lold);
+    k_local<<<grid_for(static_cast<uint64_t>(n_loc) + 1), kT, 0, st>>>(order, sdeg, n, R, C, g->cr, rank, n_loc, ldeg,
+                                                                        lold);
     cudaFree(sdeg);
     cudaFree(order);
 
@@ -294,32 +314,49 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
         const int t = std::atoi(force);
         if (t == kTileSmall || t == kTileLarge) g->tile = t;
     }
-    build_item_table(g->rowptr, n_loc, g->tile / 2, kTileMaxRows, kHubPieceEdges, &g->items, &g->n_items, &g->n_hubs,
-                     &g->n_hub_items, st);
-    g->n_tiles = g->n_items - g->n_hub_items;
+    g->tables.clear();
+    uint32_t slots = 0;
+    for (uint32_t c = 0; c < C; ++c) {
+        ItemTable t = build_item_table(g->rowptr, c * g->cr, (c + 1) * g->cr, g->tile / 2, kTileMaxRows,
+                                       kHubPieceEdges, slots, st);
+        slots += t.n_hub_items;  // one partial slot per hub piece
+        g->tables.push_back(t);
+    }
+    g->n_partials = slots;
+    g->n_items = g->n_hubs = g->n_hub_items = g->n_tiles = 0;
+    for (const auto& t : g->tables) {
+        g->n_items += t.n_items;
+        g->n_hubs += t.n_hubs;
+        g->n_hub_items += t.n_hub_items;
+        g->n_tiles += t.n_items - t.n_hub_items;
+    }
     CPG_CUDA(cudaGetLastError());
 }
 
 void ensure_batch_tables(cpg_graph* g, int B) {
-    if (g->bitems && g->bitems_width == B) return;
-    if (g->bitems) cudaFree(g->bitems);
-    g->bitems = nullptr;
-    if (batch_uses_tiles(B)) {
-        // staged tiles: <= E(B) edges and <= R(B) rows, hubs split in E-edge pieces
-        uint32_t n_items = 0, n_hub = 0, n_hub_items = 0;
-        build_item_table(g->rowptr, g->n_loc, batch_tile_edges(B) / 2, batch_tile_rows(B), batch_tile_edges(B),
-                         &g->bitems, &n_items, &n_hub, &n_hub_items, g->stream);
-        g->n_bitems = n_items;
-        g->n_bhubs = n_hub;
-        g->n_bhub_items = n_hub_items;
-    } else {
-        uint32_t n_hub = 0, n_items = 0;
-        const int64_t hb = batch_hub_edges(B);
-        build_hub_items(g->rowptr, g->n_loc, hb, hb, &g->bitems, &n_hub, &n_items, 0, g->stream);
-        g->n_bhubs = n_hub;
-        g->n_bhub_items = n_items;
-        g->n_bitems = n_items;
+    if (!g->btables.empty() && g->bitems_width == B) return;
+    for (auto& t : g->btables) cudaFree(t.items);
+    g->btables.clear();
+    uint32_t slots = 0;
+    const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
+    for (uint32_t c = 0; c < C; ++c) {
+        ItemTable t;
+        if (batch_uses_tiles(B)) {
+            // staged tiles: <= E(B) edges and <= R(B) rows, hubs split in E-edge pieces
+            t = build_item_table(g->rowptr, c * g->cr, (c + 1) * g->cr, batch_tile_edges(B) / 2, batch_tile_rows(B),
+                                 batch_tile_edges(B), slots, g->stream);
+        } else {
+            const int64_t hb = batch_hub_edges(B);
+            build_hub_items(g->rowptr, c * g->cr, (c + 1) * g->cr, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items,
+                            0, g->stream);
+            t.n_items = t.n_hub_items;
+            t.row_begin = c * g->cr;
+            t.row_end = (c + 1) * g->cr;
+        }
+        slots += t.n_hub_items;
+        g->btables.push_back(t);
     }
+    g->n_bpartials = slots;
     g->bitems_width = B;
     CPG_CUDA(cudaGetLastError());
 }

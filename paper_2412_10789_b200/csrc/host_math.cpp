@@ -258,18 +258,22 @@ int cpg_parse_kernel_spec(const char* spec_c, int* family, double* param) {
     });
 }
 
-int cpg_shard_plan(const uint64_t* offsets, uint32_t n, int nranks, uint32_t* new_of_old, uint32_t* n_local) {
+int cpg_shard_plan(const uint64_t* offsets, uint32_t n, int nranks, int chunks, uint32_t* new_of_old,
+                   uint32_t* rows_per_chunk) {
     return guarded([&] {
-        require(offsets && new_of_old && n_local && nranks >= 1 && n > 0, "bad argument");
+        require(offsets && new_of_old && rows_per_chunk && nranks >= 1 && chunks >= 1 && n > 0, "bad argument");
         std::vector<uint32_t> order(n);
         for (uint32_t i = 0; i < n; ++i) order[i] = i;
         std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
             return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
         });
-        const uint32_t R = static_cast<uint32_t>(nranks);
-        const uint32_t nl = (n + R - 1) / R;
-        for (uint32_t i = 0; i < n; ++i) new_of_old[order[i]] = (i % R) * nl + i / R;
-        *n_local = nl;
+        const uint64_t R = static_cast<uint64_t>(nranks), C = static_cast<uint64_t>(chunks);
+        const uint64_t cr = (n + R * C - 1) / (R * C);
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint64_t t = i / R;
+            new_of_old[order[i]] = static_cast<uint32_t>((t % C) * R * cr + (i % R) * cr + t / C);
+        }
+        *rows_per_chunk = static_cast<uint32_t>(cr);
     });
 }
 

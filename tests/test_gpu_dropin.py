@@ -63,3 +63,53 @@ def test_sharded_handle_single_rank_nccl(cpg, gpu):
         assert_parity(got[j], want)
         assert_parity(got_b[j], want)
     assert st.mass_err_max <= 1e-9
+
+
+@pytest.mark.parametrize("chunks", ["1", "3"])
+def test_sharded_single_rank_chunked(cpg, gpu, chunks, monkeypatch):
+    """Chunked layout (CPG_CHUNKS) with per-chunk NCCL in-place all-gathers on the
+    comm stream (one rank), single-source and batched, against the oracle."""
+    import ctypes
+
+    from oracle import Port
+
+    monkeypatch.setenv("CPG_CHUNKS", chunks)
+    off, nb = cpg.gen_rmat(13, 16 << 13, seed=4)
+    offs = np.ascontiguousarray(off, np.uint64)
+    nbs = np.ascontiguousarray(nb, np.uint32)
+    dg = cpg.DeviceGraph.sharded(offs.ctypes.data_as(ctypes.c_void_p), nbs.ctypes.data_as(ctypes.c_void_p),
+                                 len(off) - 1, len(nb), False, 0, 0, 1, cpg.nccl_unique_id())
+    n = len(off) - 1
+    assert dg.info.n_padded >= n
+    k = cpg.Kernel.ppr(0.2)
+    c = k.cheby_coeffs(26)
+    src = [0, 5, n // 2, n - 1]
+    got, st = cpg.cheby_power_many(dg, k, src, 26)
+    got_b, _ = cpg.cheby_power_many(dg, k, src, 26, batched=True, tile=4)
+    for j, s in enumerate(src):
+        want, _, _ = Port.cheby_power(off, nb, c, 26, s)
+        assert_parity(got[j], want)
+        assert_parity(got_b[j], want)
+    assert st.mass_err_max <= 1e-9
+
+
+@pytest.mark.parametrize("chunks", ["2", "5"])
+def test_single_gpu_chunked_layout(cpg, gpu, chunks, monkeypatch):
+    """Chunked item tables / per-chunk launches without NCCL (one GPU)."""
+    from oracle import Port
+
+    monkeypatch.setenv("CPG_CHUNKS", chunks)
+    off, nb = cpg.gen_chunglu(40000, 400000, 2.1, 20.0, 9000, seed=6)
+    dg = cpg.DeviceGraph.from_host(off, nb, 0)
+    k = cpg.Kernel.hkpr(5.0)
+    c = k.cheby_coeffs(15)
+    src = [0, 3, 20000]
+    got, st = cpg.cheby_power_many(dg, k, src, 15)
+    got_b, _ = cpg.cheby_power_many(dg, k, src, 15, batched=True, tile=16)
+    for j, s in enumerate(src):
+        want, _, _ = Port.cheby_power(off, nb, c, 15, s)
+        assert_parity(got[j], want)
+        assert_parity(got_b[j], want)
+    est = cpg.cheby_power(dg, k, 7, 15, observer=lambda kk, r, e: None)
+    want, _, _ = Port.cheby_power(off, nb, c, 15, 7)
+    assert_parity(est.values, want)

@@ -128,21 +128,24 @@ def test_select_sources_matches_reference(cpg):
         cpg.select_sources_uniform(10, 11, 1)
 
 
-def test_shard_plan_is_a_balanced_permutation(cpg):
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_shard_plan_is_a_balanced_permutation(cpg, chunks):
     off, nb = cpg.gen_rmat(12, 8 << 12, seed=6)
     n = len(off) - 1
     deg = np.diff(off)
     for R in (1, 2, 3, 8):
-        no, nl = cpg.shard_plan(off, R)
-        assert nl == -(-n // R)
-        assert len(np.unique(no)) == n and no.max() < nl * R
-        owner = no // nl
-        counts = np.bincount(owner, minlength=R)
+        no, cr = cpg.shard_plan(off, R, chunks)
+        assert cr == -(-n // (R * chunks))
+        assert len(np.unique(no)) == n and no.max() < cr * R * chunks
+        chunk = no // (R * cr)
+        owner = (no % (R * cr)) // cr
+        counts = np.bincount(owner * chunks + chunk, minlength=R * chunks)
         assert counts.max() - counts.min() <= 1
         vol = np.bincount(owner, weights=deg, minlength=R)
         assert vol.max() <= 1.1 * vol.mean() + deg.max()
-        # within a rank, rows are degree-descending
+        # within a (rank, chunk), rows are degree-descending
         for r in range(R):
-            rows = np.argsort(no[owner == r])
-            d = deg[owner == r][rows]
-            assert np.all(np.diff(d.astype(np.int64)) <= 0)
+            for c in range(chunks):
+                sel = (owner == r) & (chunk == c)
+                d = deg[sel][np.argsort(no[sel])]
+                assert np.all(np.diff(d.astype(np.int64)) <= 0)
