@@ -5,7 +5,9 @@
 
 A "step" is one pass of the hot path over one batch of queries: every source
 of the config (16 or 64) runs its K Chebyshev iterations.  The default workload
-is config 3 (LiveJournal-size Chung-Lu, single-source SpMV path, 1 GPU).
+is config 5 (the 1.8B-edge R-MAT graph, 16 SSPPR sources as one 16-column tile
+of the batched step; row-partitioned with per-chunk NCCL all-gathers when
+launched on N GPUs).
 
 value  = GTEPS = K * nnz * sources / t   (the reference's push_work / wall_seconds,
          solvers.cpp:214,223), device-resident inputs, CUDA events, max over ranks.
@@ -48,9 +50,11 @@ CONFIGS = {
             exponent=2.1, mean=76.0, cap=33_000, seed=4, family=HKPR, param=5.0, eps=1e-8, sources=64,
             mode="batched"),
     5: dict(name="rmat-friendster-size ppr", gen="rmat", scale=27, samples=1_840_000_000, seed=5,
-            family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
+            family=PPR, param=0.2, eps=1e-8, sources=16, mode="batched", tile=16),
 }
-DEFAULT_CONFIG = 3
+# Headline: config 5, the 1.8B-edge graph the metric is quoted on at 1/2/4/8 B200;
+# its 16 sources run as one 16-column tile through the batched step.
+DEFAULT_CONFIG = 5
 
 
 def log(*a):
@@ -133,40 +137,65 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def cpu_baseline(cfg, off, nb, sources, K, budget_s=20.0, threads=None):
-    """Reference cheby_power (oracle/_ref) on host cores, bounded sample.
+BIG_NNZ = 300_000_000  # above this a full CPU query takes minutes: sample one iteration instead
 
-    The checker library is used only here, as the timed CPU baseline."""
+
+def _host_threads(n):
+    """All host threads, capped so the per-thread iterate buffers fit in free RAM."""
+    threads = os.cpu_count() or 1
+    try:
+        import psutil
+
+        free = psutil.virtual_memory().available
+        threads = max(1, min(threads, int(0.5 * free // max(1, 2 * 8 * n))))
+    except Exception:
+        pass
+    return threads
+
+
+def cpu_sample(cfg, off, nb, sources, K, budget_s=20.0, threads=None):
+    """Time the reference's CPU ChebyPower on the host cores (bounded sample).
+
+    nnz <= BIG_NNZ: whole cheby_power queries of the reference library
+    (oracle/_ref, compiled from /root/reference), one per thread, the
+    reference bench's worker pool (tools/chebyprop.cpp:305-334).
+    nnz >  BIG_NNZ: one steady-state iteration per thread -- the reference's
+    apply_walk (graph.cpp:257-267, restated bit-exact in oracle/cheby_oracle.c)
+    over a dense vector -- since one full query takes minutes per core there.
+    GTEPS = edges visited / wall time either way.  The checker libraries are
+    used only here, as the timed CPU baseline."""
     import oracle
 
-    threads = threads or os.cpu_count() or 1
-    coeffs = oracle.Port.cheby_coeffs(cfg["family"], cfg["param"], K)
-    nnz = len(nb)
+    n, nnz = len(off) - 1, len(nb)
+    threads = threads or _host_threads(n)
+    if nnz > BIG_NNZ:
+        per = 400_000_000  # edges per thread per sample (~1-2 s of one core)
+        wall, edges = oracle.Port.apply_walk_pool(off, nb, threads, per)
+        gteps = edges / wall / 1e9
+        return {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": "port",
+                "queries_per_s": gteps * 1e9 / (K * nnz),
+                "sample": f"{threads} threads x ~{per/1e6:.0f}M edges of the reference's dense apply_walk "
+                          f"(per-step SpMV, oracle restatement) in {wall:.1f}s; queries/s = GTEPS/(K*nnz)",
+                "cpu_model": _cpu_model()}
     kind = "reference" if oracle.Ref.available() else "port"
-    # size the sample: one query per thread per round, rounds until ~budget
+    coeffs = oracle.Port.cheby_coeffs(cfg["family"], cfg["param"], K)
     t0 = time.perf_counter()
-    if kind == "reference":
-        g = oracle.RefGraph.from_csr(off, nb)
+    g = oracle.RefGraph.from_csr(off, nb) if kind == "reference" else None
     setup = time.perf_counter() - t0
     done, wall = 0, 0.0
-    sample = []
-    while wall < budget_s and done < len(sources) * 4:
+    while wall < budget_s / 2 and done < len(sources) * 4:
         batch = [int(sources[(done + i) % len(sources)]) for i in range(threads)]
         t = time.perf_counter()
-        if kind == "reference":
+        if g is not None:
             g.cheby_power_pool(cfg["family"], cfg["param"], batch, K, threads, keep=False)
         else:
             oracle.Port.cheby_power_pool(off, nb, coeffs, K, batch, threads, keep=False)
         wall += time.perf_counter() - t
         done += len(batch)
-        sample.append(len(batch))
-        if wall > budget_s / 2 and len(sample) >= 1:
-            break
-    gteps = K * nnz * done / wall / 1e9
-    return {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
+    return {"value": K * nnz * done / wall / 1e9, "unit": "GTEPS", "cores": threads, "kind": kind,
             "queries_per_s": done / wall,
-            "sample": f"{done} queries x K={K} on {threads} threads ({wall:.1f}s; graph setup {setup:.1f}s excluded)",
-            "cpu_model": _cpu_model()}
+            "sample": f"{done} full queries x K={K} on {threads} threads ({wall:.1f}s; graph setup {setup:.1f}s "
+                      f"excluded)", "cpu_model": _cpu_model()}
 
 
 def _cpu_model():
@@ -181,46 +210,48 @@ def _cpu_model():
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's CPU cheby_power on all host threads."""
+    """--impl reference: the reference's CPU ChebyPower on all host threads.
+
+    Same config, metric and unit as our arm; each step is one bounded sample
+    (cpu_sample).  The synthetic input graph is built with the GPU generator
+    when a GPU is visible (input preparation only, outside the timed region),
+    else on the host."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import oracle
     import paper_2412_10789_b200 as P
 
-    off, nb = make_host_graph(cfg)
+    try:
+        import torch
+
+        gpu = torch.cuda.is_available()
+    except Exception:
+        gpu = False
+    if gpu:
+        csr = make_device_csr(cfg, 0)
+        off, nb = csr.to_host()
+        csr.close()
+    else:
+        off, nb = make_host_graph(cfg)
     n = len(off) - 1
     kernel = P.Kernel.ppr(cfg["param"]) if cfg["family"] == PPR else P.Kernel.hkpr(cfg["param"])
     K = P.plan_truncation(kernel, cfg["eps"]).cheby_steps
     sources = P.select_sources_uniform(n, cfg["sources"], 1)
-    threads = os.cpu_count() or 1
-    kind = "reference" if oracle.Ref.available() else "port"
-    coeffs = oracle.Port.cheby_coeffs(cfg["family"], cfg["param"], K)
-    g = oracle.RefGraph.from_csr(off, nb) if kind == "reference" else None
-    per_step = max(1, min(len(sources), threads))  # bounded sample: one query per thread per step
-
-    def one_step(i):
-        batch = [int(sources[(i * per_step + j) % len(sources)]) for j in range(per_step)]
-        if g is not None:
-            g.cheby_power_pool(cfg["family"], cfg["param"], batch, K, threads, keep=False)
-        else:
-            oracle.Port.cheby_power_pool(off, nb, coeffs, K, batch, threads, keep=False)
-
-    for i in range(args.warmup):
-        one_step(i)
-    t = time.perf_counter()
-    for i in range(args.steps):
-        one_step(args.warmup + i)
-    wall = time.perf_counter() - t
-    gteps = K * len(nb) * per_step * args.steps / wall / 1e9
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(cfg, off, nb, sources, K, budget_s=args.cpu_budget)
+        if i >= args.warmup:
+            samples.append(r)
+    gteps = float(np.median([r["value"] for r in samples]))
+    qps = float(np.median([r["queries_per_s"] for r in samples]))
+    last = samples[-1]
     line = {"metric": METRIC, "value": gteps, "unit": "GTEPS", "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "queries_per_s": per_step * args.steps / wall,
-            "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": len(nb), "K": K,
-                       "sources_per_step": per_step},
-            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
-                             "sample": f"{per_step} queries per step x {args.steps} steps", "cpu_model": _cpu_model()},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "queries_per_s": qps,
+            "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": len(nb), "K": K},
+            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": last["cores"], "kind": last["kind"],
+                             "sample": last["sample"], "cpu_model": last["cpu_model"]},
             "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -390,7 +421,7 @@ def run_ours(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         off, nb = csr.to_host()
-        cpu = cpu_baseline(cfg, off, nb, sources, K, budget_s=args.cpu_budget)
+        cpu = cpu_sample(cfg, off, nb, sources, K, budget_s=args.cpu_budget)
     csr.close()
 
     if rank == 0:

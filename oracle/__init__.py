@@ -101,6 +101,8 @@ class Port:
             L.cpo_edges_to_csr.argtypes = [_i64p, c_uint64, _u32p, _u64p, _u64p, _u32p]
             L.cpo_cheby_power_pool.argtypes = [c_uint32, _u64p, _u32p, _f64p, c_uint64, _u32p,
                                                c_uint64, _f64p, c_int]
+            L.cpo_apply_walk_pool.argtypes = [c_uint32, _u64p, _u32p, c_int, c_uint64, _u64p]
+            L.cpo_apply_walk_pool.restype = c_double
             cls._lib = L
         return cls._lib
 
@@ -229,6 +231,18 @@ class Port:
                                                   _p(coeffs, _f64p), K, _p(sources, _u32p),
                                                   len(sources), _p(out, _f64p), n_threads), "pool")
         return out
+
+    @classmethod
+    def apply_walk_pool(cls, offsets, nbrs, n_threads, edges_per_thread=0):
+        """(wall seconds, edges) for n_threads concurrent dense apply_walk runs, each over
+        ~edges_per_thread edges (0 = one full iteration each)."""
+        offsets, nbrs = _csr(offsets, nbrs)
+        done = c_uint64()
+        t = cls.lib().cpo_apply_walk_pool(len(offsets) - 1, _p(offsets, _u64p), _p(nbrs, _u32p), n_threads,
+                                          edges_per_thread, ctypes.byref(done))
+        if t < 0:
+            raise OracleError("apply_walk_pool: out of memory")
+        return t, done.value
 
     @classmethod
     def select_sources_uniform(cls, n, count, seed):

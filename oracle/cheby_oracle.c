@@ -20,6 +20,7 @@
  * the reference so the restatement is bit-exact with it (no FMA: compiled with
  * -ffp-contract=off, like the reference's default x86-64 build).
  */
+#define _POSIX_C_SOURCE 200809L
 #include <math.h>
 #include <pthread.h>
 #include <stdint.h>
@@ -415,4 +416,75 @@ int cpo_edges_to_csr(const int64_t* pairs, uint64_t m, uint32_t* n_out, uint64_t
     }
     free(half);
     return CPO_OK;
+}
+
+/* ---- steady-state iteration sample for huge graphs --------------------------
+ * n_threads threads each run the reference's apply_walk inner loop
+ * (graph.cpp:261-266: w = x[u] * inv_deg[u]; out[v] += w for v in N(u)) over a
+ * dense seeded vector for a contiguous run of source rows starting at a
+ * thread-specific offset until ~edges_per_thread edges are processed (0 =
+ * the whole graph, i.e. one full iteration).  The scatter still targets the
+ * full-length out vector, so the memory behaviour is the reference's.
+ * Returns wall seconds; *edges_done = edges processed by all threads. */
+typedef struct {
+    uint32_t n;
+    const uint64_t* offsets;
+    const uint32_t* nbrs;
+    uint64_t seed;
+    uint32_t row0;
+    uint64_t edge_budget;
+    uint64_t edges;
+    int failed;
+} cpo_walk_job;
+
+static double now_secs(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static void* walk_worker(void* arg) {
+    cpo_walk_job* j = (cpo_walk_job*)arg;
+    double* x = (double*)malloc((size_t)j->n * sizeof(double));
+    double* out = (double*)calloc((size_t)j->n, sizeof(double));
+    if (!x || !out) { free(x); free(out); j->failed = 1; return NULL; }
+    cpo_random_vector(j->n, j->seed, 0.0, 1.0, x);
+    uint64_t done = 0;
+    uint32_t u = j->row0;
+    for (uint32_t cnt = 0; cnt < j->n && done < j->edge_budget; ++cnt) {
+        const double xu = x[u];
+        if (xu != 0.0) {
+            const double w = xu * (1.0 / (double)(j->offsets[u + 1] - j->offsets[u]));
+            for (uint64_t i = j->offsets[u]; i < j->offsets[u + 1]; ++i) out[j->nbrs[i]] += w;
+        }
+        done += j->offsets[u + 1] - j->offsets[u];
+        if (++u == j->n) u = 0;
+    }
+    j->edges = done;
+    free(x); free(out);
+    return NULL;
+}
+
+double cpo_apply_walk_pool(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs, int n_threads,
+                           uint64_t edges_per_thread, uint64_t* edges_done) {
+    if (n_threads < 1) n_threads = 1;
+    if (edges_per_thread == 0) edges_per_thread = offsets[n];
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);
+    cpo_walk_job* jobs = (cpo_walk_job*)calloc((size_t)n_threads, sizeof(cpo_walk_job));
+    double t = now_secs();
+    for (int i = 0; i < n_threads; ++i) {
+        jobs[i] = (cpo_walk_job){n, offsets, nbrs, (uint64_t)(1000 + i),
+                                 (uint32_t)(((uint64_t)i * n) / (uint64_t)n_threads), edges_per_thread, 0, 0};
+        pthread_create(&th[i], NULL, walk_worker, &jobs[i]);
+    }
+    for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+    double wall = now_secs() - t;
+    uint64_t total = 0;
+    for (int i = 0; i < n_threads; ++i) {
+        if (jobs[i].failed) wall = -1;
+        total += jobs[i].edges;
+    }
+    if (edges_done) *edges_done = total;
+    free(th); free(jobs);
+    return wall;
 }
