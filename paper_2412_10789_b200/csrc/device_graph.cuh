@@ -94,9 +94,18 @@ struct StepArgs {
     int last;              // write out = d * acc instead of acc
 };
 
+// Streaming batched step (cheby_batch_stream_kernel): each lane slot (B/2
+// lanes) walks an edge-balanced contiguous edge range through a per-warp
+// cp.async ring of kStreamStages stages.
+constexpr int kStreamStages = 16;
+constexpr int kStreamWarps = 8;
+
 struct BatchArgs {
     const int64_t* rowptr;
     const uint32_t* col;
+    const int64_t* slot_edge;   // streaming: [n_slots+1] first edge of each slot
+    const uint32_t* slot_row;   // streaming: [n_slots] row holding the slot's first edge
+    uint32_t n_slots;
     const WorkItem* hub_items;  // hub pieces (row, slot_base, piece | hub bit); tiled: + row tiles
     uint32_t n_hub_items;
     uint32_t n_items;           // tiled kernel: hub pieces + tiles

@@ -22,6 +22,8 @@
 // run (no floating-point atomics).
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "device_graph.cuh"
 
 namespace cpg {
@@ -627,6 +629,245 @@ size_t staged_smem() {
 }
 
 // ---------------------------------------------------------------------------
+// Streaming batched step (the default batched path).  The chunk's edges are
+// split into n_slots equal contiguous ranges; a slot of L = B/2 lanes walks its
+// range as one stream of stages: per row it owns entirely, two operand stages
+// (the row of w_{k-1} and of acc) then one stage per edge (the gathered
+// B*8-byte row of w_k); rows cut by a slot boundary are summed per segment and
+// combined by the ordered last-arriver reduction.  Every stage is one 16-B
+// cp.async per lane into a per-warp ring of kStreamStages stages, so up to
+// 16 x 512 B per warp are in flight without holding registers; no CTA
+// barriers.  The consumer (kStreamStages-1 stages behind the producer)
+// accumulates in edge order, so results are bit-reproducible.
+// ---------------------------------------------------------------------------
+enum : uint32_t { kEvNone = 0, kEvOpW = 1, kEvOpAcc = 2, kEvEdge = 3, kEvEndFull = 4, kEvEndPart = 5 };
+
+template <int B>
+struct StreamCfg {
+    static constexpr int L = B / 2;     // lanes per slot
+    static constexpr int RPW = 32 / L;  // slots per warp
+    static constexpr int S = kStreamStages;
+};
+
+template <int B>
+size_t stream_smem_bytes() {
+    return static_cast<size_t>(kStreamWarps) * kStreamStages * 32 * (sizeof(double2) + sizeof(uint2));
+}
+
+__device__ __forceinline__ uint32_t slot_of_edge(const int64_t* slot_edge, uint32_t n_slots, int64_t e) {
+    uint32_t lo = 0, hi = n_slots;  // last s with slot_edge[s] <= e
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (slot_edge[mid] <= e) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <int V>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&w)[V], int v) {
+    uint32_t r = w[0];
+#pragma unroll
+    for (int i = 1; i < V; ++i) r = v == i ? w[i] : r;
+    return r;
+}
+template <int V>
+__device__ __forceinline__ int64_t pick(const int64_t (&w)[V], int v) {
+    int64_t r = w[0];
+#pragma unroll
+    for (int i = 1; i < V; ++i) r = v == i ? w[i] : r;
+    return r;
+}
+
+template <int B>
+__global__ void __launch_bounds__(kStreamWarps * 32, 2) cheby_batch_stream_kernel(const BatchArgs a) {
+    using C = StreamCfg<B>;
+    constexpr int W = 32;          // index / row-end window per slot
+    constexpr int V = W / C::L;    // window entries per lane
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sl = lane / C::L, cl = lane % C::L;
+    const int lane0 = sl * C::L;   // first lane of this slot
+    double2* ring = reinterpret_cast<double2*>(smem_raw) + static_cast<size_t>(warp) * C::S * 32;
+    uint2* desc = reinterpret_cast<uint2*>(smem_raw + static_cast<size_t>(kStreamWarps) * C::S * 32 * sizeof(double2)) +
+                  static_cast<size_t>(warp) * C::S * 32;
+    const uint32_t slot = (blockIdx.x * kStreamWarps + warp) * C::RPW + sl;
+    const bool live = slot < a.n_slots;
+    const unsigned smask = C::L == 32 ? 0xffffffffu : (((1u << C::L) - 1u) << lane0);
+
+    // ---- producer state (replicated across the slot's lanes) ----
+    int64_t p_e = 0, p_end = 0, p_rs = 0, p_re = 0, s_begin = 0;
+    uint32_t p_row = 0;
+    int p_phase = 2;  // 0: operand w, 1: operand acc, 2: edges
+    bool p_full = false;
+    if (live) {
+        s_begin = a.slot_edge[slot];
+        p_end = a.slot_edge[slot + 1];
+        p_e = s_begin;
+        p_row = a.slot_row[slot];
+    }
+    // windows: column ids of edges [cb, cb+W) and row ends rowptr[rb+1 .. rb+W]
+    int64_t cb = p_e, rb = p_row;
+    uint32_t cw[V], cn[V];
+    int64_t rw[V], rn[V];
+    const uint32_t row_lim = a.n_loc;  // rows of this chunk end here (rowptr has row_lim+1 valid entries)
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int64_t e = cb + v * C::L + cl, e2 = e + W;
+        cw[v] = live && e < p_end ? ld_index(a.col + e) : 0u;
+        cn[v] = live && e2 < p_end ? ld_index(a.col + e2) : 0u;
+        const int64_t r = rb + 1 + v * C::L + cl, r2 = r + W;
+        rw[v] = live && r <= row_lim ? a.rowptr[r] : 0;
+        rn[v] = live && r2 <= row_lim ? a.rowptr[r2] : 0;
+    }
+    if (live) {
+        p_rs = a.rowptr[p_row];
+        p_re = __shfl_sync(smask, rw[0], lane0);  // rowptr[p_row + 1]
+        p_full = p_rs >= s_begin && p_re <= p_end;
+        p_phase = p_full ? 0 : 2;
+    }
+
+    // ---- consumer state ----
+    double2 c_sum = {0.0, 0.0}, c_wp = {0.0, 0.0}, c_ac = {0.0, 0.0};
+
+    auto produce = [&](int stage) {
+        // window lookups (all lanes, converged): current edge's column and the next row's end
+        const int ie = static_cast<int>(p_e - cb);
+        const uint32_t u = __shfl_sync(0xffffffffu, pick<V>(cw, ie / C::L), lane0 + ie % C::L);
+        const int ir = static_cast<int>(p_row + 1 - rb);  // window slot of rowptr[p_row + 2]
+        const int64_t next_re = __shfl_sync(0xffffffffu, pick<V>(rw, ir / C::L), lane0 + ir % C::L);
+        uint2 d = make_uint2(0u, kEvNone << 29);
+        if (p_e < p_end) {
+            const uint32_t gr = a.row0 + p_row;
+            const uint32_t deg = static_cast<uint32_t>(p_re - p_rs);
+            if (p_phase == 0) {
+                const double* src = (a.first ? a.w_cur : a.w_io) + static_cast<size_t>(gr) * B + 2 * cl;
+                cp_async16(&ring[stage * 32 + lane], src);
+                d = make_uint2(p_row, (kEvOpW << 29) | deg);
+                p_phase = 1;
+            } else if (p_phase == 1) {
+                if (!a.first) cp_async16(&ring[stage * 32 + lane], a.acc + static_cast<size_t>(p_row) * B + 2 * cl);
+                d = make_uint2(p_row, (kEvOpAcc << 29) | deg);
+                p_phase = 2;
+            } else {
+                cp_async16(&ring[stage * 32 + lane], a.w_cur + static_cast<size_t>(u) * B + 2 * cl);
+                const bool row_done = p_e + 1 == p_re, slot_done = p_e + 1 == p_end;
+                uint32_t ev = kEvEdge;
+                if (row_done && p_full) ev = kEvEndFull;
+                else if (row_done || slot_done) ev = kEvEndPart;
+                d = make_uint2(p_row, (ev << 29) | deg);
+                ++p_e;
+                if (p_e - cb == W) {  // slide the column window
+                    cb += W;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        cw[v] = cn[v];
+                        const int64_t e2 = cb + W + v * C::L + cl;
+                        cn[v] = e2 < p_end ? ld_index(a.col + e2) : 0u;
+                    }
+                }
+                if (row_done && p_e < p_end) {  // advance to the next row
+                    ++p_row;
+                    p_rs = p_re;
+                    p_re = next_re;
+                    p_full = p_re <= p_end;
+                    p_phase = p_full ? 0 : 2;
+                    if (p_row + 1 - rb == W) {  // slide the row-end window
+                        rb += W;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            rw[v] = rn[v];
+                            const int64_t r2 = rb + 1 + W + v * C::L + cl;
+                            rn[v] = r2 <= row_lim ? a.rowptr[r2] : 0;
+                        }
+                    }
+                }
+            }
+        }
+        desc[stage * 32 + lane] = d;
+    };
+
+    auto consume = [&](int stage) {
+        const uint2 d = desc[stage * 32 + lane];
+        const uint32_t ev = d.y >> 29;
+        if (ev == kEvNone) return;
+        const double2 v = ring[stage * 32 + lane];
+        if (ev == kEvOpW) {
+            c_wp = v;
+            return;
+        }
+        if (ev == kEvOpAcc) {
+            c_ac = a.first ? make_double2(0.0, 0.0) : v;
+            return;
+        }
+        c_sum.x += v.x;
+        c_sum.y += v.y;
+        if (ev == kEvEdge) return;
+        const uint32_t row = d.x;
+        const int64_t deg = d.y & ((1u << 28) - 1);
+        if (ev == kEvEndFull) {
+            batch_epilogue<B>(a, row, c_sum, deg, cl, c_wp, c_ac);
+        } else {  // segment of a row shared with neighbouring slots
+            const int64_t rs = a.rowptr[row], re = rs + deg;
+            const int64_t seg0 = rs > s_begin ? rs : s_begin;
+            const int64_t seg1 = re < p_end ? re : p_end;
+            const uint32_t pidx = seg0 == s_begin ? 0u : 1u;
+            reinterpret_cast<double2*>(a.hub_partial + (static_cast<size_t>(slot) * 2 + pidx) * B)[cl] = c_sum;
+            __threadfence();
+            __syncwarp(smask);
+            unsigned prev = 0;
+            const unsigned seg_len = static_cast<unsigned>(seg1 - seg0);
+            if (cl == 0) prev = atomicAdd(&a.hub_count[row], seg_len);
+            prev = __shfl_sync(smask, prev, lane0);
+            if (prev + seg_len == static_cast<unsigned>(deg)) {  // last segment: ordered combine
+                __threadfence();
+                const uint32_t s0 = slot_of_edge(a.slot_edge, a.n_slots, rs);
+                const uint32_t s1 = slot_of_edge(a.slot_edge, a.n_slots, re - 1);
+                double2 y = {0.0, 0.0};
+                for (uint32_t q = s0; q <= s1; ++q) {
+                    const int64_t qb = a.slot_edge[q];
+                    if (a.slot_edge[q + 1] == qb) continue;  // empty slot
+                    const uint32_t qi = (rs > qb ? rs : qb) == qb ? 0u : 1u;
+                    const double2 t = __ldcg(reinterpret_cast<const double2*>(
+                                                 a.hub_partial + (static_cast<size_t>(q) * 2 + qi) * B) + cl);
+                    y.x += t.x;
+                    y.y += t.y;
+                }
+                if (cl == 0) a.hub_count[row] = 0u;
+                double2 wp, ac;
+                batch_prefetch<B>(a, row, cl, wp, ac);
+                batch_epilogue<B>(a, row, y, deg, cl, wp, ac);
+            }
+        }
+        c_sum = make_double2(0.0, 0.0);
+    };
+
+#pragma unroll 1
+    for (int st = 0; st < C::S - 1; ++st) {
+        produce(st);
+        cp_async_commit();
+    }
+    int stage_p = C::S - 1, stage_c = 0;
+#pragma unroll 1
+    while (true) {
+        produce(stage_p);
+        cp_async_commit();
+        cp_async_wait<C::S - 1>();  // this lane's copies of stage_c have landed
+        consume(stage_c);
+        stage_p = stage_p + 1 == C::S ? 0 : stage_p + 1;
+        stage_c = stage_c + 1 == C::S ? 0 : stage_c + 1;
+        if (!__any_sync(0xffffffffu, p_e < p_end)) {  // drain the S-1 stages in flight
+            cp_async_wait<0>();
+#pragma unroll 1
+            for (int st = 0; st < C::S - 1; ++st) {
+                consume(stage_c);
+                stage_c = stage_c + 1 == C::S ? 0 : stage_c + 1;
+            }
+            break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
 
@@ -727,6 +968,59 @@ int staged_occupancy() {
     int blocks = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_staged_kernel<B>, kBatchThreads, bytes);
     return blocks;
+}
+
+template <int B>
+void launch_stream_t(const BatchArgs& a, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t bytes = stream_smem_bytes<B>();
+    if (!configured) {
+        cudaFuncSetAttribute(cheby_batch_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+        configured = true;
+    }
+    cheby_batch_stream_kernel<B><<<grid, kStreamWarps * 32, bytes, st>>>(a);
+}
+
+template <int B>
+int stream_occupancy_t() {
+    const size_t bytes = stream_smem_bytes<B>();
+    cudaFuncSetAttribute(cheby_batch_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bytes));
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_stream_kernel<B>, kStreamWarps * 32, bytes);
+    return blocks;
+}
+
+// The register-pipelined slot kernel is the batched default (fastest measured,
+// profiles/r01); CPG_BATCH_KERNEL=stream selects the cp.async streaming kernel
+// (issue-bound: ~25 instructions per gathered row) for comparison.
+bool batch_uses_stream() {
+    static const bool on = [] {
+        const char* e = std::getenv("CPG_BATCH_KERNEL");
+        return e && std::string(e) == "stream";
+    }();
+    return on;
+}
+
+void launch_stream(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    switch (B) {
+    case 4: launch_stream_t<4>(a, grid, st); break;
+    case 8: launch_stream_t<8>(a, grid, st); break;
+    case 16: launch_stream_t<16>(a, grid, st); break;
+    case 32: launch_stream_t<32>(a, grid, st); break;
+    default: launch_stream_t<64>(a, grid, st); break;
+    }
+}
+
+int stream_occupancy(int B) {
+    switch (B) {
+    case 4: return stream_occupancy_t<4>();
+    case 8: return stream_occupancy_t<8>();
+    case 16: return stream_occupancy_t<16>();
+    case 32: return stream_occupancy_t<32>();
+    default: return stream_occupancy_t<64>();
+    }
 }
 
 int batch_staged_occupancy(int B) {
