@@ -334,12 +334,14 @@ __device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, i
     }
 }
 
-template <int B>
-__global__ void __launch_bounds__(kBatchThreads, B == 64 ? 4 : 3) cheby_batch_kernel(const BatchArgs a) {
+// Occupancy over registers: 4 CTAs x 8 warps per SM (64 regs) measured best
+// for B = 16 and 64 (profiles/r01/slot_sweep.txt), even with small spills.
+template <int B, int U = 8, int MINB = 4>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const BatchArgs a) {
     constexpr int L = B / 2;      // lanes per row slot
     constexpr int RPW = 32 / L;   // row slots per warp
     constexpr int V = 32 / L;     // indices per lane per 32-edge chunk
-    constexpr int U = 8;          // row gathers in flight per lane
+    // U: row gathers in flight per lane
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const unsigned smask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
@@ -1032,6 +1034,37 @@ int batch_staged_occupancy(int B) {
     }
 }
 
+template <int B, int U, int MINB>
+void launch_slot(const BatchArgs& a, cudaStream_t st) {
+    int occ = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_kernel<B, U, MINB>, kBatchThreads, 0);
+    cheby_batch_kernel<B, U, MINB><<<occ * sms, kBatchThreads, 0, st>>>(a);
+}
+
+template <int B>
+bool launch_slot_b(const BatchArgs& a, int cfg, cudaStream_t st) {
+    switch (cfg) {
+    case 41: launch_slot<B, 4, 4>(a, st); return true;
+    case 45: launch_slot<B, 4, 5>(a, st); return true;
+    case 46: launch_slot<B, 4, 6>(a, st); return true;
+    case 64: launch_slot<B, 6, 4>(a, st); return true;
+    case 84: launch_slot<B, 8, 4>(a, st); return true;
+    case 85: launch_slot<B, 8, 5>(a, st); return true;
+    default: return false;
+    }
+}
+
+bool launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
+    switch (B) {
+    case 16: return launch_slot_b<16>(a, cfg, st);
+    case 32: return launch_slot_b<32>(a, cfg, st);
+    case 64: return launch_slot_b<64>(a, cfg, st);
+    default: return false;
+    }
+}
+
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
     if (batch_uses_tiles(B)) {
         switch (B) {
@@ -1041,6 +1074,11 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
         default: launch_staged<32>(a, grid, st); return;
         }
     }
+    static const int cfg = [] {  // tuning hook: CPG_SLOT_CFG = U*10 + MINB
+        const char* e = std::getenv("CPG_SLOT_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (cfg && launch_slot_cfg(a, B, cfg, st)) return;
     switch (B) {
     case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
     case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
