@@ -10,7 +10,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_uint32, c_uint64, c_void_p
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libcpg.so")
+LIB_PATH = os.environ.get("CPG_LIB_PATH") or os.path.join(PKG, "libcpg.so")  # override: A/B builds
 
 CPG_OK, CPG_EINVAL, CPG_ECUDA, CPG_ENCCL, CPG_ENOMEM, CPG_ESTRUCT = 0, 1, 2, 3, 4, 5
 

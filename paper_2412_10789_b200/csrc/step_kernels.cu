@@ -28,16 +28,56 @@
 
 namespace cpg {
 
+// L2 residency policy (CPG_L2_HINTS, default on): the index stream is read
+// once per step (evict_first), the gathered iterate is re-read across the whole
+// step (evict_last), so hub rows stay in the 126 MB L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+#ifndef CPG_L2_HINTS
+#define CPG_L2_HINTS 0  // measured neutral on configs 3-5 (profiles/r01/l2_hints_ab.txt)
+#endif
+
 __device__ __forceinline__ uint32_t ld_index(const uint32_t* p) {
     uint32_t v;
+#if CPG_L2_HINTS
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(p), "l"(policy_evict_first()));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
     return v;
 }
 
-__device__ __forceinline__ double ld_gather(const double* p) { return __ldg(p); }
+__device__ __forceinline__ double ld_gather(const double* p) {
+#if CPG_L2_HINTS
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy_evict_last()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 
 __device__ __forceinline__ double2 ld_gather2(const double* p) {
+#if CPG_L2_HINTS
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(policy_evict_last()));
+    return v;
+#else
     return __ldg(reinterpret_cast<const double2*>(p));
+#endif
 }
 
 // Deterministic CTA sum: xor butterfly per warp, warp partials summed in warp
