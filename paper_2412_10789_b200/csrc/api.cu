@@ -293,7 +293,8 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
     uint32_t launches = 0;
     const size_t cols = B;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
-    const bool stream = batch_uses_stream();
+    const bool bulk = batch_uses_bulk(static_cast<int>(B));
+    const bool stream = !bulk && batch_uses_stream();
     const bool staged = !stream && batch_uses_tiles(static_cast<int>(B));
     const int occ = staged ? batch_staged_occupancy(static_cast<int>(B)) : batch_occupancy();
     uint32_t part_off = 0;  // partial slots of earlier chunks
@@ -318,7 +319,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         part_off = 0;
         for (uint32_t c = 0; c < C; ++c) {
             const ItemTable& t = g->btables[c];
-            if (stream) {
+            if (bulk || stream) {
                 b.slot_edge = t.slot_edge;
                 b.slot_row = t.slot_row;
                 b.n_slots = t.n_slots;
@@ -327,7 +328,10 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                 b.hub_partial = g->bhub_partial + static_cast<size_t>(part_off) * B;
                 part_off += 2 * t.n_slots;
                 if (prof) prof->before(st);
-                launch_stream(b, static_cast<int>(B), static_cast<int>(t.grid), st);
+                if (bulk)
+                    launch_bulk(b, static_cast<int>(B), static_cast<int>(t.grid), st);
+                else
+                    launch_stream(b, static_cast<int>(B), static_cast<int>(t.grid), st);
                 if (prof) prof->after(st);
                 ++launches;
                 gather_chunk(g, b.w_io, c, cols, st);

@@ -96,6 +96,9 @@ int batch_staged_occupancy(int B);
 void launch_stream(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int stream_occupancy(int B);
 bool batch_uses_stream();
+bool batch_uses_bulk(int B);
+void launch_bulk(const BatchArgs& a, int B, int grid, cudaStream_t st);
+int bulk_occupancy(int B);
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,

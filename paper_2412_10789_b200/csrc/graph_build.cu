@@ -373,7 +373,19 @@ void ensure_batch_tables(cpg_graph* g, int B) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
-        if (batch_uses_stream()) {
+        if (batch_uses_bulk(B)) {
+            // one edge-balanced range per warp, >= 256 edges each
+            const uint32_t per_cta = 8;
+            int64_t len = 0, b0 = 0;
+            CPG_CUDA(cudaMemcpy(&b0, g->rowptr + t.row_begin, sizeof(b0), cudaMemcpyDeviceToHost));
+            CPG_CUDA(cudaMemcpy(&len, g->rowptr + t.row_end, sizeof(len), cudaMemcpyDeviceToHost));
+            len -= b0;
+            uint64_t n_slots = static_cast<uint64_t>(std::max(1, bulk_occupancy(B)) * g->sm_count) * per_cta;
+            n_slots = std::max<uint64_t>(1, std::min<uint64_t>(n_slots, static_cast<uint64_t>(len) / 256));
+            t.grid = static_cast<uint32_t>((n_slots + per_cta - 1) / per_cta);
+            build_stream_slots(g->rowptr, t, static_cast<uint32_t>(n_slots), g->stream);
+            slots += 2 * static_cast<uint32_t>(n_slots);
+        } else if (batch_uses_stream()) {
             // edge-balanced slots: one per lane group of every resident warp
             // edge-balanced slots, one per lane group of every resident warp, but
             // >= 64 edges per slot (small graphs get fewer slots)

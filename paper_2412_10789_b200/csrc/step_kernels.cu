@@ -910,6 +910,192 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 2) cheby_batch_stream_kerne
 }
 
 // ---------------------------------------------------------------------------
+// Bulk-copy (TMA) batched step, B in {4, 8, 16, 32}.  Each warp owns an
+// edge-balanced contiguous edge range.  Per stage of 32 edges every lane issues
+// ONE cp.async.bulk (the TMA engine) copying the gathered B*8-byte row of
+// w_k for its edge into a per-warp shared-memory ring; completion is tracked
+// by an mbarrier per stage (expect_tx), so in-flight bytes cost neither
+// registers nor LSU issue slots.  B lanes then walk the staged edges in order
+// (segmented by row, bit-reproducible), finished rows are queued in shared
+// memory and their fused epilogues run 32 rows at a time so the operand loads
+// overlap.  Rows cut by a warp boundary use the ordered last-arriver combine.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int B>
+struct BulkCfg {
+    static constexpr int WARPS = 8;
+    static constexpr int STAGE_BYTES = 32 * B * 8;
+    static constexpr int S0 = (20 * 1024) / STAGE_BYTES;
+    static constexpr int S = S0 < 2 ? 2 : (S0 > 8 ? 8 : S0);  // ring stages per warp
+    static constexpr int FR = 32;                              // queued finished rows
+    static constexpr int RAW_BYTES = S * STAGE_BYTES + FR * B * 8 + FR * 16 + S * 8;
+    static constexpr int WARP_BYTES = (RAW_BYTES + 127) / 128 * 128;  // 16-B bulk-copy alignment per warp
+};
+
+template <int B>
+size_t bulk_smem_bytes() {
+    return static_cast<size_t>(BulkCfg<B>::WARPS) * BulkCfg<B>::WARP_BYTES;
+}
+
+template <int B>
+__device__ __forceinline__ void bulk_flush(const BatchArgs& a, const double* fin, const uint2* fin_meta, int nf,
+                                           int lane) {
+    // nf finished rows x B columns: each lane takes (row, column pair) items.
+    constexpr int PAIRS = B / 2;
+    for (int it = lane; it < nf * PAIRS; it += 32) {
+        const int q = it / PAIRS, cl = it % PAIRS;
+        const uint32_t row = fin_meta[q].x;
+        const int64_t deg = fin_meta[q].y;
+        double2 wp, ac;
+        batch_prefetch<B>(a, row, cl, wp, ac);
+        const double2 y = reinterpret_cast<const double2*>(fin + static_cast<size_t>(q) * B)[cl];
+        batch_epilogue<B>(a, row, y, deg, cl, wp, ac);
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(BulkCfg<B>::WARPS * 32, 1) cheby_batch_bulk_kernel(const BatchArgs a) {
+    using C = BulkCfg<B>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem_raw + static_cast<size_t>(warp) * C::WARP_BYTES;
+    double* ring = reinterpret_cast<double*>(base);                              // [S][32][B]
+    double* fin = reinterpret_cast<double*>(base + C::S * C::STAGE_BYTES);       // [FR][B]
+    uint2* fin_meta = reinterpret_cast<uint2*>(base + C::S * C::STAGE_BYTES + C::FR * B * 8);  // [FR]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::S * C::STAGE_BYTES + C::FR * B * 8 + C::FR * 16);
+
+    const uint32_t w = blockIdx.x * C::WARPS + warp;
+    if (w >= a.n_slots) return;
+    const int64_t e_begin = a.slot_edge[w], e_end = a.slot_edge[w + 1];
+    if (e_begin >= e_end) return;
+
+    if (lane == 0)
+        for (int st = 0; st < C::S; ++st) mbar_init(&bar[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+
+    // producer: stage t covers edges [e_begin + 32t, +32)
+    const int64_t n_edges = e_end - e_begin;
+    const int64_t n_stages = (n_edges + 31) / 32;
+    uint32_t col_next = lane < n_edges ? ld_index(a.col + e_begin + lane) : 0u;
+    auto issue = [&](int64_t t) {
+        const int st = static_cast<int>(t % C::S);
+        const int64_t e0 = e_begin + 32 * t;
+        const int nvalid = static_cast<int>(e_end - e0 < 32 ? e_end - e0 : 32);
+        const uint32_t u = col_next;
+        // prefetch the next stage's column ids
+        const int64_t en = e0 + 32 + lane;
+        col_next = en < e_end ? ld_index(a.col + en) : 0u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was read by generic loads
+        if (lane == 0) mbar_arrive_expect_tx(&bar[st], static_cast<uint32_t>(nvalid) * B * 8);
+        __syncwarp();
+        if (lane < nvalid)
+            bulk_g2s(ring + (static_cast<size_t>(st) * 32 + lane) * B, a.w_cur + static_cast<size_t>(u) * B, B * 8,
+                     &bar[st]);
+    };
+
+    // consumer state (uniform across the warp; lanes < B hold one column each)
+    uint32_t row = a.slot_row[w];
+    int64_t row_rs = a.rowptr[row], row_re = a.rowptr[row + 1];
+    double sum = 0.0;
+    int nf = 0;
+
+    int64_t t_issue = 0;
+    for (; t_issue < n_stages && t_issue < C::S; ++t_issue) issue(t_issue);
+
+    for (int64_t t = 0; t < n_stages; ++t) {
+        const int st = static_cast<int>(t % C::S);
+        mbar_wait(&bar[st], static_cast<uint32_t>((t / C::S) & 1));
+        const int64_t e0 = e_begin + 32 * t;
+        const int nvalid = static_cast<int>(e_end - e0 < 32 ? e_end - e0 : 32);
+        const double* stage = ring + static_cast<size_t>(st) * 32 * B;
+        for (int j = 0; j < nvalid; ++j) {
+            if (lane < B) sum += stage[j * B + lane];
+            const int64_t e = e0 + j + 1;
+            if (e == row_re || e == e_end) {  // row (or this warp's segment of it) ends here
+                const bool full = row_rs >= e_begin && row_re <= e_end;
+                const int64_t deg = row_re - row_rs;
+                if (full) {
+                    if (lane < B) fin[nf * B + lane] = sum;
+                    if (lane == 0) fin_meta[nf] = make_uint2(row, static_cast<uint32_t>(deg));
+                    ++nf;
+                    if (nf == C::FR) {
+                        __syncwarp();
+                        bulk_flush<B>(a, fin, fin_meta, nf, lane);
+                        __syncwarp();
+                        nf = 0;
+                    }
+                } else {
+                    const int64_t seg0 = row_rs > e_begin ? row_rs : e_begin;
+                    const int64_t seg1 = row_re < e_end ? row_re : e_end;
+                    const uint32_t pidx = seg0 == e_begin ? 0u : 1u;
+                    if (lane < B) a.hub_partial[(static_cast<size_t>(w) * 2 + pidx) * B + lane] = sum;
+                    __threadfence();
+                    __syncwarp();
+                    unsigned prev = 0;
+                    if (lane == 0) prev = atomicAdd(&a.hub_count[row], static_cast<unsigned>(seg1 - seg0));
+                    prev = __shfl_sync(0xffffffffu, prev, 0);
+                    if (prev + static_cast<unsigned>(seg1 - seg0) == static_cast<unsigned>(deg)) {
+                        __threadfence();
+                        const uint32_t s0 = slot_of_edge(a.slot_edge, a.n_slots, row_rs);
+                        const uint32_t s1 = slot_of_edge(a.slot_edge, a.n_slots, row_re - 1);
+                        double y = 0.0;
+                        for (uint32_t q = s0; q <= s1; ++q) {
+                            const int64_t qb = a.slot_edge[q];
+                            if (a.slot_edge[q + 1] == qb) continue;
+                            const uint32_t qi = (row_rs > qb ? row_rs : qb) == qb ? 0u : 1u;
+                            if (lane < B) y += __ldcg(a.hub_partial + (static_cast<size_t>(q) * 2 + qi) * B + lane);
+                        }
+                        if (lane == 0) a.hub_count[row] = 0u;
+                        if (lane < B) fin[nf * B + lane] = y;
+                        if (lane == 0) fin_meta[nf] = make_uint2(row, static_cast<uint32_t>(deg));
+                        ++nf;
+                        if (nf == C::FR) {
+                            __syncwarp();
+                            bulk_flush<B>(a, fin, fin_meta, nf, lane);
+                            __syncwarp();
+                            nf = 0;
+                        }
+                    }
+                }
+                sum = 0.0;
+                if (e < e_end) {  // next row (rows never have degree 0 inside an edge range)
+                    ++row;
+                    row_rs = row_re;
+                    row_re = a.rowptr[row + 1];
+                }
+            }
+        }
+        __syncwarp();  // every lane is done reading this stage
+        if (t_issue < n_stages) issue(t_issue++);
+    }
+    __syncwarp();
+    bulk_flush<B>(a, fin, fin_meta, nf, lane);
+}
+
+// ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
 
@@ -1037,6 +1223,61 @@ int stream_occupancy_t() {
 // The register-pipelined slot kernel is the batched default (fastest measured,
 // profiles/r01); CPG_BATCH_KERNEL=stream selects the cp.async streaming kernel
 // (issue-bound: ~25 instructions per gathered row) for comparison.
+template <int B>
+void launch_bulk_t(const BatchArgs& a, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t bytes = bulk_smem_bytes<B>();
+    if (!configured) {
+        cudaFuncSetAttribute(cheby_batch_bulk_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+        configured = true;
+    }
+    cheby_batch_bulk_kernel<B><<<grid, BulkCfg<B>::WARPS * 32, bytes, st>>>(a);
+}
+
+void launch_bulk(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    switch (B) {
+    case 4: launch_bulk_t<4>(a, grid, st); break;
+    case 8: launch_bulk_t<8>(a, grid, st); break;
+    case 16: launch_bulk_t<16>(a, grid, st); break;
+    default: launch_bulk_t<32>(a, grid, st); break;
+    }
+}
+
+int bulk_occupancy(int B) {
+    const size_t bytes = B == 4 ? bulk_smem_bytes<4>() : B == 8 ? bulk_smem_bytes<8>() : B == 16 ? bulk_smem_bytes<16>()
+                                                                                                   : bulk_smem_bytes<32>();
+    int blocks = 0;
+    switch (B) {
+    case 4:
+        cudaFuncSetAttribute(cheby_batch_bulk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<4>, 256, bytes);
+        break;
+    case 8:
+        cudaFuncSetAttribute(cheby_batch_bulk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<8>, 256, bytes);
+        break;
+    case 16:
+        cudaFuncSetAttribute(cheby_batch_bulk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<16>, 256, bytes);
+        break;
+    default:
+        cudaFuncSetAttribute(cheby_batch_bulk_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<32>, 256, bytes);
+        break;
+    }
+    return blocks;
+}
+
+// CPG_BATCH_KERNEL=bulk selects the TMA bulk-copy kernel for B <= 32.
+bool batch_uses_bulk(int B) {
+    static const bool on = [] {
+        const char* e = std::getenv("CPG_BATCH_KERNEL");
+        return e && std::string(e) == "bulk";
+    }();
+    return on && B <= 32;
+}
+
 bool batch_uses_stream() {
     static const bool on = [] {
         const char* e = std::getenv("CPG_BATCH_KERNEL");
