@@ -293,11 +293,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
     uint32_t launches = 0;
     const size_t cols = B;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
-    const bool bulk = batch_uses_bulk(static_cast<int>(B));
-    const bool stream = !bulk && batch_uses_stream();
-    const bool staged = !stream && batch_uses_tiles(static_cast<int>(B));
-    const int occ = staged ? batch_staged_occupancy(static_cast<int>(B)) : batch_occupancy();
-    uint32_t part_off = 0;  // partial slots of earlier chunks
+    const int occ = batch_occupancy();
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
     launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
     ++launches;
@@ -316,36 +312,16 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.first = k == 1;
         b.last = k == K;
         if (k > 1) wait_gathers(g, st);
-        part_off = 0;
         for (uint32_t c = 0; c < C; ++c) {
             const ItemTable& t = g->btables[c];
-            if (bulk || stream) {
-                b.slot_edge = t.slot_edge;
-                b.slot_row = t.slot_row;
-                b.n_slots = t.n_slots;
-                b.n_loc = t.row_end;
-                b.row0 = chunk_row0(g, c);
-                b.hub_partial = g->bhub_partial + static_cast<size_t>(part_off) * B;
-                part_off += 2 * t.n_slots;
-                if (prof) prof->before(st);
-                if (bulk)
-                    launch_bulk(b, static_cast<int>(B), static_cast<int>(t.grid), st);
-                else
-                    launch_stream(b, static_cast<int>(B), static_cast<int>(t.grid), st);
-                if (prof) prof->after(st);
-                ++launches;
-                gather_chunk(g, b.w_io, c, cols, st);
-                continue;
-            }
             b.hub_items = t.items;
             b.n_hub_items = t.n_hub_items;
-            b.n_items = t.n_items;
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
-            const uint32_t jobs = staged ? t.n_items : t.n_hub_items + (t.row_end - b.hub_rows);
+            const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
             if (jobs) {
-                const int grid = staged ? table_grid(g, t.n_items, occ) : occ * g->sm_count;
+                const int grid = occ * g->sm_count;
                 if (prof) prof->before(st);
                 launch_batch(b, static_cast<int>(B), grid, st);
                 if (prof) prof->after(st);
@@ -617,11 +593,8 @@ int cpg_graph_destroy(cpg_graph* g) {
         cudaDeviceSynchronize();
         if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
         for (auto& t : g->tables) cudaFree(t.items);
-        for (auto& t : g->btables) {
+        for (auto& t : g->btables)
             if (t.items) cudaFree(t.items);
-            if (t.slot_edge) cudaFree(t.slot_edge);
-            if (t.slot_row) cudaFree(t.slot_row);
-        }
         for (auto e : g->chunk_ev)
             if (e) cudaEventDestroy(e);
         if (g->comm_stream) cudaStreamDestroy(g->comm_stream);

@@ -16,10 +16,6 @@ struct ItemTable {
     WorkItem* items = nullptr;
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0;
     uint32_t row_begin = 0, row_end = 0;
-    // streaming batched step: edge-balanced slots over the chunk's edges
-    int64_t* slot_edge = nullptr;  // [n_slots+1]
-    uint32_t* slot_row = nullptr;  // [n_slots]
-    uint32_t n_slots = 0, grid = 0;
 };
 } // namespace cpg
 
@@ -92,13 +88,7 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st);
 int step_occupancy(int tile);
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int batch_occupancy();
-int batch_staged_occupancy(int B);
-void launch_stream(const BatchArgs& a, int B, int grid, cudaStream_t st);
-int stream_occupancy(int B);
-bool batch_uses_stream();
-bool batch_uses_bulk(int B);
-void launch_bulk(const BatchArgs& a, int B, int grid, cudaStream_t st);
-int bulk_occupancy(int B);
+
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,

@@ -16,7 +16,6 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <cstdlib>
 
 namespace cpg {
 
@@ -33,25 +32,6 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
 constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
-// Staged (cp.async) batched tiles for B <= 32: a tile stages the gathered
-// rows of <= batch_tile_edges(B) edges (kBatchTileBytes of shared memory per
-// buffer, double-buffered) and has <= batch_tile_rows(B) rows (2 epilogue rows
-// per row slot of B/2 lanes).
-constexpr int kBatchTileBytes = 32768;
-// Measured on B200 (profiles/r01): the register-pipelined slot kernel beats the
-// staged kernel at every width on configs 3 and 5, so staging is opt-in
-// (CPG_BATCH_STAGED=1) and only wins on tiny graphs (config 1).
-__host__ inline bool batch_uses_tiles(int B) {
-    static const bool staged = [] {
-        const char* e = std::getenv("CPG_BATCH_STAGED");
-        return e && e[0] == '1';
-    }();
-    return staged && B <= 32;
-}
-__host__ __device__ constexpr int batch_tile_edges(int B) { return kBatchTileBytes / (8 * B); }
-__host__ __device__ constexpr int batch_tile_rows(int B) {
-    return (2 * kBatchThreads / (B / 2)) < 256 ? (2 * kBatchThreads / (B / 2)) : 256;
-}
 // Hub piece for width B: one row slot (B/2 lanes) handles a piece, so the
 // piece shrinks with the slot width to keep pieces equally long in time.
 __host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges * B / 64; }
@@ -94,21 +74,11 @@ struct StepArgs {
     int last;              // write out = d * acc instead of acc
 };
 
-// Streaming batched step (cheby_batch_stream_kernel): each lane slot (B/2
-// lanes) walks an edge-balanced contiguous edge range through a per-warp
-// cp.async ring of kStreamStages stages.
-constexpr int kStreamStages = 16;
-constexpr int kStreamWarps = 8;
-
 struct BatchArgs {
     const int64_t* rowptr;
     const uint32_t* col;
-    const int64_t* slot_edge;   // streaming: [n_slots+1] first edge of each slot
-    const uint32_t* slot_row;   // streaming: [n_slots] row holding the slot's first edge
-    uint32_t n_slots;
-    const WorkItem* hub_items;  // hub pieces (row, slot_base, piece | hub bit); tiled: + row tiles
+    const WorkItem* hub_items;  // hub pieces (row, partial slot base, first edge | count | hub bit)
     uint32_t n_hub_items;
-    uint32_t n_items;           // tiled kernel: hub pieces + tiles
     uint32_t hub_rows;          // rows [0, hub_rows) are hubs
     uint32_t n_loc;
     const double* w_cur;        // [n_pad][64]

@@ -190,33 +190,7 @@ void build_hub_items(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_
     *n_items_out = total;
 }
 
-__global__ void k_slots(const int64_t* rowptr, uint32_t row0, uint32_t row1, uint32_t n_slots, int64_t* slot_edge,
-                        uint32_t* slot_row) {
-    const int64_t e_begin = rowptr[row0], len = rowptr[row1] - e_begin;
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s <= n_slots; s += gridDim.x * blockDim.x) {
-        const int64_t e = e_begin + (len * static_cast<int64_t>(s)) / n_slots;
-        slot_edge[s] = e;
-        if (s == n_slots) continue;
-        uint32_t lo = row0, hi = row1;  // last row r with rowptr[r] <= e
-        while (hi - lo > 1) {
-            const uint32_t mid = lo + (hi - lo) / 2;
-            if (rowptr[mid] <= e) lo = mid; else hi = mid;
-        }
-        slot_row[s] = lo;
-    }
-}
-
 } // namespace
-
-// Edge-balanced slots for the streaming batched step over rows [row0, row1).
-void build_stream_slots(const int64_t* rowptr, ItemTable& t, uint32_t n_slots, cudaStream_t st) {
-    t.n_slots = n_slots;
-    t.slot_edge = dalloc<int64_t>(static_cast<size_t>(n_slots) + 1);
-    t.slot_row = dalloc<uint32_t>(n_slots);
-    k_slots<<<grid_for(static_cast<uint64_t>(n_slots) + 1), kT, 0, st>>>(rowptr, t.row_begin, t.row_end, n_slots,
-                                                                         t.slot_edge, t.slot_row);
-    CPG_CUDA(cudaStreamSynchronize(st));
-}
 
 // Work table over local rows [row0, row1): hub pieces (rows with deg > chunk,
 // split into `piece`-edge pieces, partial slots from slot_off) then row tiles
@@ -361,56 +335,20 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
 
 void ensure_batch_tables(cpg_graph* g, int B) {
     if (!g->btables.empty() && g->bitems_width == B) return;
-    for (auto& t : g->btables) {
+    for (auto& t : g->btables)
         if (t.items) cudaFree(t.items);
-        if (t.slot_edge) cudaFree(t.slot_edge);
-        if (t.slot_row) cudaFree(t.slot_row);
-    }
     g->btables.clear();
     uint32_t slots = 0;
     const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
+    const int64_t hb = batch_hub_edges(B);
     for (uint32_t c = 0; c < C; ++c) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
-        if (batch_uses_bulk(B)) {
-            // one edge-balanced range per warp, >= 256 edges each
-            const uint32_t per_cta = 8;
-            int64_t len = 0, b0 = 0;
-            CPG_CUDA(cudaMemcpy(&b0, g->rowptr + t.row_begin, sizeof(b0), cudaMemcpyDeviceToHost));
-            CPG_CUDA(cudaMemcpy(&len, g->rowptr + t.row_end, sizeof(len), cudaMemcpyDeviceToHost));
-            len -= b0;
-            uint64_t n_slots = static_cast<uint64_t>(std::max(1, bulk_occupancy(B)) * g->sm_count) * per_cta;
-            n_slots = std::max<uint64_t>(1, std::min<uint64_t>(n_slots, static_cast<uint64_t>(len) / 256));
-            t.grid = static_cast<uint32_t>((n_slots + per_cta - 1) / per_cta);
-            build_stream_slots(g->rowptr, t, static_cast<uint32_t>(n_slots), g->stream);
-            slots += 2 * static_cast<uint32_t>(n_slots);
-        } else if (batch_uses_stream()) {
-            // edge-balanced slots: one per lane group of every resident warp
-            // edge-balanced slots, one per lane group of every resident warp, but
-            // >= 64 edges per slot (small graphs get fewer slots)
-            const uint32_t per_cta = kStreamWarps * (64 / B);
-            int64_t len = 0, b0 = 0;
-            CPG_CUDA(cudaMemcpy(&b0, g->rowptr + t.row_begin, sizeof(b0), cudaMemcpyDeviceToHost));
-            CPG_CUDA(cudaMemcpy(&len, g->rowptr + t.row_end, sizeof(len), cudaMemcpyDeviceToHost));
-            len -= b0;
-            uint64_t n_slots = static_cast<uint64_t>(std::max(1, stream_occupancy(B)) * g->sm_count) * per_cta;
-            n_slots = std::max<uint64_t>(1, std::min<uint64_t>(n_slots, static_cast<uint64_t>(len) / 64));
-            t.grid = static_cast<uint32_t>((n_slots + per_cta - 1) / per_cta);
-            build_stream_slots(g->rowptr, t, static_cast<uint32_t>(n_slots), g->stream);
-            slots += 2 * n_slots;  // two partial segments per slot
-        } else if (batch_uses_tiles(B)) {
-            // staged tiles: <= E(B) edges and <= R(B) rows, hubs split in E-edge pieces
-            t = build_item_table(g->rowptr, c * g->cr, (c + 1) * g->cr, batch_tile_edges(B) / 2, batch_tile_rows(B),
-                                 batch_tile_edges(B), slots, g->stream);
-            slots += t.n_hub_items;
-        } else {
-            const int64_t hb = batch_hub_edges(B);
-            build_hub_items(g->rowptr, c * g->cr, (c + 1) * g->cr, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items,
-                            0, g->stream);
-            t.n_items = t.n_hub_items;
-            slots += t.n_hub_items;
-        }
+        build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0,
+                        g->stream);
+        t.n_items = t.n_hub_items;
+        slots += t.n_hub_items;
         g->btables.push_back(t);
     }
     g->n_bpartials = slots;

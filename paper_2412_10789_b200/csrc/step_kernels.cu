@@ -12,7 +12,7 @@
 //   last step: out(v) = d_v acc(v)                      (= yhat, solvers.cpp:225)
 //
 // Load balance for power-law degrees (rows are degree-sorted at upload):
-//   * row tiles: <= 2048 edges; indices streamed coalesced (L1 no-allocate),
+//   * row tiles: <= 1024 or 4096 edges (per graph); indices streamed coalesced (L1 no-allocate),
 //     gathered values staged in shared memory, then each row reduced by a
 //     power-of-two lane group sized to the tile's mean degree;
 //   * hub rows (deg > 1024): split into 4096-edge pieces, one CTA each; the
@@ -22,13 +22,13 @@
 // run (no floating-point atomics).
 #include <cuda_runtime.h>
 
-#include <string>
+#include <cstdlib>
 
 #include "device_graph.cuh"
 
 namespace cpg {
 
-// L2 residency policy (CPG_L2_HINTS, default on): the index stream is read
+// L2 residency policy (CPG_L2_HINTS, default off): the index stream is read
 // once per step (evict_first), the gathered iterate is re-read across the whole
 // step (evict_last), so hub rows stay in the 126 MB L2.
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -448,654 +448,6 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 }
 
 // ---------------------------------------------------------------------------
-// Staged batched step (B <= 32): persistent CTAs walk the batched item table
-// (hub pieces, then row tiles).  For each item the gathered neighbour rows
-// (E = 32 KB / (8B) edges x B columns) are copied HBM/L2 -> shared memory with
-// cp.async (16 B per copy, no register staging), double-buffered so the copies
-// of item t+1 are in flight while item t is reduced.  In-flight bytes are
-// bounded by shared memory (2 x 32 KB per CTA), not by registers.  Row slots of
-// L = B/2 lanes then sum their rows' staged vectors in edge order
-// (deterministic) and run the fused epilogue.  Hub pieces reduce over their E
-// edges (fixed slot order) and use the ordered last-arriver combine.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
-
-template <int B>
-struct StagedTile {
-    static constexpr int L = B / 2;                  // lanes (double2 columns) per row slot
-    static constexpr int SLOTS = kBatchThreads / L;  // row slots per CTA
-    static constexpr int E = batch_tile_edges(B);    // staged edges per item
-    static constexpr int R = batch_tile_rows(B);     // rows per tile
-    static constexpr int RPS = R / SLOTS;            // epilogue rows per slot
-    static constexpr int PER = E * L / kBatchThreads; // 16-B copies per thread per item
-    double2 buf[2][E][L];
-    int64_t rp[2][R + 1];
-    double2 red[SLOTS][L];
-    int flag;
-};
-
-// Raw 16-B work item; fields decoded on use (keeps the 3-deep pipeline in registers).
-struct ItemInfo {
-    uint32_t a, b;
-    uint64_t c;
-    __device__ __forceinline__ bool hub() const { return (c & kHubBit) != 0; }
-    __device__ __forceinline__ uint32_t rb() const { return a; }
-    __device__ __forceinline__ uint32_t re() const { return hub() ? a + 1 : b; }
-    __device__ __forceinline__ uint32_t slot() const { return b; }
-    __device__ __forceinline__ int64_t e0() const { return code_e0(c); }
-    __device__ __forceinline__ int cnt() const { return code_cnt(c); }
-};
-
-template <int B>
-__device__ __forceinline__ ItemInfo decode_item(const BatchArgs& a, uint32_t i) {
-    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + i);
-    ItemInfo it;
-    it.a = raw.x;
-    it.b = raw.y;
-    it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-    return it;
-}
-
-// Issue the cp.async copies of one item into buffer `b`, given its column ids.
-template <int B>
-__device__ __forceinline__ void stage_item(const BatchArgs& a, StagedTile<B>& sm, int b, const ItemInfo& it,
-                                           const uint32_t (&cols)[StagedTile<B>::PER]) {
-    using T = StagedTile<B>;
-    const int cnt = it.cnt();
-#pragma unroll
-    for (int i = 0; i < T::PER; ++i) {
-        const int k = i * kBatchThreads + threadIdx.x;
-        const int e = k / T::L, part = k % T::L;
-        if (e < cnt) cp_async16(&sm.buf[b][e][part], a.w_cur + static_cast<size_t>(cols[i]) * B + 2 * part);
-    }
-    if (!it.hub()) {
-        const int nr = static_cast<int>(it.re() - it.rb());
-        for (int j = threadIdx.x; j <= nr; j += kBatchThreads) cp_async8(&sm.rp[b][j], a.rowptr + it.rb() + j);
-    }
-}
-
-template <int B>
-__device__ __forceinline__ void load_cols(const BatchArgs& a, const ItemInfo& it,
-                                          uint32_t (&cols)[StagedTile<B>::PER]) {
-    using T = StagedTile<B>;
-    const int cnt = it.cnt();
-    const uint32_t* colp = a.col + it.e0();
-#pragma unroll
-    for (int i = 0; i < T::PER; ++i) {
-        const int e = (i * kBatchThreads + static_cast<int>(threadIdx.x)) / T::L;
-        cols[i] = e < cnt ? ld_index(colp + e) : 0u;
-    }
-}
-
-template <int B>
-__device__ __forceinline__ void reduce_item(const BatchArgs& a, StagedTile<B>& sm, int b, const ItemInfo& it) {
-    using T = StagedTile<B>;
-    const int slot = threadIdx.x / T::L, cl = threadIdx.x % T::L;
-    const uint32_t rb = it.rb();
-    if (!it.hub()) {
-        const int nr = static_cast<int>(it.re() - rb);
-        const int64_t e0 = sm.rp[b][0];
-        // prefetch epilogue operands of this slot's rows, then sum staged rows
-        double2 wp[T::RPS], ac[T::RPS];
-#pragma unroll
-        for (int q = 0; q < T::RPS; ++q) {
-            const int r = q * T::SLOTS + slot;
-            if (r < nr) batch_prefetch<B>(a, rb + r, cl, wp[q], ac[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < T::RPS; ++q) {
-            const int r = q * T::SLOTS + slot;
-            if (r < nr) {
-                const int b0 = static_cast<int>(sm.rp[b][r] - e0), b1 = static_cast<int>(sm.rp[b][r + 1] - e0);
-                double2 s = {0.0, 0.0};
-                for (int e = b0; e < b1; ++e) {
-                    const double2 v = sm.buf[b][e][cl];
-                    s.x += v.x;
-                    s.y += v.y;
-                }
-                batch_epilogue<B>(a, rb + r, s, b1 - b0, cl, wp[q], ac[q]);
-            }
-        }
-        return;
-    }
-    // hub piece: slot s sums edges s, s+SLOTS, ...; slots combined in order.
-    double2 s = {0.0, 0.0};
-    const int cnt = it.cnt();
-    for (int e = slot; e < cnt; e += T::SLOTS) {
-        const double2 v = sm.buf[b][e][cl];
-        s.x += v.x;
-        s.y += v.y;
-    }
-    sm.red[slot][cl] = s;
-    __syncthreads();
-    if (slot == 0) {
-        double2 t = {0.0, 0.0};
-        for (int q = 0; q < T::SLOTS; ++q) {
-            t.x += sm.red[q][cl].x;
-            t.y += sm.red[q][cl].y;
-        }
-        const int64_t rs = a.rowptr[rb];
-        const int64_t d = a.rowptr[rb + 1] - rs;
-        const uint32_t P = static_cast<uint32_t>((d + T::E - 1) / T::E);
-        const uint32_t piece = static_cast<uint32_t>((it.e0() - rs) / T::E);
-        if (P == 1) {
-            double2 wp, ac;
-            batch_prefetch<B>(a, rb, cl, wp, ac);
-            batch_epilogue<B>(a, rb, t, d, cl, wp, ac);
-        } else {
-            reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(it.slot() + piece) * B)[cl] = t;
-            __threadfence();
-            if (T::L < 32) __syncwarp((1u << T::L) - 1u);
-            else __syncwarp();
-            if (cl == 0) {
-                const unsigned prev = atomicAdd(&a.hub_count[rb], 1u);
-                sm.flag = prev == P - 1;
-            }
-            if (T::L < 32) __syncwarp((1u << T::L) - 1u);
-            else __syncwarp();
-            if (sm.flag) {
-                __threadfence();
-                double2 y = {0.0, 0.0};
-                for (uint32_t p = 0; p < P; ++p) {
-                    const double2 v = __ldcg(
-                        reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(it.slot() + p) * B) + cl);
-                    y.x += v.x;
-                    y.y += v.y;
-                }
-                if (cl == 0) a.hub_count[rb] = 0u;
-                double2 wp, ac;
-                batch_prefetch<B>(a, rb, cl, wp, ac);
-                batch_epilogue<B>(a, rb, y, d, cl, wp, ac);
-            }
-        }
-    }
-}
-
-template <int B>
-__global__ void __launch_bounds__(kBatchThreads, 3) cheby_batch_staged_kernel(const BatchArgs a) {
-    using T = StagedTile<B>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T& sm = *reinterpret_cast<T*>(smem_raw);
-    uint32_t i = blockIdx.x;
-    if (i >= a.n_items) return;
-    // software pipeline: item i reduced while the rows of i+G are in flight
-    // (cp.async) and the column ids of i+2G are being loaded (registers).
-    uint32_t cols[T::PER];
-    ItemInfo cur = decode_item<B>(a, i);
-    load_cols<B>(a, cur, cols);
-    stage_item<B>(a, sm, 0, cur, cols);
-    cp_async_commit();
-    ItemInfo nxt{0u, 0u, 0ull};
-    if (i + gridDim.x < a.n_items) {
-        nxt = decode_item<B>(a, i + gridDim.x);
-        load_cols<B>(a, nxt, cols);
-    }
-    int b = 0;
-    for (; i < a.n_items; i += gridDim.x) {
-        const bool has_next = i + gridDim.x < a.n_items;
-        if (has_next) stage_item<B>(a, sm, b ^ 1, nxt, cols);
-        cp_async_commit();
-        ItemInfo nn{0u, 0u, 0ull};
-        const uint32_t i2 = i + 2 * gridDim.x;
-        if (i2 < a.n_items) {
-            nn = decode_item<B>(a, i2);
-            load_cols<B>(a, nn, cols);
-        }
-        cp_async_wait<1>();  // the copies of item i have landed
-        __syncthreads();
-        reduce_item<B>(a, sm, b, cur);
-        __syncthreads();  // buffer b is free again
-        cur = nxt;
-        nxt = nn;
-        b ^= 1;
-    }
-    cp_async_wait<0>();
-}
-
-template <int B>
-size_t staged_smem() {
-    return sizeof(StagedTile<B>);
-}
-
-// ---------------------------------------------------------------------------
-// Streaming batched step (the default batched path).  The chunk's edges are
-// split into n_slots equal contiguous ranges; a slot of L = B/2 lanes walks its
-// range as one stream of stages: per row it owns entirely, two operand stages
-// (the row of w_{k-1} and of acc) then one stage per edge (the gathered
-// B*8-byte row of w_k); rows cut by a slot boundary are summed per segment and
-// combined by the ordered last-arriver reduction.  Every stage is one 16-B
-// cp.async per lane into a per-warp ring of kStreamStages stages, so up to
-// 16 x 512 B per warp are in flight without holding registers; no CTA
-// barriers.  The consumer (kStreamStages-1 stages behind the producer)
-// accumulates in edge order, so results are bit-reproducible.
-// ---------------------------------------------------------------------------
-enum : uint32_t { kEvNone = 0, kEvOpW = 1, kEvOpAcc = 2, kEvEdge = 3, kEvEndFull = 4, kEvEndPart = 5 };
-
-template <int B>
-struct StreamCfg {
-    static constexpr int L = B / 2;     // lanes per slot
-    static constexpr int RPW = 32 / L;  // slots per warp
-    static constexpr int S = kStreamStages;
-};
-
-template <int B>
-size_t stream_smem_bytes() {
-    return static_cast<size_t>(kStreamWarps) * kStreamStages * 32 * (sizeof(double2) + sizeof(uint2));
-}
-
-__device__ __forceinline__ uint32_t slot_of_edge(const int64_t* slot_edge, uint32_t n_slots, int64_t e) {
-    uint32_t lo = 0, hi = n_slots;  // last s with slot_edge[s] <= e
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (slot_edge[mid] <= e) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-template <int V>
-__device__ __forceinline__ uint32_t pick(const uint32_t (&w)[V], int v) {
-    uint32_t r = w[0];
-#pragma unroll
-    for (int i = 1; i < V; ++i) r = v == i ? w[i] : r;
-    return r;
-}
-template <int V>
-__device__ __forceinline__ int64_t pick(const int64_t (&w)[V], int v) {
-    int64_t r = w[0];
-#pragma unroll
-    for (int i = 1; i < V; ++i) r = v == i ? w[i] : r;
-    return r;
-}
-
-template <int B>
-__global__ void __launch_bounds__(kStreamWarps * 32, 2) cheby_batch_stream_kernel(const BatchArgs a) {
-    using C = StreamCfg<B>;
-    constexpr int W = 32;          // index / row-end window per slot
-    constexpr int V = W / C::L;    // window entries per lane
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sl = lane / C::L, cl = lane % C::L;
-    const int lane0 = sl * C::L;   // first lane of this slot
-    double2* ring = reinterpret_cast<double2*>(smem_raw) + static_cast<size_t>(warp) * C::S * 32;
-    uint2* desc = reinterpret_cast<uint2*>(smem_raw + static_cast<size_t>(kStreamWarps) * C::S * 32 * sizeof(double2)) +
-                  static_cast<size_t>(warp) * C::S * 32;
-    const uint32_t slot = (blockIdx.x * kStreamWarps + warp) * C::RPW + sl;
-    const bool live = slot < a.n_slots;
-    const unsigned smask = C::L == 32 ? 0xffffffffu : (((1u << C::L) - 1u) << lane0);
-
-    // ---- producer state (replicated across the slot's lanes) ----
-    int64_t p_e = 0, p_end = 0, p_rs = 0, p_re = 0, s_begin = 0;
-    uint32_t p_row = 0;
-    int p_phase = 2;  // 0: operand w, 1: operand acc, 2: edges
-    bool p_full = false;
-    if (live) {
-        s_begin = a.slot_edge[slot];
-        p_end = a.slot_edge[slot + 1];
-        p_e = s_begin;
-        p_row = a.slot_row[slot];
-    }
-    // windows: column ids of edges [cb, cb+W) and row ends rowptr[rb+1 .. rb+W]
-    int64_t cb = p_e, rb = p_row;
-    uint32_t cw[V], cn[V];
-    int64_t rw[V], rn[V];
-    const uint32_t row_lim = a.n_loc;  // rows of this chunk end here (rowptr has row_lim+1 valid entries)
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-        const int64_t e = cb + v * C::L + cl, e2 = e + W;
-        cw[v] = live && e < p_end ? ld_index(a.col + e) : 0u;
-        cn[v] = live && e2 < p_end ? ld_index(a.col + e2) : 0u;
-        const int64_t r = rb + 1 + v * C::L + cl, r2 = r + W;
-        rw[v] = live && r <= row_lim ? a.rowptr[r] : 0;
-        rn[v] = live && r2 <= row_lim ? a.rowptr[r2] : 0;
-    }
-    if (live) {
-        p_rs = a.rowptr[p_row];
-        p_re = __shfl_sync(smask, rw[0], lane0);  // rowptr[p_row + 1]
-        p_full = p_rs >= s_begin && p_re <= p_end;
-        p_phase = p_full ? 0 : 2;
-    }
-
-    // ---- consumer state ----
-    double2 c_sum = {0.0, 0.0}, c_wp = {0.0, 0.0}, c_ac = {0.0, 0.0};
-
-    auto produce = [&](int stage) {
-        // window lookups (all lanes, converged): current edge's column and the next row's end
-        const int ie = static_cast<int>(p_e - cb);
-        const uint32_t u = __shfl_sync(0xffffffffu, pick<V>(cw, ie / C::L), lane0 + ie % C::L);
-        const int ir = static_cast<int>(p_row + 1 - rb);  // window slot of rowptr[p_row + 2]
-        const int64_t next_re = __shfl_sync(0xffffffffu, pick<V>(rw, ir / C::L), lane0 + ir % C::L);
-        uint2 d = make_uint2(0u, kEvNone << 29);
-        if (p_e < p_end) {
-            const uint32_t gr = a.row0 + p_row;
-            const uint32_t deg = static_cast<uint32_t>(p_re - p_rs);
-            if (p_phase == 0) {
-                const double* src = (a.first ? a.w_cur : a.w_io) + static_cast<size_t>(gr) * B + 2 * cl;
-                cp_async16(&ring[stage * 32 + lane], src);
-                d = make_uint2(p_row, (kEvOpW << 29) | deg);
-                p_phase = 1;
-            } else if (p_phase == 1) {
-                if (!a.first) cp_async16(&ring[stage * 32 + lane], a.acc + static_cast<size_t>(p_row) * B + 2 * cl);
-                d = make_uint2(p_row, (kEvOpAcc << 29) | deg);
-                p_phase = 2;
-            } else {
-                cp_async16(&ring[stage * 32 + lane], a.w_cur + static_cast<size_t>(u) * B + 2 * cl);
-                const bool row_done = p_e + 1 == p_re, slot_done = p_e + 1 == p_end;
-                uint32_t ev = kEvEdge;
-                if (row_done && p_full) ev = kEvEndFull;
-                else if (row_done || slot_done) ev = kEvEndPart;
-                d = make_uint2(p_row, (ev << 29) | deg);
-                ++p_e;
-                if (p_e - cb == W) {  // slide the column window
-                    cb += W;
-#pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        cw[v] = cn[v];
-                        const int64_t e2 = cb + W + v * C::L + cl;
-                        cn[v] = e2 < p_end ? ld_index(a.col + e2) : 0u;
-                    }
-                }
-                if (row_done && p_e < p_end) {  // advance to the next row
-                    ++p_row;
-                    p_rs = p_re;
-                    p_re = next_re;
-                    p_full = p_re <= p_end;
-                    p_phase = p_full ? 0 : 2;
-                    if (p_row + 1 - rb == W) {  // slide the row-end window
-                        rb += W;
-#pragma unroll
-                        for (int v = 0; v < V; ++v) {
-                            rw[v] = rn[v];
-                            const int64_t r2 = rb + 1 + W + v * C::L + cl;
-                            rn[v] = r2 <= row_lim ? a.rowptr[r2] : 0;
-                        }
-                    }
-                }
-            }
-        }
-        desc[stage * 32 + lane] = d;
-    };
-
-    auto consume = [&](int stage) {
-        const uint2 d = desc[stage * 32 + lane];
-        const uint32_t ev = d.y >> 29;
-        if (ev == kEvNone) return;
-        const double2 v = ring[stage * 32 + lane];
-        if (ev == kEvOpW) {
-            c_wp = v;
-            return;
-        }
-        if (ev == kEvOpAcc) {
-            c_ac = a.first ? make_double2(0.0, 0.0) : v;
-            return;
-        }
-        c_sum.x += v.x;
-        c_sum.y += v.y;
-        if (ev == kEvEdge) return;
-        const uint32_t row = d.x;
-        const int64_t deg = d.y & ((1u << 28) - 1);
-        if (ev == kEvEndFull) {
-            batch_epilogue<B>(a, row, c_sum, deg, cl, c_wp, c_ac);
-        } else {  // segment of a row shared with neighbouring slots
-            const int64_t rs = a.rowptr[row], re = rs + deg;
-            const int64_t seg0 = rs > s_begin ? rs : s_begin;
-            const int64_t seg1 = re < p_end ? re : p_end;
-            const uint32_t pidx = seg0 == s_begin ? 0u : 1u;
-            reinterpret_cast<double2*>(a.hub_partial + (static_cast<size_t>(slot) * 2 + pidx) * B)[cl] = c_sum;
-            __threadfence();
-            __syncwarp(smask);
-            unsigned prev = 0;
-            const unsigned seg_len = static_cast<unsigned>(seg1 - seg0);
-            if (cl == 0) prev = atomicAdd(&a.hub_count[row], seg_len);
-            prev = __shfl_sync(smask, prev, lane0);
-            if (prev + seg_len == static_cast<unsigned>(deg)) {  // last segment: ordered combine
-                __threadfence();
-                const uint32_t s0 = slot_of_edge(a.slot_edge, a.n_slots, rs);
-                const uint32_t s1 = slot_of_edge(a.slot_edge, a.n_slots, re - 1);
-                double2 y = {0.0, 0.0};
-                for (uint32_t q = s0; q <= s1; ++q) {
-                    const int64_t qb = a.slot_edge[q];
-                    if (a.slot_edge[q + 1] == qb) continue;  // empty slot
-                    const uint32_t qi = (rs > qb ? rs : qb) == qb ? 0u : 1u;
-                    const double2 t = __ldcg(reinterpret_cast<const double2*>(
-                                                 a.hub_partial + (static_cast<size_t>(q) * 2 + qi) * B) + cl);
-                    y.x += t.x;
-                    y.y += t.y;
-                }
-                if (cl == 0) a.hub_count[row] = 0u;
-                double2 wp, ac;
-                batch_prefetch<B>(a, row, cl, wp, ac);
-                batch_epilogue<B>(a, row, y, deg, cl, wp, ac);
-            }
-        }
-        c_sum = make_double2(0.0, 0.0);
-    };
-
-#pragma unroll 1
-    for (int st = 0; st < C::S - 1; ++st) {
-        produce(st);
-        cp_async_commit();
-    }
-    int stage_p = C::S - 1, stage_c = 0;
-#pragma unroll 1
-    while (true) {
-        produce(stage_p);
-        cp_async_commit();
-        cp_async_wait<C::S - 1>();  // this lane's copies of stage_c have landed
-        consume(stage_c);
-        stage_p = stage_p + 1 == C::S ? 0 : stage_p + 1;
-        stage_c = stage_c + 1 == C::S ? 0 : stage_c + 1;
-        if (!__any_sync(0xffffffffu, p_e < p_end)) {  // drain the S-1 stages in flight
-            cp_async_wait<0>();
-#pragma unroll 1
-            for (int st = 0; st < C::S - 1; ++st) {
-                consume(stage_c);
-                stage_c = stage_c + 1 == C::S ? 0 : stage_c + 1;
-            }
-            break;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Bulk-copy (TMA) batched step, B in {4, 8, 16, 32}.  Each warp owns an
-// edge-balanced contiguous edge range.  Per stage of 32 edges every lane issues
-// ONE cp.async.bulk (the TMA engine) copying the gathered B*8-byte row of
-// w_k for its edge into a per-warp shared-memory ring; completion is tracked
-// by an mbarrier per stage (expect_tx), so in-flight bytes cost neither
-// registers nor LSU issue slots.  B lanes then walk the staged edges in order
-// (segmented by row, bit-reproducible), finished rows are queued in shared
-// memory and their fused epilogues run 32 rows at a time so the operand loads
-// overlap.  Rows cut by a warp boundary use the ordered last-arriver combine.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-template <int B>
-struct BulkCfg {
-    static constexpr int WARPS = 8;
-    static constexpr int STAGE_BYTES = 32 * B * 8;
-    static constexpr int S0 = (20 * 1024) / STAGE_BYTES;
-    static constexpr int S = S0 < 2 ? 2 : (S0 > 8 ? 8 : S0);  // ring stages per warp
-    static constexpr int FR = 32;                              // queued finished rows
-    static constexpr int RAW_BYTES = S * STAGE_BYTES + FR * B * 8 + FR * 16 + S * 8;
-    static constexpr int WARP_BYTES = (RAW_BYTES + 127) / 128 * 128;  // 16-B bulk-copy alignment per warp
-};
-
-template <int B>
-size_t bulk_smem_bytes() {
-    return static_cast<size_t>(BulkCfg<B>::WARPS) * BulkCfg<B>::WARP_BYTES;
-}
-
-template <int B>
-__device__ __forceinline__ void bulk_flush(const BatchArgs& a, const double* fin, const uint2* fin_meta, int nf,
-                                           int lane) {
-    // nf finished rows x B columns: each lane takes (row, column pair) items.
-    constexpr int PAIRS = B / 2;
-    for (int it = lane; it < nf * PAIRS; it += 32) {
-        const int q = it / PAIRS, cl = it % PAIRS;
-        const uint32_t row = fin_meta[q].x;
-        const int64_t deg = fin_meta[q].y;
-        double2 wp, ac;
-        batch_prefetch<B>(a, row, cl, wp, ac);
-        const double2 y = reinterpret_cast<const double2*>(fin + static_cast<size_t>(q) * B)[cl];
-        batch_epilogue<B>(a, row, y, deg, cl, wp, ac);
-    }
-}
-
-template <int B>
-__global__ void __launch_bounds__(BulkCfg<B>::WARPS * 32, 1) cheby_batch_bulk_kernel(const BatchArgs a) {
-    using C = BulkCfg<B>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* base = smem_raw + static_cast<size_t>(warp) * C::WARP_BYTES;
-    double* ring = reinterpret_cast<double*>(base);                              // [S][32][B]
-    double* fin = reinterpret_cast<double*>(base + C::S * C::STAGE_BYTES);       // [FR][B]
-    uint2* fin_meta = reinterpret_cast<uint2*>(base + C::S * C::STAGE_BYTES + C::FR * B * 8);  // [FR]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::S * C::STAGE_BYTES + C::FR * B * 8 + C::FR * 16);
-
-    const uint32_t w = blockIdx.x * C::WARPS + warp;
-    if (w >= a.n_slots) return;
-    const int64_t e_begin = a.slot_edge[w], e_end = a.slot_edge[w + 1];
-    if (e_begin >= e_end) return;
-
-    if (lane == 0)
-        for (int st = 0; st < C::S; ++st) mbar_init(&bar[st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-
-    // producer: stage t covers edges [e_begin + 32t, +32)
-    const int64_t n_edges = e_end - e_begin;
-    const int64_t n_stages = (n_edges + 31) / 32;
-    uint32_t col_next = lane < n_edges ? ld_index(a.col + e_begin + lane) : 0u;
-    auto issue = [&](int64_t t) {
-        const int st = static_cast<int>(t % C::S);
-        const int64_t e0 = e_begin + 32 * t;
-        const int nvalid = static_cast<int>(e_end - e0 < 32 ? e_end - e0 : 32);
-        const uint32_t u = col_next;
-        // prefetch the next stage's column ids
-        const int64_t en = e0 + 32 + lane;
-        col_next = en < e_end ? ld_index(a.col + en) : 0u;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was read by generic loads
-        if (lane == 0) mbar_arrive_expect_tx(&bar[st], static_cast<uint32_t>(nvalid) * B * 8);
-        __syncwarp();
-        if (lane < nvalid)
-            bulk_g2s(ring + (static_cast<size_t>(st) * 32 + lane) * B, a.w_cur + static_cast<size_t>(u) * B, B * 8,
-                     &bar[st]);
-    };
-
-    // consumer state (uniform across the warp; lanes < B hold one column each)
-    uint32_t row = a.slot_row[w];
-    int64_t row_rs = a.rowptr[row], row_re = a.rowptr[row + 1];
-    double sum = 0.0;
-    int nf = 0;
-
-    int64_t t_issue = 0;
-    for (; t_issue < n_stages && t_issue < C::S; ++t_issue) issue(t_issue);
-
-    for (int64_t t = 0; t < n_stages; ++t) {
-        const int st = static_cast<int>(t % C::S);
-        mbar_wait(&bar[st], static_cast<uint32_t>((t / C::S) & 1));
-        const int64_t e0 = e_begin + 32 * t;
-        const int nvalid = static_cast<int>(e_end - e0 < 32 ? e_end - e0 : 32);
-        const double* stage = ring + static_cast<size_t>(st) * 32 * B;
-        for (int j = 0; j < nvalid; ++j) {
-            if (lane < B) sum += stage[j * B + lane];
-            const int64_t e = e0 + j + 1;
-            if (e == row_re || e == e_end) {  // row (or this warp's segment of it) ends here
-                const bool full = row_rs >= e_begin && row_re <= e_end;
-                const int64_t deg = row_re - row_rs;
-                if (full) {
-                    if (lane < B) fin[nf * B + lane] = sum;
-                    if (lane == 0) fin_meta[nf] = make_uint2(row, static_cast<uint32_t>(deg));
-                    ++nf;
-                    if (nf == C::FR) {
-                        __syncwarp();
-                        bulk_flush<B>(a, fin, fin_meta, nf, lane);
-                        __syncwarp();
-                        nf = 0;
-                    }
-                } else {
-                    const int64_t seg0 = row_rs > e_begin ? row_rs : e_begin;
-                    const int64_t seg1 = row_re < e_end ? row_re : e_end;
-                    const uint32_t pidx = seg0 == e_begin ? 0u : 1u;
-                    if (lane < B) a.hub_partial[(static_cast<size_t>(w) * 2 + pidx) * B + lane] = sum;
-                    __threadfence();
-                    __syncwarp();
-                    unsigned prev = 0;
-                    if (lane == 0) prev = atomicAdd(&a.hub_count[row], static_cast<unsigned>(seg1 - seg0));
-                    prev = __shfl_sync(0xffffffffu, prev, 0);
-                    if (prev + static_cast<unsigned>(seg1 - seg0) == static_cast<unsigned>(deg)) {
-                        __threadfence();
-                        const uint32_t s0 = slot_of_edge(a.slot_edge, a.n_slots, row_rs);
-                        const uint32_t s1 = slot_of_edge(a.slot_edge, a.n_slots, row_re - 1);
-                        double y = 0.0;
-                        for (uint32_t q = s0; q <= s1; ++q) {
-                            const int64_t qb = a.slot_edge[q];
-                            if (a.slot_edge[q + 1] == qb) continue;
-                            const uint32_t qi = (row_rs > qb ? row_rs : qb) == qb ? 0u : 1u;
-                            if (lane < B) y += __ldcg(a.hub_partial + (static_cast<size_t>(q) * 2 + qi) * B + lane);
-                        }
-                        if (lane == 0) a.hub_count[row] = 0u;
-                        if (lane < B) fin[nf * B + lane] = y;
-                        if (lane == 0) fin_meta[nf] = make_uint2(row, static_cast<uint32_t>(deg));
-                        ++nf;
-                        if (nf == C::FR) {
-                            __syncwarp();
-                            bulk_flush<B>(a, fin, fin_meta, nf, lane);
-                            __syncwarp();
-                            nf = 0;
-                        }
-                    }
-                }
-                sum = 0.0;
-                if (e < e_end) {  // next row (rows never have degree 0 inside an edge range)
-                    ++row;
-                    row_rs = row_re;
-                    row_re = a.rowptr[row + 1];
-                }
-            }
-        }
-        __syncwarp();  // every lane is done reading this stage
-        if (t_issue < n_stages) issue(t_issue++);
-    }
-    __syncwarp();
-    bulk_flush<B>(a, fin, fin_meta, nf, lane);
-}
-
-// ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
 
@@ -1176,145 +528,6 @@ int step_occupancy(int tile) {
                                                       kStepThreads, 0);
     return blocks;
 }
-template <int B>
-void launch_staged(const BatchArgs& a, int grid, cudaStream_t st) {
-    static bool configured = false;
-    const size_t bytes = staged_smem<B>();
-    if (!configured) {
-        cudaFuncSetAttribute(cheby_batch_staged_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bytes));
-        configured = true;
-    }
-    cheby_batch_staged_kernel<B><<<grid, kBatchThreads, bytes, st>>>(a);
-}
-
-template <int B>
-int staged_occupancy() {
-    const size_t bytes = staged_smem<B>();
-    cudaFuncSetAttribute(cheby_batch_staged_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(bytes));
-    int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_staged_kernel<B>, kBatchThreads, bytes);
-    return blocks;
-}
-
-template <int B>
-void launch_stream_t(const BatchArgs& a, int grid, cudaStream_t st) {
-    static bool configured = false;
-    const size_t bytes = stream_smem_bytes<B>();
-    if (!configured) {
-        cudaFuncSetAttribute(cheby_batch_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bytes));
-        configured = true;
-    }
-    cheby_batch_stream_kernel<B><<<grid, kStreamWarps * 32, bytes, st>>>(a);
-}
-
-template <int B>
-int stream_occupancy_t() {
-    const size_t bytes = stream_smem_bytes<B>();
-    cudaFuncSetAttribute(cheby_batch_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(bytes));
-    int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_stream_kernel<B>, kStreamWarps * 32, bytes);
-    return blocks;
-}
-
-// The register-pipelined slot kernel is the batched default (fastest measured,
-// profiles/r01); CPG_BATCH_KERNEL=stream selects the cp.async streaming kernel
-// (issue-bound: ~25 instructions per gathered row) for comparison.
-template <int B>
-void launch_bulk_t(const BatchArgs& a, int grid, cudaStream_t st) {
-    static bool configured = false;
-    const size_t bytes = bulk_smem_bytes<B>();
-    if (!configured) {
-        cudaFuncSetAttribute(cheby_batch_bulk_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bytes));
-        configured = true;
-    }
-    cheby_batch_bulk_kernel<B><<<grid, BulkCfg<B>::WARPS * 32, bytes, st>>>(a);
-}
-
-void launch_bulk(const BatchArgs& a, int B, int grid, cudaStream_t st) {
-    switch (B) {
-    case 4: launch_bulk_t<4>(a, grid, st); break;
-    case 8: launch_bulk_t<8>(a, grid, st); break;
-    case 16: launch_bulk_t<16>(a, grid, st); break;
-    default: launch_bulk_t<32>(a, grid, st); break;
-    }
-}
-
-int bulk_occupancy(int B) {
-    const size_t bytes = B == 4 ? bulk_smem_bytes<4>() : B == 8 ? bulk_smem_bytes<8>() : B == 16 ? bulk_smem_bytes<16>()
-                                                                                                   : bulk_smem_bytes<32>();
-    int blocks = 0;
-    switch (B) {
-    case 4:
-        cudaFuncSetAttribute(cheby_batch_bulk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<4>, 256, bytes);
-        break;
-    case 8:
-        cudaFuncSetAttribute(cheby_batch_bulk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<8>, 256, bytes);
-        break;
-    case 16:
-        cudaFuncSetAttribute(cheby_batch_bulk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<16>, 256, bytes);
-        break;
-    default:
-        cudaFuncSetAttribute(cheby_batch_bulk_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_bulk_kernel<32>, 256, bytes);
-        break;
-    }
-    return blocks;
-}
-
-// CPG_BATCH_KERNEL=bulk selects the TMA bulk-copy kernel for B <= 32.
-bool batch_uses_bulk(int B) {
-    static const bool on = [] {
-        const char* e = std::getenv("CPG_BATCH_KERNEL");
-        return e && std::string(e) == "bulk";
-    }();
-    return on && B <= 32;
-}
-
-bool batch_uses_stream() {
-    static const bool on = [] {
-        const char* e = std::getenv("CPG_BATCH_KERNEL");
-        return e && std::string(e) == "stream";
-    }();
-    return on;
-}
-
-void launch_stream(const BatchArgs& a, int B, int grid, cudaStream_t st) {
-    switch (B) {
-    case 4: launch_stream_t<4>(a, grid, st); break;
-    case 8: launch_stream_t<8>(a, grid, st); break;
-    case 16: launch_stream_t<16>(a, grid, st); break;
-    case 32: launch_stream_t<32>(a, grid, st); break;
-    default: launch_stream_t<64>(a, grid, st); break;
-    }
-}
-
-int stream_occupancy(int B) {
-    switch (B) {
-    case 4: return stream_occupancy_t<4>();
-    case 8: return stream_occupancy_t<8>();
-    case 16: return stream_occupancy_t<16>();
-    case 32: return stream_occupancy_t<32>();
-    default: return stream_occupancy_t<64>();
-    }
-}
-
-int batch_staged_occupancy(int B) {
-    switch (B) {
-    case 4: return staged_occupancy<4>();
-    case 8: return staged_occupancy<8>();
-    case 16: return staged_occupancy<16>();
-    default: return staged_occupancy<32>();
-    }
-}
-
 template <int B, int U, int MINB>
 void launch_slot(const BatchArgs& a, cudaStream_t st) {
     int occ = 0, sms = 0, dev = 0;
@@ -1347,14 +560,6 @@ bool launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
 }
 
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
-    if (batch_uses_tiles(B)) {
-        switch (B) {
-        case 4: launch_staged<4>(a, grid, st); return;
-        case 8: launch_staged<8>(a, grid, st); return;
-        case 16: launch_staged<16>(a, grid, st); return;
-        default: launch_staged<32>(a, grid, st); return;
-        }
-    }
     static const int cfg = [] {  // tuning hook: CPG_SLOT_CFG = U*10 + MINB
         const char* e = std::getenv("CPG_SLOT_CFG");
         return e ? std::atoi(e) : 0;
