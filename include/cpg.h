@@ -95,6 +95,10 @@ int cpg_ppr_cheby_coeffs(double alpha, uint64_t max_index, double* out);   /* ke
 int cpg_hkpr_cheby_coeffs(double t, uint64_t max_index, double* out);      /* kernels.cpp:172-194 */
 int cpg_cheby_coeffs(int family, double param, uint64_t max_index, double* out);
 int cpg_plan_truncation(int family, double param, double epsilon, cpg_plan* out); /* :253-341 */
+/* Taylor (power-basis) coefficients zeta_0..zeta_max (kernels.cpp:78-96). */
+int cpg_taylor_coeffs(int family, double param, uint64_t max_index, double* out);
+/* Ground-truth truncation N (eval.cpp:39-50): ceil(ln 1e20 / alpha), ceil(2 t ln 1e20). */
+uint64_t cpg_ground_truth_steps(int family, double param);
 /* "ppr:alpha=0.2" / "hkpr:t=5" (kernels.cpp:343-362) */
 int cpg_parse_kernel_spec(const char* spec, int* family, double* param);
 
@@ -172,6 +176,12 @@ int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K
  * solvers.cpp:215,219,226.  Either trace pointer may be NULL. */
 int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source,
                          double* out, double* r_trace, double* est_trace);
+
+/* PwMethod (solvers.cpp:87-121), the reference's ground-truth engine
+ * (eval.cpp:52-59): out = sum_{k<n_steps} zeta_k P^k e_s, n_steps - 1 fused
+ * SpMV steps per source (same kernels, Taylor epilogue). */
+int cpg_power_method(cpg_graph* g, const double* zeta, uint32_t n_steps, const uint32_t* sources,
+                     uint32_t n_sources, double* out, cpg_stats* stats);
 
 /* Single walk y = A D^-1 x (graph.cpp:257-267) for tests; host vectors. */
 int cpg_apply_walk(cpg_graph* g, const double* x, double* y);

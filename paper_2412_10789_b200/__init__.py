@@ -41,7 +41,8 @@ __all__ = [
     "ParameterError", "StructuralError", "DeviceError", "Graph", "DeviceGraph", "Kernel", "KernelFamily",
     "TruncationPlan", "SolveStats", "Estimate", "ppr_cheby_coeffs", "hkpr_cheby_coeffs", "plan_truncation",
     "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
-    "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR",
+    "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
+    "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan",
 ]
 
 
@@ -145,6 +146,12 @@ class Kernel:
     def cheby_coeffs(self, max_index: int) -> np.ndarray:
         out = np.empty(max_index + 1)
         _check(L.lib().cpg_cheby_coeffs(self._family, self._param, int(max_index), _f64p(out)))
+        return out
+
+    def taylor_coeffs(self, max_index: int) -> np.ndarray:
+        """zeta_0 .. zeta_max_index (kernels.cpp:78-96)."""
+        out = np.empty(max_index + 1)
+        _check(L.lib().cpg_taylor_coeffs(self._family, self._param, int(max_index), _f64p(out)))
         return out
 
     def descriptor(self) -> str:  # kernels.cpp:132-137
@@ -418,6 +425,37 @@ def cheby_power_many(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int
     else:
         _check(L.lib().cpg_chebypower(dg.handle, _f64p(c), K, _u32p(src), len(src), ptr, ctypes.byref(s)))
     return out, _to_stats(s, K)
+
+
+def power_method(g, kernel: Kernel, source: int, n_steps: int, device: int = 0) -> Estimate:
+    """PwMethod (solvers.cpp:87-121) on the GPU: sum_{k<N} zeta_k P^k e_source."""
+    t0 = time.perf_counter()
+    N = int(n_steps)
+    if N < 1:
+        raise ParameterError("power_method: n_steps must be >= 1")
+    dg = _dev(g, device)
+    if source < 0 or source >= dg.n:
+        raise ParameterError(f"source node {source} out of range")
+    zeta = kernel.taylor_coeffs(N - 1)
+    out = np.empty(dg.n)
+    s = cpg_stats()
+    src = np.array([source], dtype=np.uint32)
+    _check(L.lib().cpg_power_method(dg.handle, _f64p(zeta), N, _u32p(src), 1, out.ctypes.data, ctypes.byref(s)))
+    st = _to_stats(s, N)
+    st.iterations, st.algorithm, st.params = N, "pw", f"N={N}"
+    st.push_work = (N - 1) * int(dg.info.nnz)
+    st.wall_seconds = time.perf_counter() - t0
+    return Estimate(out, st)
+
+
+def ground_truth_steps(kernel: Kernel) -> int:
+    """eval.cpp:39-50."""
+    return int(L.lib().cpg_ground_truth_steps(kernel.family(), kernel.param))
+
+
+def ground_truth(g, kernel: Kernel, source: int, device: int = 0) -> np.ndarray:
+    """eval.cpp:52-59: PwMethod far past convergence, on the GPU."""
+    return power_method(g, kernel, source, ground_truth_steps(kernel), device=device).values
 
 
 def apply_walk(g, x, device: int = 0) -> np.ndarray:

@@ -48,6 +48,9 @@ SIGNATURES = {
     "cpg_cheby_coeffs": (c_int, [c_int, c_double, c_uint64, _f64p]),
     "cpg_plan_truncation": (c_int, [c_int, c_double, c_double, POINTER(cpg_plan)]),
     "cpg_parse_kernel_spec": (c_int, [c_char_p, POINTER(c_int), POINTER(c_double)]),
+    "cpg_taylor_coeffs": (c_int, [c_int, c_double, c_uint64, _f64p]),
+    "cpg_ground_truth_steps": (c_uint64, [c_int, c_double]),
+    "cpg_power_method": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_void_p, POINTER(cpg_stats)]),
     "cpg_validate_csr": (c_int, [_u64p, _u32p, c_uint64, c_uint64, _u64p]),
     "cpg_graph_create": (c_int, [_u64p, _u32p, c_uint32, c_uint64, c_int, c_int, POINTER(_G)]),
     "cpg_graph_create_device": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, POINTER(_G)]),

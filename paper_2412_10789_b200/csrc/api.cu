@@ -220,7 +220,7 @@ const double* gather_result(cpg_graph* g, size_t cols, cudaStream_t st) {
 
 // The K fused steps of one query, chunk by chunk (last = write d*acc).
 uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
-                   cudaStream_t st, StepProf* prof) {
+                   cudaStream_t st, StepProf* prof, bool taylor = false) {
     uint32_t launches = 0;
     const int occ = std::max(1, step_occupancy(g->tile));
     const uint32_t C = static_cast<uint32_t>(g->chunks);
@@ -238,6 +238,7 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
         a.tile = g->tile;
         a.k = static_cast<int>(k);
         a.first = k == 1;
+        a.taylor = taylor;
         a.last = last_writes_out && k == K;
         if (k > 1) wait_gathers(g, st);
         for (uint32_t c = 0; c < C; ++c) {
@@ -263,7 +264,7 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
 // One single-source (or dense-seed, when seed_dev != null) query; result
 // d*acc unpermuted into d_dst[n] (caller ids) if non-null.
 uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
-                    cudaStream_t st, StepProf* prof) {
+                    cudaStream_t st, StepProf* prof, bool taylor = false) {
     uint32_t launches = 0;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
@@ -273,7 +274,7 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
     else
         launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
     ++launches;
-    launches += run_steps(g, 1, K, K, true, st, prof);
+    launches += run_steps(g, 1, K, K, true, st, prof, taylor);
     launch_mass_steps(g->d_mass_partial, C * g->step_grid, K, g->d_step_mass, st);
     ++launches;
     if (g->nccl_comm) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
@@ -426,8 +427,8 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
                 dst = g->d_stage + (b & 1) * slot;
                 CPG_CUDA(cudaStreamWaitEvent(st, g->ev[b & 1], 0));  // slot free (copy of b-2 done)
             }
-            if (mode == 0) {
-                launches += run_single(g, K, q0, nullptr, 1.0, dst, st, prof.get());
+            if (mode == 0 || mode == 3) {
+                launches += run_single(g, K, q0, nullptr, 1.0, dst, st, prof.get(), mode == 3);
             } else if (mode == 1) {
                 const double* sh = seeds_host + static_cast<size_t>(q0) * n;
                 double mass0 = 0.0;
@@ -635,6 +636,24 @@ int cpg_chebypower_batched(cpg_graph* g, const double* coeffs, uint32_t K, const
 int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
                                   uint32_t n_sources, uint32_t tile, double* d_out, void* stream, cpg_stats* stats) {
     return drive(g, coeffs, K, sources, nullptr, n_sources, tile, 2, d_out, true, stream, stats);
+}
+
+// PwMethod (solvers.cpp:87-121): yhat = sum_{k<N} zeta_k P^k e_s with N-1
+// fused SpMV steps; N = 1 is zeta_0 e_s.
+int cpg_power_method(cpg_graph* g, const double* zeta, uint32_t n_steps, const uint32_t* sources,
+                     uint32_t n_sources, double* out, cpg_stats* stats) {
+    if (n_steps >= 2) return drive(g, zeta, n_steps - 1, sources, nullptr, n_sources, 1, 3, out, false, nullptr, stats);
+    return guarded([&] {
+        require(n_steps >= 1, "power_method: n_steps must be >= 1");  // solvers.cpp:91
+        check_query(g, zeta, 1, sources, n_sources);
+        if (!out) return;
+        for (uint32_t q = 0; q < n_sources; ++q) {
+            double* o = out + static_cast<size_t>(q) * g->n;
+            std::fill(o, o + g->n, 0.0);
+            o[sources[q]] = zeta[0];
+        }
+        if (stats) *stats = cpg_stats{1, 0, 0.0, 0.0, 0.0, 0.0, 0, 0.0, 0};
+    });
 }
 
 int cpg_apply_walk(cpg_graph* g, const double* x, double* y) {

@@ -71,6 +71,7 @@ struct StepArgs {
     int tile;              // kTileSmall or kTileLarge (must match the table)
     int k;                 // computing w_k (1..K)
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
+    int taylor;            // power method (PwMethod, solvers.cpp:87-116): w_k = D^-1 A w_{k-1}
     int last;              // write out = d * acc instead of acc
 };
 

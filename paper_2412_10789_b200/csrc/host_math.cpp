@@ -216,6 +216,36 @@ int cpg_cheby_coeffs(int family, double param, uint64_t max_index, double* out) 
     return CPG_EINVAL;
 }
 
+// zeta_k: alpha (1-alpha)^k (PPR) or e^-t t^k / k! (HKPR), kernels.cpp:78-96.
+int cpg_taylor_coeffs(int family, double param, uint64_t max_index, double* out) {
+    return guarded([&] {
+        require(out != nullptr, "null output");
+        if (family == CPG_PPR) {
+            check_alpha(param);
+            double z = param;
+            for (uint64_t k = 0; k <= max_index; ++k) {
+                out[k] = z;
+                z *= 1.0 - param;
+            }
+        } else {
+            require(family == CPG_HKPR, "unknown kernel family");
+            check_t(param);
+            double z = std::exp(-param);
+            for (uint64_t k = 0; k <= max_index; ++k) {
+                out[k] = z;
+                z *= param / static_cast<double>(k + 1);
+            }
+        }
+    });
+}
+
+// N = ceil(ln(1e20)/alpha) (PPR) or ceil(2 t ln(1e20)) (HKPR), eval.cpp:39-50.
+uint64_t cpg_ground_truth_steps(int family, double param) {
+    const double target = std::log(1e20);
+    if (family == CPG_PPR) return static_cast<uint64_t>(std::ceil(target / param));
+    return static_cast<uint64_t>(std::ceil(2.0 * param * target));
+}
+
 int cpg_plan_truncation(int family, double param, double epsilon, cpg_plan* out) {
     return guarded([&] {
         require(out != nullptr, "null output");

@@ -109,6 +109,9 @@ __device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, dou
         if (a.first) {
             w_new = y / dd;  // w_1 = D^-1 A w_0   (T_1 = P T_0, solvers.cpp:212)
             acc_new = a.coeffs[0] * w_prev + a.coeffs[1] * w_new;
+        } else if (a.taylor) {
+            w_new = y / dd;  // r_{k} = P r_{k-1} (solvers.cpp:105-106)
+            acc_new = acc_old + a.coeffs[a.k] * w_new;  // solvers.cpp:102
         } else {
             w_new = 2.0 * y / dd - w_prev;  // solvers.cpp:221
             acc_new = acc_old + a.coeffs[a.k] * w_new;  // solvers.cpp:218 (for k+1)

@@ -268,3 +268,38 @@ def test_large_graph_default_tiles(cpg, gpu):
         want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
         assert_parity(got[j], want)
     assert st.mass_err_max <= 1e-9
+
+
+@pytest.mark.parametrize("family,param", [(PPR, 0.2), (HKPR, 5.0)])
+def test_ground_truth_power_method_matches_reference(graphs, cpg, family, param):
+    """GPU PwMethod with the reference's ground-truth N (eval.cpp:39-59) vs the reference."""
+    kern = cpg.Kernel.ppr(param) if family == PPR else cpg.Kernel.hkpr(param)
+    assert cpg.ground_truth_steps(kern) == (231 if family == PPR else 461)
+    for name in ("ring_chord_1000", "chunglu", "rmat12"):
+        off, nb = graphs[name]
+        g = cpg.Graph.from_csr(off, nb)
+        ref = _ref_graph(off, nb)
+        for s in (0, g.node_count() // 3):
+            assert_parity(cpg.ground_truth(g, kern, s), ref.ground_truth(family, param, s))
+
+
+def test_power_method_small_n(graphs, cpg):
+    """test_solvers.cpp:29-35 (N = 1 is zeta_0 e_s) and the Taylor tail bound (:42-51)."""
+    from oracle import Port
+
+    off, nb = Port.make_graph(12, 10, 5)
+    g = cpg.Graph.from_csr(off, nb)
+    est = cpg.power_method(g, cpg.Kernel.ppr(0.3), 4, 1)
+    assert est.values[4] == 0.3 and np.count_nonzero(est.values) == 1 and est.stats.iterations == 1
+    off, nb = Port.make_graph(40, 60, 9)
+    g = cpg.Graph.from_csr(off, nb)
+    P = np.zeros((g.node_count(), g.node_count()))
+    for u in range(g.node_count()):
+        for v in nb[off[u]:off[u + 1]]:
+            P[v, u] = 1.0 / (off[u + 1] - off[u])
+    exact = np.linalg.solve(np.eye(g.node_count()) - 0.8 * P, 0.2 * np.eye(g.node_count())[3])
+    for n_steps in (5, 10, 25):
+        est = cpg.power_method(g, cpg.Kernel.ppr(0.2), 3, n_steps)
+        assert np.abs(est.values - exact).sum() <= 0.8 ** n_steps * (1 + 1e-12)
+        want = Port.power_method(off, nb, Port.taylor_coeffs(PPR, 0.2, n_steps - 1), n_steps, 3)
+        assert np.abs(est.values - want).max() <= 1e-12

@@ -41,6 +41,13 @@ def test_coefficients_and_plans_match_golden(cpg):
 
 
 @needs_ref
+def test_taylor_coefficients_and_truth_steps_vs_reference(cpg):
+    for fam, p in ((PPR, 0.2), (PPR, 0.02), (HKPR, 5.0), (HKPR, 40.0)):
+        assert np.array_equal(cpg.Kernel(fam, p).taylor_coeffs(300), Ref.taylor_coeffs(fam, p, 300))
+        assert cpg.ground_truth_steps(cpg.Kernel(fam, p)) == Ref.ground_truth_steps(fam, p)
+
+
+@needs_ref
 def test_coefficients_bit_exact_vs_reference(cpg):
     for a in (0.2, 0.1, 0.02, 0.5, 0.999):
         assert np.array_equal(cpg.ppr_cheby_coeffs(a, 300), Ref.ppr_cheby_coeffs(a, 300))
