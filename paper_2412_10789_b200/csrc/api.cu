@@ -320,13 +320,32 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
-            const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
-            if (jobs) {
-                const int grid = occ * g->sm_count;
+            if (batch_split(g->nnz_loc)) {
+                // hub pieces (fused kernel with no plain rows), then the plain rows
                 if (prof) prof->before(st);
-                launch_batch(b, static_cast<int>(B), grid, st);
+                if (t.n_hub_items) {
+                    BatchArgs h = b;
+                    h.n_loc = b.hub_rows;
+                    const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
+                    const int hgrid = static_cast<int>(std::max<uint32_t>(
+                        1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
+                    launch_batch(h, static_cast<int>(B), hgrid, st);
+                    ++launches;
+                }
+                if (t.row_end > b.hub_rows) {
+                    launch_batch_rows(b, static_cast<int>(B), occ * g->sm_count, st);
+                    ++launches;
+                }
                 if (prof) prof->after(st);
-                ++launches;
+            } else {
+                const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
+                if (jobs) {
+                    const int grid = occ * g->sm_count;
+                    if (prof) prof->before(st);
+                    launch_batch(b, static_cast<int>(B), grid, st);
+                    if (prof) prof->after(st);
+                    ++launches;
+                }
             }
             gather_chunk(g, b.w_io, c, cols, st);
         }

@@ -450,6 +450,75 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
     }
 }
 
+// Plain-row batched step (rows [hub_rows, n_loc) of the chunk; hub pieces run
+// in cheby_batch_kernel first).  Without the hub path the kernel fits more
+// warps, and the next row's range and first index chunk are prefetched while
+// the current row's gathers and epilogue are in flight.
+template <int B, int U = 8, int MINB = 4>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(const BatchArgs a) {
+    constexpr int L = B / 2;     // lanes per row slot
+    constexpr int RPW = 32 / L;  // row slots per warp
+    constexpr int V = 32 / L;    // indices per lane per 32-edge chunk
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / L, cl = lane % L;
+    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t r_end = a.n_loc;
+    const uint32_t stride = nw * RPW;
+    uint32_t r = a.hub_rows + wg * RPW + slot;
+    int64_t e0 = 0, e1 = 0;
+    if (r < r_end) {
+        e0 = a.rowptr[r];
+        e1 = a.rowptr[r + 1];
+    }
+    uint32_t c[V];
+    auto load_chunk = [&](int64_t e, int64_t end) {
+        const int m = static_cast<int>(e < end ? (end - e < 32 ? end - e : 32) : 0);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int t = v * L + cl;
+            c[v] = t < m ? ld_index(a.col + e + t) : 0u;
+        }
+    };
+    load_chunk(e0, e1);
+    while (__any_sync(0xffffffffu, r < r_end)) {
+        const uint32_t rn = r + stride;
+        int64_t ne0 = 0, ne1 = 0;
+        if (rn < r_end) {  // next row's range, in flight during this row
+            ne0 = a.rowptr[rn];
+            ne1 = a.rowptr[rn + 1];
+        }
+        double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
+        if (r < r_end) batch_prefetch<B>(a, r, cl, wp, ac);
+        double2 s = {0.0, 0.0};
+        for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
+            const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
+            if (e != e0) load_chunk(e, e1);
+#pragma unroll
+            for (int t0 = 0; t0 < 32; t0 += U) {
+                if (!__any_sync(0xffffffffu, t0 < m)) break;
+                double2 val[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int t = t0 + q;
+                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    s.x += val[q].x;
+                    s.y += val[q].y;
+                }
+            }
+        }
+        load_chunk(ne0, ne1);  // next row's first chunk, overlapping this epilogue
+        if (r < r_end) batch_epilogue<B>(a, r, s, e1 - e0, cl, wp, ac);
+        r = rn;
+        e0 = ne0;
+        e1 = ne1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
@@ -576,6 +645,28 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
     default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
     }
 }
+// Split path: hub pieces through cheby_batch_kernel, then plain rows through
+// cheby_batch_rows_kernel.  Faster on every graph with >= 8M local edges
+// (profiles/r01/batch_split_ab.txt); tiny graphs keep the single fused launch.
+// CPG_BATCH_SPLIT=0/1 forces either.
+bool batch_split(uint64_t nnz_loc) {
+    static const int force = [] {
+        const char* e = std::getenv("CPG_BATCH_SPLIT");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    return force >= 0 ? force == 1 : nnz_loc >= (8ull << 20);
+}
+
+void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    switch (B) {
+    case 4: cheby_batch_rows_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 8: cheby_batch_rows_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 16: cheby_batch_rows_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 32: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
+    default: cheby_batch_rows_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    }
+}
+
 int batch_occupancy() {
     int blocks = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel<64>, kBatchThreads, 0);
