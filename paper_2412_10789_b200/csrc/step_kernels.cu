@@ -396,13 +396,25 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
         double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
         if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
         double2 s = {0.0, 0.0};
-        for (int64_t e = j.e0; __any_sync(0xffffffffu, e < j.e1); e += 32) {
-            const int m = static_cast<int>(e < j.e1 ? (j.e1 - e < 32 ? j.e1 - e : 32) : 0);
-            uint32_t c[V];
+        uint32_t c[V], cn[V];
+        {
+            const int m0 = static_cast<int>(j.e0 < j.e1 ? (j.e1 - j.e0 < 32 ? j.e1 - j.e0 : 32) : 0);
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const int t = v * L + cl;
-                c[v] = t < m ? ld_index(a.col + e + t) : 0u;
+                cn[v] = t < m0 ? ld_index(a.col + j.e0 + t) : 0u;
+            }
+        }
+        for (int64_t e = j.e0; __any_sync(0xffffffffu, e < j.e1); e += 32) {
+            const int m = static_cast<int>(e < j.e1 ? (j.e1 - e < 32 ? j.e1 - e : 32) : 0);
+            // current chunk <- prefetched one; prefetch the next chunk (in flight during the gathers)
+            const int64_t en = e + 32;
+            const int mn = static_cast<int>(en < j.e1 ? (j.e1 - en < 32 ? j.e1 - en : 32) : 0);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                c[v] = cn[v];
+                const int t = v * L + cl;
+                cn[v] = t < mn ? ld_index(a.col + en + t) : 0u;
             }
 #pragma unroll
             for (int t0 = 0; t0 < 32; t0 += U) {
@@ -491,9 +503,22 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
         double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
         if (r < r_end) batch_prefetch<B>(a, r, cl, wp, ac);
         double2 s = {0.0, 0.0};
+        uint32_t cn[V];
         for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
             const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
-            if (e != e0) load_chunk(e, e1);
+            if (e != e0) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) c[v] = cn[v];
+            }
+            if (__any_sync(0xffffffffu, e + 32 < e1)) {  // long row: prefetch the next chunk
+                const int64_t en = e + 32;
+                const int mn = static_cast<int>(en < e1 ? (e1 - en < 32 ? e1 - en : 32) : 0);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const int t = v * L + cl;
+                    cn[v] = t < mn ? ld_index(a.col + en + t) : 0u;
+                }
+            }
 #pragma unroll
             for (int t0 = 0; t0 < 32; t0 += U) {
                 if (!__any_sync(0xffffffffu, t0 < m)) break;
