@@ -329,7 +329,10 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                     const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
                         1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
-                    launch_batch(h, static_cast<int>(B), hgrid, st);
+                    if (std::getenv("CPG_PIECES_FUSED"))  // A/B hook: hub pieces through the fused kernel
+                        launch_batch(h, static_cast<int>(B), hgrid, st);
+                    else
+                        launch_batch_pieces(h, static_cast<int>(B), hgrid, st);
                     ++launches;
                 }
                 if (t.row_end > b.hub_rows) {

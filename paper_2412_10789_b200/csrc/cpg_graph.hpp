@@ -90,6 +90,7 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
 void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st);
+void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st);
 
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);

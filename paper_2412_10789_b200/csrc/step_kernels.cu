@@ -544,6 +544,119 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
     }
 }
 
+// Hub-piece batched step (split path): the jobs are the hub pieces of the
+// chunk.  The 16-B item carries the piece's first edge and length, so the next
+// piece's item and first index chunk are prefetched while the current piece's
+// gathers are in flight (as in cheby_batch_rows_kernel); pieces are combined
+// by the ordered last-arriver reduction.
+template <int B, int U = 8, int MINB = 4>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel(const BatchArgs a) {
+    constexpr int L = B / 2;
+    constexpr int RPW = 32 / L;
+    constexpr int V = 32 / L;
+    constexpr int HB = batch_hub_edges(B);
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / L, cl = lane % L;
+    const unsigned smask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
+    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_jobs = a.n_hub_items;
+    const uint32_t stride = nw * RPW;
+    uint32_t job = wg * RPW + slot;
+    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& sb, int64_t& e0, int64_t& e1) {
+        if (jb < n_jobs) {
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + jb);
+            const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+            r = raw.x;
+            sb = raw.y;
+            e0 = code_e0(c);
+            e1 = e0 + code_cnt(c);
+        } else {
+            r = sb = 0;
+            e0 = e1 = 0;
+        }
+    };
+    uint32_t c[V], cn[V];
+    auto load_chunk = [&](uint32_t (&dst)[V], int64_t e, int64_t end) {
+        const int m = static_cast<int>(e < end ? (end - e < 32 ? end - e : 32) : 0);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int t = v * L + cl;
+            dst[v] = t < m ? ld_index(a.col + e + t) : 0u;
+        }
+    };
+    uint32_t r, sb;
+    int64_t e0, e1;
+    load_item(job, r, sb, e0, e1);
+    load_chunk(c, e0, e1);
+    while (__any_sync(0xffffffffu, job < n_jobs)) {
+        uint32_t nr, nsb;
+        int64_t ne0, ne1;
+        load_item(job + stride, nr, nsb, ne0, ne1);  // in flight during this piece
+        int64_t rs = 0, re = 0;
+        if (job < n_jobs) {
+            rs = a.rowptr[r];
+            re = a.rowptr[r + 1];
+        }
+        double2 s = {0.0, 0.0};
+        for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
+            const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
+            if (e != e0) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) c[v] = cn[v];
+            }
+            if (__any_sync(0xffffffffu, e + 32 < e1)) load_chunk(cn, e + 32, e1);
+#pragma unroll
+            for (int t0 = 0; t0 < 32; t0 += U) {
+                if (!__any_sync(0xffffffffu, t0 < m)) break;
+                double2 val[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int t = t0 + q;
+                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    s.x += val[q].x;
+                    s.y += val[q].y;
+                }
+            }
+        }
+        load_chunk(c, ne0, ne1);  // next piece's first chunk
+        const bool live = job < n_jobs;
+        const int64_t d = re - rs;
+        const uint32_t P = live ? static_cast<uint32_t>((d + HB - 1) / HB) : 0u;
+        const uint32_t piece = live ? static_cast<uint32_t>((e0 - rs) / HB) : 0u;
+        if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[cl] = s;
+        __threadfence();
+        __syncwarp();
+        unsigned prev = 0;
+        if (live && cl == 0) prev = atomicAdd(&a.hub_count[r], 1u);
+        prev = __shfl_sync(0xffffffffu, prev, slot * L);
+        if (live && prev == P - 1) {  // last piece of the row: ordered combine + epilogue
+            __threadfence();
+            double2 y = {0.0, 0.0};
+            for (uint32_t p = 0; p < P; ++p) {
+                const double2 v =
+                    __ldcg(reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(sb + p) * B) + cl);
+                y.x += v.x;
+                y.y += v.y;
+            }
+            if (cl == 0) a.hub_count[r] = 0u;
+            double2 wp, ac;
+            batch_prefetch<B>(a, r, cl, wp, ac);
+            batch_epilogue<B>(a, r, y, d, cl, wp, ac);
+        }
+        (void)smask;
+        job += stride;
+        r = nr;
+        sb = nsb;
+        e0 = ne0;
+        e1 = ne1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
@@ -680,6 +793,16 @@ bool batch_split(uint64_t nnz_loc) {
         return e ? (e[0] == '0' ? 0 : 1) : -1;
     }();
     return force >= 0 ? force == 1 : nnz_loc >= (8ull << 20);
+}
+
+void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    switch (B) {
+    case 4: cheby_batch_pieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 16: cheby_batch_pieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 32: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
+    default: cheby_batch_pieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    }
 }
 
 void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st) {
