@@ -22,6 +22,7 @@
 // run (no floating-point atomics).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "device_graph.cuh"
@@ -796,6 +797,34 @@ bool batch_split(uint64_t nnz_loc) {
 }
 
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+    static const int cfg = [] {  // tuning hook: CPG_PIECES_CFG = U*10 + MINB (B = 16)
+        const char* e = std::getenv("CPG_PIECES_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (B == 16 && cfg) {
+        int occ = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        switch (cfg) {
+        case 83:
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 8, 3>, kBatchThreads, 0);
+            cheby_batch_pieces_kernel<16, 8, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            return;
+        case 163:
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 16, 3>, kBatchThreads, 0);
+            cheby_batch_pieces_kernel<16, 16, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            return;
+        case 44:
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 4, 4>, kBatchThreads, 0);
+            cheby_batch_pieces_kernel<16, 4, 4><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            return;
+        case 65:
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 6, 5>, kBatchThreads, 0);
+            cheby_batch_pieces_kernel<16, 6, 5><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            return;
+        default: break;
+        }
+    }
     switch (B) {
     case 4: cheby_batch_pieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
     case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
