@@ -128,6 +128,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def load_traffic(cfg_index, mode, tile):
+    """DRAM bytes per step of this workload's step kernel(s) from a committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"{cfg_index}:{mode}:{tile}", {}).get("bytes")
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -437,7 +447,9 @@ def run_ours(args, cfg):
                        "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": load_traffic(args.config, cfg["mode"], tile if batched else 1),
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, per step)",
                          "kernel": ("cheby_batch_kernel (hub pieces) + cheby_batch_rows_kernel, timed as one step"
                                     if batched else "cheby_step_kernel"),
                          "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms,
