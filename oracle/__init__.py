@@ -441,8 +441,12 @@ def edge_text(pairs) -> str:
     return "".join(f"{int(a)} {int(b)}\n" for a, b in np.asarray(pairs).reshape(-1, 2))
 
 
-def parity(gpu, ref, topk=100):
-    """max-abs, L1 and top-k set agreement (value desc, id asc: tools/chebyprop.cpp:151-156)."""
+def parity(gpu, ref, topk=100, tie_tol=1e-12):
+    """max-abs, L1 and top-k set agreement (value desc, id asc: tools/chebyprop.cpp:151-156).
+
+    ``topk_equal`` is exact set equality.  ``topk_equal_mod_ties`` allows the
+    sets to differ only in nodes whose scores lie within ``tie_tol`` of the k-th
+    score in both vectors (structural ties broken by last-bit rounding)."""
     gpu = np.asarray(gpu, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     d = np.abs(gpu - ref)
@@ -450,7 +454,15 @@ def parity(gpu, ref, topk=100):
 
     def top(v):
         order = np.lexsort((np.arange(len(v)), -v))
-        return set(order[:k].tolist())
+        return order[:k]
 
-    return {"max_abs": float(d.max()) if len(d) else 0.0, "l1": float(d.sum()),
-            "topk_equal": top(gpu) == top(ref)}
+    tg, tr = top(gpu), top(ref)
+    sg, sr = set(tg.tolist()), set(tr.tolist())
+    eq = sg == sr
+    mod_ties = eq
+    if not eq and k > 0:
+        kth = ref[tr[-1]]
+        diff = np.array(sorted(sg ^ sr))
+        mod_ties = bool(np.all(np.abs(ref[diff] - kth) <= tie_tol) and np.all(np.abs(gpu[diff] - kth) <= tie_tol))
+    return {"max_abs": float(d.max()) if len(d) else 0.0, "l1": float(d.sum()), "topk_equal": eq,
+            "topk_equal_mod_ties": mod_ties}

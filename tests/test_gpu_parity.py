@@ -303,3 +303,84 @@ def test_power_method_small_n(graphs, cpg):
         assert np.abs(est.values - exact).sum() <= 0.8 ** n_steps * (1 + 1e-12)
         want = Port.power_method(off, nb, Port.taylor_coeffs(PPR, 0.2, n_steps - 1), n_steps, 3)
         assert np.abs(est.values - want).max() <= 1e-12
+
+
+def test_edge_cases(cpg, gpu):
+    """Empty source list, duplicate sources, repeated calls, large K and extreme parameters."""
+    from oracle import Port
+
+    off, nb = Port.make_graph(300, 500, 13)
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    out, st = cpg.cheby_power_many(g, k, [], 26)
+    assert out.shape == (0, g.node_count()) and st.push_work == 0
+    out_b, _ = cpg.cheby_power_many(g, k, [], 26, batched=True)
+    assert out_b.shape == (0, g.node_count())
+    got, _ = cpg.cheby_power_many(g, k, [5, 5, 5], 26)
+    want, _, _ = ref.cheby_power(PPR, 0.2, 5, 26)
+    for j in range(3):
+        assert_parity(got[j], want)
+    got_b, _ = cpg.cheby_power_many(g, k, [5, 5, 7], 26, batched=True, tile=3)
+    assert_parity(got_b[0], want) and assert_parity(got_b[1], want)
+    for fam, p, eps in ((PPR, 0.02, 1e-10), (HKPR, 40.0, 1e-12), (PPR, 0.9, 1e-3), (HKPR, 0.3, 1e-6)):
+        kern = cpg.Kernel.ppr(p) if fam == PPR else cpg.Kernel.hkpr(p)
+        K = cpg.plan_truncation(kern, eps).cheby_steps
+        est = cpg.cheby_power(g, kern, 11, K)
+        want, _, _ = ref.cheby_power(fam, p, 11, K)
+        assert_parity(est.values, want)
+    est = cpg.cheby_power(g, k, 0, 200)  # far past convergence
+    want, _, _ = ref.cheby_power(PPR, 0.2, 0, 200)
+    assert_parity(est.values, want)
+
+
+def _cheby_power_longdouble(off, nb, coeffs, K, s):
+    """The reference recurrence (solvers.cpp:197-234) in x87 extended precision (numpy longdouble)."""
+    n = len(off) - 1
+    deg = np.diff(off).astype(np.longdouble)
+    rows = np.repeat(np.arange(n), np.diff(off).astype(np.int64))
+
+    def walk(x):  # graph.cpp:257-267
+        out = np.zeros(n, dtype=np.longdouble)
+        np.add.at(out, nb, (x / deg)[rows])
+        return out
+
+    c = np.asarray(coeffs, dtype=np.longdouble)
+    seed = np.zeros(n, dtype=np.longdouble)
+    seed[s] = 1
+    y = c[0] * seed
+    r_prev, r_cur = seed, walk(seed)
+    for k in range(1, K):
+        y = y + c[k] * r_cur
+        r_prev, r_cur = r_cur, 2 * walk(r_cur) - r_prev
+    return y + c[K] * r_cur
+
+
+def test_giant_hub_star(cpg, gpu):
+    """A 200k-leaf star (+ path among leaves): hub pieces P > 1 in every kernel.
+
+    The hub's score sums 200k terms; the reference adds them sequentially
+    (error up to ~n*eps relative), the GPU in pieces and trees.  Both are
+    compared against an extended-precision evaluation: the GPU must be at
+    least as accurate as the reference, and within 5e-12 of it."""
+    from oracle import Port
+
+    m = 200_000
+    pairs = [[0, i] for i in range(1, m + 1)] + [[i, i + 1] for i in range(1, m, 7)]
+    off, nb = Port.edges_to_csr(pairs)
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    k = cpg.Kernel.hkpr(5.0)
+    c = k.cheby_coeffs(15)
+    src = [0, 1, 12345]
+    got, _ = cpg.cheby_power_many(g, k, src, 15)
+    for tile in (3, 16, 64):
+        got_b, _ = cpg.cheby_power_many(g, k, src, 15, batched=True, tile=tile)
+        for j, s in enumerate(src):
+            want, _, _ = ref.cheby_power(HKPR, 5.0, s, 15)
+            truth = _cheby_power_longdouble(off, nb, c, 15, s)
+            for v in (got[j], got_b[j]):
+                assert_parity(v, want, max_abs=5e-12)
+                err_gpu = float(np.abs(v.astype(np.longdouble) - truth).max())
+                err_ref = float(np.abs(want.astype(np.longdouble) - truth).max())
+                assert err_gpu <= err_ref + 1e-13, (err_gpu, err_ref)
