@@ -171,6 +171,13 @@ int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K
                                   const uint32_t* sources, uint32_t n_sources, uint32_t tile,
                                   double* d_out, void* stream, cpg_stats* stats);
 
+/* general_gp_vector / general_gp_matrix with ChebyPower (solvers.cpp:390-414):
+ * z_j = D^-a f(P) D^a x_j for n_cols dense host columns X (n_cols x n), with the
+ * D^{+-a} scalings fused into the seed and output kernels; tile > 1 runs tiles
+ * of `tile` columns (<= 64) through the batched step. */
+int cpg_general_gp(cpg_graph* g, const double* coeffs, uint32_t K, double a, const double* X,
+                   uint32_t n_cols, uint32_t tile, double* out, cpg_stats* stats);
+
 /* Test/observer slow path: T_k(P)e_s for k = 0..K ((K+1) x n, host) and the
  * partial estimates after each step ((K+1) x n), the StepObserver arguments of
  * solvers.cpp:215,219,226.  Either trace pointer may be NULL. */

@@ -469,22 +469,27 @@ def apply_walk(g, x, device: int = 0) -> np.ndarray:
     return y
 
 
-def general_gp_vector(g: Graph, kernel: Kernel, a: float, x, steps: int, device: int = 0) -> np.ndarray:
+def general_gp_matrix(g, kernel: Kernel, a: float, columns, steps: int, tile: int = 64, device: int = 0):
+    """z_j = D^-a f(P) D^a x_j with ChebyPower for every column (solvers.cpp:390-414).
+
+    The D^{+-a} scalings are fused into the device seed/output kernels; columns
+    run in tiles of ``tile`` through the batched step (tile=1: one at a time)."""
+    K = _steps(steps)
+    dg = _dev(g, device)
+    cols = np.ascontiguousarray(np.atleast_2d(np.asarray(columns, dtype=np.float64)))
+    if cols.shape[1] != dg.n:
+        raise ParameterError("seed vector length mismatch")  # solvers.cpp:36-37
+    c = kernel.cheby_coeffs(K)
+    out = np.empty_like(cols)
+    s = cpg_stats()
+    _check(L.lib().cpg_general_gp(dg.handle, _f64p(c), K, float(a), _f64p(cols), cols.shape[0],
+                                  max(1, min(int(tile), 64)), out.ctypes.data, ctypes.byref(s)))
+    return list(out)
+
+
+def general_gp_vector(g, kernel: Kernel, a: float, x, steps: int, device: int = 0) -> np.ndarray:
     """z = D^-a f(P) D^a x with ChebyPower (solvers.cpp:390-403)."""
-    deg = g.degrees().astype(np.float64)
-    x = np.asarray(x, dtype=np.float64)
-    scaled = np.power(deg, a) * x
-    est = cheby_power_vec(g, kernel, scaled, steps, device=device)
-    return np.power(deg, -a) * est.values
-
-
-def general_gp_matrix(g: Graph, kernel: Kernel, a: float, columns, steps: int, device: int = 0):
-    """Column-wise general_gp_vector (solvers.cpp:405-414), all columns in one device call."""
-    cols = np.atleast_2d(np.asarray(columns, dtype=np.float64))
-    deg = g.degrees().astype(np.float64)
-    scaled = cols * np.power(deg, a)[None, :]
-    est = cheby_power_vec(g, kernel, scaled, steps, device=device)
-    return list(est.values * np.power(deg, -a)[None, :])
+    return general_gp_matrix(g, kernel, a, [x], steps, tile=1, device=device)[0]
 
 
 # ---- synthetic inputs ----------------------------------------------------------------------

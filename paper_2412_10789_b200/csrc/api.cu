@@ -264,13 +264,13 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
 // One single-source (or dense-seed, when seed_dev != null) query; result
 // d*acc unpermuted into d_dst[n] (caller ids) if non-null.
 uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
-                    cudaStream_t st, StepProf* prof, bool taylor = false) {
+                    cudaStream_t st, StepProf* prof, bool taylor = false, double gp_a = 0.0) {
     uint32_t launches = 0;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
     CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * C * g->step_grid, st));
     if (seed_dev)
-        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, st);
+        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, gp_a, st);
     else
         launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
     ++launches;
@@ -281,7 +281,7 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
     launch_mass_err(g->d_step_mass, K, mass0, g->d_mass_err, st);
     ++launches;
     if (d_dst) {
-        launch_unpermute(d_dst, gather_result(g, 1, st), g->new_of_old, g->n, st);
+        launch_unpermute(d_dst, gather_result(g, 1, st), g->new_of_old, g->n, g->gdeg, gp_a, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -290,13 +290,16 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
 
 // One tile of up to B sources (q0 .. q0+count) through the batched step.
 uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
-                   cudaStream_t st, StepProf* prof) {
+                   cudaStream_t st, StepProf* prof, const double* seeds_dev = nullptr, double gp_a = 0.0) {
     uint32_t launches = 0;
     const size_t cols = B;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     const int occ = batch_occupancy();
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
-    launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
+    if (seeds_dev)
+        launch_init_dense_batch(g->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
+    else
+        launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
     ++launches;
     for (uint32_t k = 1; k <= K; ++k) {
         BatchArgs b;
@@ -355,7 +358,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
     }
     wait_gathers(g, st);
     if (d_dst) {
-        launch_unpermute_batch(d_dst, gather_result(g, cols, st), g->new_of_old, g->n, count, B, st);
+        launch_unpermute_batch(d_dst, gather_result(g, cols, st), g->new_of_old, g->n, count, B, g->gdeg, gp_a, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -388,13 +391,16 @@ void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, do
 }
 
 // Shared driver for host / device outputs.  mode 0 = one-hot single source,
-// 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources.
+// 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources,
+// 3 = power method (Taylor), 4 = batched dense seed columns (general_gp_matrix).
 int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
           uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
-          cpg_stats* stats) {
+          cpg_stats* stats, double gp_a = 0.0) {
     return guarded([&] {
         require(g != nullptr, "null graph handle");
-        if (mode == 1) {
+        require(std::isfinite(gp_a), "general_gp: exponent must be finite");
+        const bool dense = mode == 1 || mode == 4;
+        if (dense) {
             require(K >= 1, "cheby_power: cheby_steps must be >= 1");
             require(coeffs && (nq == 0 || seeds_host), "null argument");
         } else {
@@ -411,9 +417,10 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             CPG_CUDA(cudaEventRecord(g->ev[4], static_cast<cudaStream_t>(user_stream)));
             CPG_CUDA(cudaStreamWaitEvent(st, g->ev[4], 0));
         }
-        const uint32_t B = mode == 2 ? batch_width(tile) : 1;
+        const bool batched = mode == 2 || mode == 4;
+        const uint32_t B = batched ? batch_width(tile) : 1;
         const size_t cols = B;
-        if (mode == 2) {
+        if (batched) {
             require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
             ensure_batch_tables(g, static_cast<int>(B));
             const size_t need = static_cast<size_t>(g->n_bpartials) * B;
@@ -428,13 +435,13 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             }
         }
         ensure_ws(g, cols);
-        upload_params(g, coeffs, K, sources, mode == 1 ? 0 : nq, st);
+        upload_params(g, coeffs, K, sources, dense ? 0 : nq, st);
         const size_t n = g->n;
-        const uint32_t per = mode == 2 ? tile : 1;
+        const uint32_t per = batched ? tile : 1;
         const uint32_t nbatches = (nq + per - 1) / per;
         const size_t slot = n * per;  // doubles per result slot
         double* seed_dev = nullptr;
-        if (mode == 1) seed_dev = dalloc<double>(n);
+        if (dense) seed_dev = dalloc<double>(n * per);
         if (!out_on_device && out) ensure_stage(g, slot);
         uint32_t launches = 0;
         std::unique_ptr<StepProf> prof(g_profile.load() ? new StepProf : nullptr);
@@ -453,10 +460,15 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
                 launches += run_single(g, K, q0, nullptr, 1.0, dst, st, prof.get(), mode == 3);
             } else if (mode == 1) {
                 const double* sh = seeds_host + static_cast<size_t>(q0) * n;
-                double mass0 = 0.0;
+                double mass0 = 0.0;  // sum of the D^a-scaled seed: the conserved mass
                 for (size_t v = 0; v < n; ++v) mass0 += sh[v];
                 CPG_CUDA(cudaMemcpyAsync(seed_dev, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-                launches += run_single(g, K, q0, seed_dev, mass0, dst, st, prof.get());
+                launches += run_single(g, K, q0, seed_dev, gp_a == 0.0 ? mass0 : std::nan(""), dst, st, prof.get(),
+                                       false, gp_a);
+            } else if (mode == 4) {
+                CPG_CUDA(cudaMemcpyAsync(seed_dev, seeds_host + static_cast<size_t>(q0) * n,
+                                         sizeof(double) * n * count, cudaMemcpyHostToDevice, st));
+                launches += run_batch(g, K, B, q0, count, dst, st, prof.get(), seed_dev, gp_a);
             } else {
                 launches += run_batch(g, K, B, q0, count, dst, st, prof.get());
             }
@@ -494,7 +506,7 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (seed_dev) cudaFree(seed_dev);
-        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, mode == 2 ? tile : 1u);
+        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, batched ? tile : 1u);
         if (stats && prof) {
             stats->step_ms = prof->total_ms();
             stats->step_launches = static_cast<uint32_t>(prof->ev.size() / 2);
@@ -676,6 +688,15 @@ int cpg_power_method(cpg_graph* g, const double* zeta, uint32_t n_steps, const u
         }
         if (stats) *stats = cpg_stats{1, 0, 0.0, 0.0, 0.0, 0.0, 0, 0.0, 0};
     });
+}
+
+// general_gp_vector / general_gp_matrix with ChebyPower (solvers.cpp:390-414):
+// z_j = D^-a f(P) D^a x_j for n_cols dense columns, in tiles of `tile` columns
+// through the batched step (tile 1: single-column path).
+int cpg_general_gp(cpg_graph* g, const double* coeffs, uint32_t K, double a, const double* X, uint32_t n_cols,
+                   uint32_t tile, double* out, cpg_stats* stats) {
+    if (tile <= 1) return drive(g, coeffs, K, nullptr, X, n_cols, 1, 1, out, false, nullptr, stats, a);
+    return drive(g, coeffs, K, nullptr, X, n_cols, tile, 4, out, false, nullptr, stats, a);
 }
 
 int cpg_apply_walk(cpg_graph* g, const double* x, double* y) {

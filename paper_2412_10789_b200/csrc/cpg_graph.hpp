@@ -97,10 +97,13 @@ void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, con
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                               uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st);
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
-                       uint32_t n, cudaStream_t st);
-void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, cudaStream_t st);
+                       uint32_t n, double a, cudaStream_t st);
+void launch_init_dense_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const double* X, uint32_t n,
+                             uint32_t count, uint32_t B, double a, cudaStream_t st);
+void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, const uint32_t* gdeg,
+                      double a, cudaStream_t st);
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
-                            uint32_t count, uint32_t B, cudaStream_t st);
+                            uint32_t count, uint32_t B, const uint32_t* gdeg, double a, cudaStream_t st);
 void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st);
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
 

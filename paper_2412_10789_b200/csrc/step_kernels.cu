@@ -679,29 +679,52 @@ __global__ void init_onehot_batch_kernel(double* W, const uint32_t* gdeg, const 
     }
 }
 
-// w_0 = D^-1 seed for a dense seed given in caller ids.
+// w_0 = D^-1 (D^a seed) for a dense seed given in caller ids (a = 0: plain
+// cheby_power_vec; a != 0: general_gp_vector's D^a scaling, solvers.cpp:396-397).
 __global__ void init_dense_kernel(double* w, const uint32_t* gdeg, const uint32_t* new_of_old,
-                                  const double* seed, uint32_t n) {
+                                  const double* seed, uint32_t n, double a) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         const uint32_t s = new_of_old[v];
-        w[s] = seed[v] / static_cast<double>(gdeg[s]);
+        const double d = static_cast<double>(gdeg[s]);
+        const double x = a == 0.0 ? seed[v] : pow(d, a) * seed[v];
+        w[s] = x / d;
     }
 }
 
-// out[v] = full[new_of_old[v]]  (back to the caller's ids).
-__global__ void unpermute_kernel(double* out, const double* full, const uint32_t* new_of_old, uint32_t n) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        out[v] = full[new_of_old[v]];
-}
-
-// Batched: out[j][v] = full[new_of_old[v]][j] for j < count (full is [n_pad][B]).
-__global__ void unpermute_batch_kernel(double* out, const double* full, const uint32_t* new_of_old,
-                                       uint32_t n, uint32_t count, uint32_t B) {
+// Batched dense seeds: column j of W_0 ([n_pad][B]) = D^-1 D^a X[j] (X is count x n).
+__global__ void init_dense_batch_kernel(double* W, const uint32_t* gdeg, const uint32_t* new_of_old,
+                                        const double* X, uint32_t n, uint32_t count, uint32_t B, double a) {
     const uint64_t total = static_cast<uint64_t>(n) * count;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t j = static_cast<uint32_t>(i / n), v = static_cast<uint32_t>(i % n);
-        out[i] = full[static_cast<size_t>(new_of_old[v]) * B + j];
+        const uint32_t s = new_of_old[v];
+        const double d = static_cast<double>(gdeg[s]);
+        const double x = a == 0.0 ? X[i] : pow(d, a) * X[i];
+        W[static_cast<size_t>(s) * B + j] = x / d;
+    }
+}
+
+// out[v] = d_v^-a full[new_of_old[v]]  (back to the caller's ids; a != 0 only
+// for general_gp_vector, solvers.cpp:400-401).
+__global__ void unpermute_kernel(double* out, const double* full, const uint32_t* new_of_old, uint32_t n,
+                                 const uint32_t* gdeg, double a) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t s = new_of_old[v];
+        out[v] = a == 0.0 ? full[s] : pow(static_cast<double>(gdeg[s]), -a) * full[s];
+    }
+}
+
+// Batched: out[j][v] = full[new_of_old[v]][j] for j < count (full is [n_pad][B]).
+__global__ void unpermute_batch_kernel(double* out, const double* full, const uint32_t* new_of_old,
+                                       uint32_t n, uint32_t count, uint32_t B, const uint32_t* gdeg, double a) {
+    const uint64_t total = static_cast<uint64_t>(n) * count;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t j = static_cast<uint32_t>(i / n), v = static_cast<uint32_t>(i % n);
+        const uint32_t s = new_of_old[v];
+        const double y = full[static_cast<size_t>(s) * B + j];
+        out[i] = a == 0.0 ? y : pow(static_cast<double>(gdeg[s]), -a) * y;
     }
 }
 
@@ -858,15 +881,20 @@ void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* n
     init_onehot_batch_kernel<<<1, 64, 0, st>>>(W, gdeg, no, src, q0, count, B);
 }
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
-                       uint32_t n, cudaStream_t st) {
-    init_dense_kernel<<<1184, 256, 0, st>>>(w, gdeg, no, seed, n);
+                       uint32_t n, double a, cudaStream_t st) {
+    init_dense_kernel<<<1184, 256, 0, st>>>(w, gdeg, no, seed, n, a);
 }
-void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, cudaStream_t st) {
-    unpermute_kernel<<<1184, 256, 0, st>>>(out, full, no, n);
+void launch_init_dense_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const double* X, uint32_t n,
+                             uint32_t count, uint32_t B, double a, cudaStream_t st) {
+    init_dense_batch_kernel<<<2368, 256, 0, st>>>(W, gdeg, no, X, n, count, B, a);
+}
+void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, const uint32_t* gdeg,
+                      double a, cudaStream_t st) {
+    unpermute_kernel<<<1184, 256, 0, st>>>(out, full, no, n, gdeg, a);
 }
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
-                            uint32_t count, uint32_t B, cudaStream_t st) {
-    unpermute_batch_kernel<<<2368, 256, 0, st>>>(out, full, no, n, count, B);
+                            uint32_t count, uint32_t B, const uint32_t* gdeg, double a, cudaStream_t st) {
+    unpermute_batch_kernel<<<2368, 256, 0, st>>>(out, full, no, n, count, B, gdeg, a);
 }
 void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st) {
     mass_steps_kernel<<<K, kStepThreads, 0, st>>>(mp, n_part, steps);

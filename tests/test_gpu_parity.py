@@ -204,6 +204,25 @@ def test_errors(graphs, cpg):
         cpg.cheby_power_vec(g, cpg.Kernel.ppr(0.2), np.zeros(2), 5)  # solvers.cpp:36-37
 
 
+@pytest.mark.parametrize("a", [0.0, 0.5, 1.0, -0.3])
+@pytest.mark.parametrize("tile", [1, 4, 16, 64])
+def test_general_gp_matrix_matches_reference(graphs, cpg, a, tile):
+    """general_gp_matrix (solvers.cpp:405-414) with fused D^{+-a} scalings, in column tiles."""
+    from oracle import Port
+
+    off, nb = graphs["chunglu"]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    cols = [Port.random_vector(g.node_count(), 100 + j, 0.0, 1.0) for j in range(7)]
+    kern = cpg.Kernel.hkpr(5.0)
+    got = cpg.general_gp_matrix(g, kern, a, cols, 15, tile=tile)
+    for j, x in enumerate(cols):
+        want = ref.general_gp_vector(HKPR, 5.0, a, x, 15)
+        scale = max(1.0, np.abs(want).max())
+        assert np.abs(got[j] - want).max() <= 1e-12 * scale
+        assert np.abs(got[j] - want).sum() <= 1e-10 * max(1.0, np.abs(want).sum())
+
+
 def test_general_gp_vector_a_half(graphs, cpg):
     """acceptance.cpp:317-347 (C12) style: a = 1/2 against the reference wrapper."""
     from oracle import Port
