@@ -171,6 +171,13 @@ int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K
                                   const uint32_t* sources, uint32_t n_sources, uint32_t tile,
                                   double* d_out, void* stream, cpg_stats* stats);
 
+/* ChebyPower ranked on the device: for each source the
+ * k best (caller id, score) pairs by (score desc, id asc), the order of the
+ * reference's query output (tools/chebyprop.cpp:148-156).  ids/vals are host
+ * arrays of n_sources*min(k,n). */
+int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                        uint32_t n_sources, uint32_t k, uint32_t* ids, double* vals, cpg_stats* stats);
+
 /* general_gp_vector / general_gp_matrix with ChebyPower (solvers.cpp:390-414):
  * z_j = D^-a f(P) D^a x_j for n_cols dense host columns X (n_cols x n), with the
  * D^{+-a} scalings fused into the seed and output kernels; tile > 1 runs tiles

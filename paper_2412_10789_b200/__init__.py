@@ -42,7 +42,7 @@ __all__ = [
     "TruncationPlan", "SolveStats", "Estimate", "ppr_cheby_coeffs", "hkpr_cheby_coeffs", "plan_truncation",
     "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
     "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
-    "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan",
+    "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan", "cheby_power_topk",
 ]
 
 
@@ -425,6 +425,22 @@ def cheby_power_many(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int
     else:
         _check(L.lib().cpg_chebypower(dg.handle, _f64p(c), K, _u32p(src), len(src), ptr, ctypes.byref(s)))
     return out, _to_stats(s, K)
+
+
+def cheby_power_topk(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, k: int = 50, device: int = 0):
+    """Top-k (ids, scores) per source ranked on the device by (score desc, id asc),
+    the order of the reference's query output (tools/chebyprop.cpp:148-156)."""
+    K = _steps(cheby_steps)
+    dg = _dev(g, device)
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    kk = min(int(k), dg.n)
+    ids = np.empty((len(src), kk), dtype=np.uint32)
+    vals = np.empty((len(src), kk))
+    c = kernel.cheby_coeffs(K)
+    s = cpg_stats()
+    _check(L.lib().cpg_chebypower_topk(dg.handle, _f64p(c), K, _u32p(src), len(src), int(k), _u32p(ids),
+                                       _f64p(vals), ctypes.byref(s)))
+    return ids, vals, _to_stats(s, K)
 
 
 def power_method(g, kernel: Kernel, source: int, n_steps: int, device: int = 0) -> Estimate:

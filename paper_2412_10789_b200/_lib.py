@@ -70,6 +70,8 @@ SIGNATURES = {
                                               c_void_p, POINTER(cpg_stats)]),
     "cpg_chebypower_trace": (c_int, [_G, _f64p, c_uint32, c_uint32, c_void_p, c_void_p, c_void_p]),
     "cpg_apply_walk": (c_int, [_G, _f64p, _f64p]),
+    "cpg_chebypower_topk": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_uint32, _u32p, _f64p,
+                                    POINTER(cpg_stats)]),
     "cpg_general_gp": (c_int, [_G, _f64p, c_uint32, c_double, _f64p, c_uint32, c_uint32, c_void_p,
                                POINTER(cpg_stats)]),
     "cpg_bytes_per_step": (c_double, [_G, c_uint32]),

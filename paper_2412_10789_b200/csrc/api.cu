@@ -690,6 +690,43 @@ int cpg_power_method(cpg_graph* g, const double* zeta, uint32_t n_steps, const u
     });
 }
 
+// Queries ranked on the device: only the top-k (caller id, score) pairs per
+// source come back (the reference ranks on the host, tools/chebyprop.cpp:148-156).
+int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t n_sources,
+                        uint32_t k, uint32_t* ids, double* vals, cpg_stats* stats) {
+    return guarded([&] {
+        check_query(g, coeffs, K, sources, n_sources);
+        require(k >= 1 && ids && vals, "topk: k >= 1 and output arrays required");
+        const uint32_t kk = std::min(k, g->n);
+        double* d_res = nullptr;
+        {
+            DeviceGuard dg(g->device);
+            d_res = dalloc<double>(g->n);
+        }
+        cpg_stats acc{};
+        for (uint32_t q = 0; q < n_sources; ++q) {
+            cpg_stats st{};
+            const int rc = drive(g, coeffs, K, sources + q, nullptr, 1, 1, 0, d_res, true, nullptr, &st);
+            if (rc != CPG_OK) {
+                cudaFree(d_res);
+                fail(rc, cpg_last_error());
+            }
+            DeviceGuard dg(g->device);
+            device_topk(d_res, g->n, kk, ids + static_cast<size_t>(q) * kk, vals + static_cast<size_t>(q) * kk,
+                        g->stream);
+            acc.iterations = st.iterations;
+            acc.push_work += st.push_work;
+            acc.wall_seconds += st.wall_seconds;
+            acc.device_ms += st.device_ms;
+            acc.mass_err_max = std::max(acc.mass_err_max, st.mass_err_max);
+            acc.bytes_model += st.bytes_model;
+            acc.launches += st.launches;
+        }
+        cudaFree(d_res);
+        if (stats) *stats = acc;
+    });
+}
+
 // general_gp_vector / general_gp_matrix with ChebyPower (solvers.cpp:390-414):
 // z_j = D^-a f(P) D^a x_j for n_cols dense columns, in tiles of `tile` columns
 // through the batched step (tile 1: single-column path).

@@ -107,6 +107,9 @@ void launch_unpermute_batch(double* out, const double* full, const uint32_t* no,
 void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st);
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
 
+// topk.cu
+void device_topk(const double* d_vals, uint32_t n, uint32_t k, uint32_t* ids, double* vals, cudaStream_t st);
+
 // nccl_dl.cpp
 void nccl_get_unique_id(void* out128);
 void* nccl_comm_init(const void* id128, int nranks, int rank);

@@ -403,3 +403,32 @@ def test_giant_hub_star(cpg, gpu):
                 err_gpu = float(np.abs(v.astype(np.longdouble) - truth).max())
                 err_ref = float(np.abs(want.astype(np.longdouble) - truth).max())
                 assert err_gpu <= err_ref + 1e-13, (err_gpu, err_ref)
+
+
+@pytest.mark.parametrize("k", [1, 50, 100, 1000])
+def test_device_topk_matches_reference_ranking(graphs, cpg, k):
+    """Device top-k equals ranking the reference's vector by (value desc, id asc)."""
+    off, nb = graphs["chunglu"]
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    src = [0, 3, 999]
+    ids, vals, _ = cpg.cheby_power_topk(g, cpg.Kernel.ppr(0.2), src, 26, k)
+    full, _ = cpg.cheby_power_many(g, cpg.Kernel.ppr(0.2), src, 26)
+    for j, s in enumerate(src):
+        order = np.lexsort((np.arange(g.node_count()), -full[j]))[:k]
+        assert np.array_equal(ids[j], order.astype(np.uint32))
+        assert np.array_equal(vals[j], full[j][order])
+        want, _, _ = ref.cheby_power(PPR, 0.2, s, 26)
+        assert np.abs(vals[j] - want[ids[j]]).max() <= 1e-12
+
+
+def test_device_topk_ties_and_k_over_n(cpg, gpu):
+    from oracle import Port
+
+    off, nb = Port.make_graph(64, 0, 1)  # plain ring: massive ties
+    g = cpg.Graph.from_csr(off, nb)
+    ids, vals, _ = cpg.cheby_power_topk(g, cpg.Kernel.ppr(0.5), [0], 1, 1000)
+    assert ids.shape == (1, 64)
+    full, _ = cpg.cheby_power_many(g, cpg.Kernel.ppr(0.5), [0], 1)
+    order = np.lexsort((np.arange(64), -full[0]))
+    assert np.array_equal(ids[0], order.astype(np.uint32))
