@@ -216,6 +216,13 @@ int cpg_gen_chunglu(uint32_t n_ids, uint64_t n_samples, double exponent, double 
                     uint32_t max_degree, uint64_t seed, int device, uint64_t** offsets,
                     uint32_t** neighbors, uint32_t* n, uint64_t* nnz);
 int cpg_free_csr(uint64_t* offsets, uint32_t* neighbors, int device);
+/* GPU ingest with the reference loader's semantics (graph.cpp:113-171): host
+ * label pairs (m x 2 int64) -> device CSR; self-loops dropped, labels interned
+ * in first-seen order, symmetrised, sorted, deduplicated.  original_ids_host
+ * (capacity original_ids_cap) receives the label of every compact id
+ * (Graph::original_ids, graph.hpp:45), or NULL. */
+int cpg_ingest_edges(const int64_t* pairs, uint64_t m, int device, uint64_t** offsets, uint32_t** neighbors,
+                     uint32_t* n, uint64_t* nnz, int64_t* original_ids_host, uint64_t original_ids_cap);
 /* Copy a device-resident CSR (e.g. from the generator) into caller host arrays. */
 int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint32_t n, uint64_t nnz,
                     int device, uint64_t* offsets, uint32_t* neighbors);

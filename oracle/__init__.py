@@ -281,6 +281,8 @@ class Ref:
                 getattr(L, f).argtypes = [c_void_p]
                 getattr(L, f).restype = c_uint64
             L.ref_graph_csr.argtypes = [c_void_p, _u64p, _u32p]
+            L.ref_graph_original_ids.argtypes = [c_void_p, _i64p]
+            L.ref_graph_original_ids.restype = c_uint64
             L.ref_apply_walk.argtypes = [c_void_p, _f64p, _f64p]
             L.ref_cheby_power.argtypes = [c_void_p, c_int, c_double, c_uint32, c_uint64, _f64p,
                                           _f64p, _u64p, _f64p]
@@ -373,6 +375,12 @@ class RefGraph:
         nb = np.empty(self.nnz, dtype=np.uint32)
         Ref.lib().ref_graph_csr(self.h, _p(off, _u64p), _p(nb, _u32p))
         return off, nb
+
+    def original_ids(self):
+        k = int(Ref.lib().ref_graph_original_ids(self.h, None))
+        out = np.empty(k, dtype=np.int64)
+        Ref.lib().ref_graph_original_ids(self.h, _p(out, _i64p))
+        return out
 
     def structure_hash(self):
         return int(Ref.lib().ref_graph_hash(self.h))

@@ -124,6 +124,13 @@ uint64_t ref_graph_n(void* g) { return static_cast<Graph*>(g)->node_count(); }
 uint64_t ref_graph_nnz(void* g) { return static_cast<Graph*>(g)->volume(); }
 uint64_t ref_graph_hash(void* g) { return static_cast<Graph*>(g)->structure_hash(); }
 
+// Graph::original_ids() (graph.hpp:45): label of every compact id (loader graphs).
+uint64_t ref_graph_original_ids(void* gp, int64_t* out) {
+    const auto& ids = static_cast<Graph*>(gp)->original_ids();
+    if (out) std::memcpy(out, ids.data(), ids.size() * sizeof(int64_t));
+    return ids.size();
+}
+
 int ref_graph_csr(void* gp, uint64_t* offsets, uint32_t* nbrs) {
     const Graph& g = *static_cast<Graph*>(gp);
     std::memcpy(offsets, g.offsets().data(), g.offsets().size() * sizeof(uint64_t));

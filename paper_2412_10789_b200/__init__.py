@@ -43,6 +43,7 @@ __all__ = [
     "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
     "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
     "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan", "cheby_power_topk",
+    "ingest_edges", "load_edge_list_file",
 ]
 
 
@@ -546,6 +547,39 @@ def _gen_result(rc, off, nbr, n, nnz, device):
         L.lib().cpg_free_csr(off, nbr, -1)
         return o, b
     return DeviceCSR(off.value, nbr.value, n.value, nnz.value, device)
+
+
+def ingest_edges(pairs, device: int = 0):
+    """Edge list -> CSR on the GPU with the reference loader's semantics (graph.cpp:113-171).
+
+    Returns (DeviceCSR, original_ids) -- original_ids[i] is the label of compact id i."""
+    pr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1, 2))
+    off, nbr = ctypes.c_void_p(), ctypes.c_void_p()
+    n, nnz = ctypes.c_uint32(), ctypes.c_uint64()
+    labels = np.empty(2 * len(pr) + 1, dtype=np.int64)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    _check(L.lib().cpg_ingest_edges(pr.ctypes.data_as(i64p), len(pr), device, ctypes.byref(off), ctypes.byref(nbr),
+                                    ctypes.byref(n), ctypes.byref(nnz), labels.ctypes.data_as(i64p), len(labels)),
+           "ingest")
+    return DeviceCSR(off.value, nbr.value, n.value, nnz.value, device), labels[: n.value].copy()
+
+
+def load_edge_list_file(path: str, device: int = 0, comment: str = "#") -> Graph:
+    """graph.cpp:173-177 + :113-171: parse "u v" lines on the host, build the CSR on the GPU."""
+    import numpy as _np
+
+    try:
+        data = _np.loadtxt(path, dtype=_np.int64, comments=comment, usecols=(0, 1), ndmin=2)
+    except OSError as e:
+        raise DeviceError(f"cannot open graph file: {path}") from e
+    except ValueError as e:
+        raise ParameterError(f"malformed edge list {path}: {e}") from e
+    csr, labels = ingest_edges(data, device)
+    off, nb = csr.to_host()
+    csr.close()
+    g = Graph(off, nb)
+    g.original_ids = labels
+    return g
 
 
 def gen_rmat(scale: int, n_samples: int, a=0.57, b=0.19, c=0.19, seed: int = 1, device: int = -1):

@@ -80,6 +80,8 @@ SIGNATURES = {
     "cpg_gen_chunglu": (c_int, [c_uint32, c_uint64, c_double, c_double, c_uint32, c_uint64, c_int,
                                 POINTER(c_void_p), POINTER(c_void_p), _u32p, _u64p]),
     "cpg_free_csr": (c_int, [c_void_p, c_void_p, c_int]),
+    "cpg_ingest_edges": (c_int, [POINTER(ctypes.c_int64), c_uint64, c_int, POINTER(c_void_p), POINTER(c_void_p),
+                                 _u32p, _u64p, POINTER(ctypes.c_int64), c_uint64]),
     "cpg_csr_to_host": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, _u64p, _u32p]),
 }
 

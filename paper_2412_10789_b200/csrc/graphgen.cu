@@ -233,6 +233,150 @@ std::vector<double> chunglu_cdf(uint32_t n, double exponent, double mean_degree,
     return cdf;
 }
 
+// ---- GPU ingest: the reference's load_edge_list semantics (graph.cpp:113-171) ----
+// Self-loops dropped (:149); labels interned in first-seen order over the
+// surviving edges, a before b (:120-124, :150-151); symmetrised (:152-153);
+// sorted and deduplicated (:158-160).
+__global__ void k_keep(const int64_t* pairs, uint64_t m, uint8_t* keep) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+        keep[e] = pairs[2 * e] != pairs[2 * e + 1];
+}
+
+// endpoint j of kept edge i: key = label with the sign bit flipped (unsigned order = signed order),
+// value = position 2i + side (first-seen order).
+__global__ void k_endpoints(const int64_t* pairs, const uint64_t* kept, uint64_t mk, uint64_t* key, uint64_t* pos) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mk; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e = kept[i];
+        key[2 * i] = static_cast<uint64_t>(pairs[2 * e]) ^ 0x8000000000000000ull;
+        key[2 * i + 1] = static_cast<uint64_t>(pairs[2 * e + 1]) ^ 0x8000000000000000ull;
+        pos[2 * i] = 2 * i;
+        pos[2 * i + 1] = 2 * i + 1;
+    }
+}
+
+// run heads of the label-sorted endpoints: head[j] = 1 if a new label starts at j
+__global__ void k_heads(const uint64_t* key, uint64_t cnt, uint32_t* head) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x)
+        head[j] = (j == 0 || key[j] != key[j - 1]) ? 1u : 0u;
+}
+
+// for each run head (unique label u = run index = run[j] - 1): first position and label
+__global__ void k_uniques(const uint64_t* key, const uint64_t* pos, const uint32_t* head, const uint32_t* run,
+                          uint64_t cnt, uint64_t* first_pos, uint64_t* label) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x)
+        if (head[j]) {
+            first_pos[run[j] - 1] = pos[j];  // stable sort: the run's first entry has the smallest position
+            label[run[j] - 1] = key[j];
+        }
+}
+
+__global__ void k_iota32(uint32_t* v, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+// id_of[run] = rank of the run's first position
+__global__ void k_rank(const uint32_t* run_by_pos, uint32_t n, uint32_t* id_of) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) id_of[run_by_pos[r]] = r;
+}
+
+__global__ void k_endpoint_ids(const uint64_t* pos, const uint32_t* run, const uint32_t* id_of, uint64_t cnt,
+                               uint32_t* id_at) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x)
+        id_at[pos[j]] = id_of[run[j] - 1];
+}
+
+__global__ void k_edge_keys(const uint32_t* id_at, uint64_t mk, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mk; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = id_at[2 * i], v = id_at[2 * i + 1];
+        keys[2 * i] = (u << 32) | v;
+        keys[2 * i + 1] = (v << 32) | u;
+    }
+}
+
+__global__ void k_labels_in_id_order(const uint64_t* label, const uint32_t* run_by_pos, uint32_t n, int64_t* out) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+        out[r] = static_cast<int64_t>(label[run_by_pos[r]] ^ 0x8000000000000000ull);
+}
+
+template <typename F>
+void cub_call(F&& f, cudaStream_t st) {
+    size_t bytes = 0;
+    f(nullptr, bytes);
+    void* tmp = nullptr;
+    CPG_CUDA(cudaMalloc(&tmp, std::max<size_t>(bytes, 1)));
+    f(tmp, bytes);
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+}
+
+template <typename T>
+T* dm(size_t count) {
+    T* p = nullptr;
+    CPG_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+    return p;
+}
+
+void ingest_device(const int64_t* d_pairs, uint64_t m, uint64_t** off_out, uint32_t** nbr_out, uint32_t* n_out,
+                   uint64_t* nnz_out, int64_t** labels_out) {
+    cudaStream_t st = 0;
+    uint8_t* keep = dm<uint8_t>(m);
+    uint64_t* kept = dm<uint64_t>(m);
+    uint64_t* d_cnt = dm<uint64_t>(1);
+    k_keep<<<grid_for(m), 256, 0, st>>>(d_pairs, m, keep);
+    cub::CountingInputIterator<uint64_t> iota(0);
+    cub_call([&](void* t, size_t& b) { cub::DeviceSelect::Flagged(t, b, iota, keep, kept, d_cnt, m, st); }, st);
+    uint64_t mk = 0;
+    CPG_CUDA(cudaMemcpy(&mk, d_cnt, sizeof(mk), cudaMemcpyDeviceToHost));
+    cudaFree(keep);
+    require(mk > 0, "empty graph after cleaning");  // graph.cpp:156
+    const uint64_t cnt = 2 * mk;
+    uint64_t *key = dm<uint64_t>(cnt), *pos = dm<uint64_t>(cnt), *key_s = dm<uint64_t>(cnt), *pos_s = dm<uint64_t>(cnt);
+    k_endpoints<<<grid_for(mk), 256, 0, st>>>(d_pairs, kept, mk, key, pos);
+    cudaFree(kept);
+    cub_call([&](void* t, size_t& b) { cub::DeviceRadixSort::SortPairs(t, b, key, key_s, pos, pos_s, cnt, 0, 64, st); },
+             st);
+    cudaFree(key);
+    cudaFree(pos);
+    uint32_t *head = dm<uint32_t>(cnt), *run = dm<uint32_t>(cnt);
+    k_heads<<<grid_for(cnt), 256, 0, st>>>(key_s, cnt, head);
+    // run[j] = number of run heads in [0, j] = 1 + run index of endpoint j
+    cub_call([&](void* t, size_t& b) { cub::DeviceScan::InclusiveSum(t, b, head, run, cnt, st); }, st);
+    uint32_t n = 0;
+    CPG_CUDA(cudaMemcpy(&n, run + cnt - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    uint64_t *first_pos = dm<uint64_t>(n), *label = dm<uint64_t>(n), *first_pos_s = dm<uint64_t>(n);
+    k_uniques<<<grid_for(cnt), 256, 0, st>>>(key_s, pos_s, head, run, cnt, first_pos, label);
+    cudaFree(head);
+    // order the labels by first appearance: id = rank of first position
+    uint32_t *runs = dm<uint32_t>(n), *run_by_pos = dm<uint32_t>(n), *id_of = dm<uint32_t>(n);
+    k_iota32<<<grid_for(n), 256, 0, st>>>(runs, n);
+    cub_call([&](void* t, size_t& b) {
+        cub::DeviceRadixSort::SortPairs(t, b, first_pos, first_pos_s, runs, run_by_pos, n, 0, 64, st);
+    }, st);
+    k_rank<<<grid_for(n), 256, 0, st>>>(run_by_pos, n, id_of);
+    uint32_t* id_at = dm<uint32_t>(cnt);
+    k_endpoint_ids<<<grid_for(cnt), 256, 0, st>>>(pos_s, run, id_of, cnt, id_at);
+    int64_t* labels = dm<int64_t>(n);
+    k_labels_in_id_order<<<grid_for(n), 256, 0, st>>>(label, run_by_pos, n, labels);
+    CPG_CUDA(cudaDeviceSynchronize());
+    for (void* p : {(void*)key_s, (void*)pos_s, (void*)run, (void*)first_pos, (void*)label, (void*)first_pos_s,
+                    (void*)runs, (void*)run_by_pos, (void*)id_of})
+        cudaFree(p);
+    uint64_t* keys = dm<uint64_t>(cnt);
+    k_edge_keys<<<grid_for(mk), 256, 0, st>>>(id_at, mk, keys);
+    cudaFree(id_at);
+    cudaFree(d_cnt);
+    try {
+        keys_to_csr_device(keys, cnt, n, 32, off_out, nbr_out, n_out, nnz_out);
+    } catch (...) {
+        cudaFree(keys);
+        cudaFree(labels);
+        throw;
+    }
+    cudaFree(keys);
+    require(*n_out == n, "ingest: id compaction mismatch");
+    *labels_out = labels;
+}
+
 } // namespace
 } // namespace cpg
 
@@ -311,6 +455,32 @@ int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint
         CPG_CUDA(cudaSetDevice(device));
         CPG_CUDA(cudaMemcpy(offsets, d_offsets, (static_cast<size_t>(n) + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
         CPG_CUDA(cudaMemcpy(neighbors, d_neighbors, nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int cpg_ingest_edges(const int64_t* pairs, uint64_t m, int device, uint64_t** offsets, uint32_t** neighbors,
+                     uint32_t* n, uint64_t* nnz, int64_t* original_ids_host, uint64_t original_ids_cap) {
+    return guarded([&] {
+        require(pairs && offsets && neighbors && n && nnz, "null argument");
+        require(device >= 0, "ingest runs on a device");
+        CPG_CUDA(cudaSetDevice(device));
+        int64_t* d_pairs = nullptr;
+        CPG_CUDA(cudaMalloc(&d_pairs, std::max<uint64_t>(1, 2 * m) * sizeof(int64_t)));
+        CPG_CUDA(cudaMemcpy(d_pairs, pairs, 2 * m * sizeof(int64_t), cudaMemcpyHostToDevice));
+        int64_t* labels = nullptr;
+        try {
+            require(m > 0, "empty graph after cleaning");
+            ingest_device(d_pairs, m, offsets, neighbors, n, nnz, &labels);
+        } catch (...) {
+            cudaFree(d_pairs);
+            throw;
+        }
+        cudaFree(d_pairs);
+        if (original_ids_host) {
+            require(original_ids_cap >= *n, "original_ids buffer too small");
+            CPG_CUDA(cudaMemcpy(original_ids_host, labels, *n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        }
+        cudaFree(labels);
     });
 }
 

@@ -432,3 +432,33 @@ def test_device_topk_ties_and_k_over_n(cpg, gpu):
     full, _ = cpg.cheby_power_many(g, cpg.Kernel.ppr(0.5), [0], 1)
     order = np.lexsort((np.arange(64), -full[0]))
     assert np.array_equal(ids[0], order.astype(np.uint32))
+
+
+def test_gpu_ingest_matches_reference_loader(cpg, gpu, tmp_path):
+    """GPU edge-list ingest == the reference's load_edge_list (graph.cpp:113-171):
+    self-loops, duplicates, both directions, negative / sparse int64 labels."""
+    from oracle import RefGraph, edge_text
+
+    rng = np.random.default_rng(7)
+    for trial in range(3):
+        m = 5000
+        labels = rng.choice(np.arange(-10**12, 10**12, 10**7), size=800, replace=False)
+        pairs = labels[rng.integers(0, 800, size=(m, 2))]
+        pairs[::97, 1] = pairs[::97, 0]          # self-loops
+        pairs = np.concatenate([pairs, pairs[:300, ::-1], pairs[:200]])  # reversed and exact duplicates
+        ref = RefGraph.from_edge_text(edge_text(pairs))
+        csr, ids = cpg.ingest_edges(pairs, 0)
+        off, nb = csr.to_host()
+        roff, rnb = ref.csr()
+        assert np.array_equal(off, roff) and np.array_equal(nb, rnb)
+        assert np.array_equal(ids, ref.original_ids())
+        csr.close()
+    path = tmp_path / "g.txt"
+    path.write_text("# comment\n\n1 2\n2 3 0.5\n  # indented comment\n3 1\n3 3\n4 1\n")
+    g = cpg.load_edge_list_file(str(path))
+    ref = RefGraph.from_edge_text("1 2\n2 3\n3 1\n3 3\n4 1\n")
+    roff, rnb = ref.csr()
+    assert np.array_equal(g.offsets(), roff) and np.array_equal(g.neighbor_array(), rnb)
+    assert list(g.original_ids) == [1, 2, 3, 4]
+    with pytest.raises(cpg.ParameterError):
+        cpg.ingest_edges([[5, 5]], 0)  # empty after cleaning
