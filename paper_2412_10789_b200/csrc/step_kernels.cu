@@ -812,11 +812,9 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
 // (profiles/r01/batch_split_ab.txt); tiny graphs keep the single fused launch.
 // CPG_BATCH_SPLIT=0/1 forces either.
 bool batch_split(uint64_t nnz_loc) {
-    static const int force = [] {
-        const char* e = std::getenv("CPG_BATCH_SPLIT");
-        return e ? (e[0] == '0' ? 0 : 1) : -1;
-    }();
-    return force >= 0 ? force == 1 : nnz_loc >= (8ull << 20);
+    const char* e = std::getenv("CPG_BATCH_SPLIT");  // read per call: tests force either path
+    if (e) return e[0] != '0';
+    return nnz_loc >= (8ull << 20);
 }
 
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st) {

@@ -462,3 +462,20 @@ def test_gpu_ingest_matches_reference_loader(cpg, gpu, tmp_path):
     assert list(g.original_ids) == [1, 2, 3, 4]
     with pytest.raises(cpg.ParameterError):
         cpg.ingest_edges([[5, 5]], 0)  # empty after cleaning
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("tile", [4, 16, 64])
+def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
+    """Both batched code paths (hub-piece + plain-row kernels, and the fused kernel)
+    on a graph with many hub pieces, against the reference."""
+    monkeypatch.setenv("CPG_BATCH_SPLIT", split)
+    off, nb = cpg.gen_chunglu(50000, 600000, 2.0, 24.0, 15000, seed=11)
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    src = ref.select_sources_uniform(min(tile, 9), 5)
+    kern = cpg.Kernel.ppr(0.2)
+    got, _ = cpg.cheby_power_many(g, kern, src, 26, batched=True, tile=tile)
+    for j, s in enumerate(src):
+        want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
+        assert_parity(got[j], want)
