@@ -295,6 +295,12 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
     const size_t cols = B;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     const int occ = batch_occupancy();
+    // L2 budget for the degree-sorted hot prefix of the gathered iterate: its rows are
+    // loaded evict_last, the rest evict_first.  64 MB of the 126 MB L2 measured best
+    // (profiles/r01/hot_prefix_sweep.txt); CPG_HOT_MB overrides, 0 = plain loads.
+    uint64_t hot_mb = 64;
+    if (const char* e = std::getenv("CPG_HOT_MB")) hot_mb = static_cast<uint64_t>(std::atoll(e));
+    const uint32_t hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (hot_mb << 20) / (8 * cols)));
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
     if (seeds_dev)
         launch_init_dense_batch(g->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
@@ -312,6 +318,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.hub_partial = g->bhub_partial;
         b.hub_count = g->bhub_count;
         b.coeffs = g->d_coeffs;
+        b.hot_rows = hot_rows;
         b.k = static_cast<int>(k);
         b.first = k == 1;
         b.last = k == K;

@@ -90,6 +90,7 @@ struct BatchArgs {
     unsigned int* hub_count;
     const double* coeffs;
     uint32_t row0;
+    uint32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last); 0 = off
     int k, first, last;
 };
 

@@ -81,6 +81,16 @@ __device__ __forceinline__ double2 ld_gather2(const double* p) {
 #endif
 }
 
+// Batched gathers with an L2 residency split: the degree-sorted hot prefix of
+// the iterate (rows < hot) is loaded evict_last, the cold tail evict_first.
+__device__ __forceinline__ double2 ld_gather2_hot(const double* p, bool hot, uint64_t pol_last, uint64_t pol_first) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(hot ? pol_last : pol_first));
+    return v;
+}
+
 // Deterministic CTA sum: xor butterfly per warp, warp partials summed in warp
 // order by thread 0.  Result valid in thread 0 only.
 template <int THREADS>
@@ -386,6 +396,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
     constexpr int RPW = 32 / L;   // row slots per warp
     constexpr int V = 32 / L;     // indices per lane per 32-edge chunk
     // U: row gathers in flight per lane
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const unsigned smask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
@@ -425,7 +436,10 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                  u < a.hot_rows, pol_last, pol_first)
+                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                   : make_double2(0.0, 0.0);
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
@@ -472,6 +486,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
     constexpr int L = B / 2;     // lanes per row slot
     constexpr int RPW = 32 / L;  // row slots per warp
     constexpr int V = 32 / L;    // indices per lane per 32-edge chunk
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -528,7 +543,10 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                  u < a.hot_rows, pol_last, pol_first)
+                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                   : make_double2(0.0, 0.0);
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
@@ -556,6 +574,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     constexpr int RPW = 32 / L;
     constexpr int V = 32 / L;
     constexpr int HB = batch_hub_edges(B);
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const unsigned smask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
@@ -615,7 +634,10 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    val[q] = t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl) : make_double2(0.0, 0.0);
+                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                  u < a.hot_rows, pol_last, pol_first)
+                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                   : make_double2(0.0, 0.0);
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
