@@ -219,6 +219,14 @@ const double* gather_result(cpg_graph* g, size_t cols, cudaStream_t st) {
 }
 
 // The K fused steps of one query, chunk by chunk (last = write d*acc).
+// Single-source L2 residency split (CPG_HOT1_MB, default 0 = off): ids below
+// the budget are gathered evict_last, the rest evict_first.
+uint32_t single_hot_rows(const cpg_graph* g) {
+    const char* e = std::getenv("CPG_HOT1_MB");
+    if (!e) return 0;
+    return static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (static_cast<uint64_t>(std::atoll(e)) << 20) / 8));
+}
+
 uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
                    cudaStream_t st, StepProf* prof, bool taylor = false) {
     uint32_t launches = 0;
@@ -236,6 +244,7 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
         a.hub_count = g->hub_count;
         a.coeffs = g->d_coeffs;
         a.tile = g->tile;
+        a.hot_rows = single_hot_rows(g);
         a.k = static_cast<int>(k);
         a.first = k == 1;
         a.taylor = taylor;

@@ -69,6 +69,7 @@ struct StepArgs {
     uint32_t row0;         // global id of local row 0
     uint32_t n_items;
     int tile;              // kTileSmall or kTileLarge (must match the table)
+    uint32_t hot_rows;     // gathers of ids < hot_rows kept in L2 (evict_last); 0 = off
     int k;                 // computing w_k (1..K)
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
     int taylor;            // power method (PwMethod, solvers.cpp:87-116): w_k = D^-1 A w_{k-1}

@@ -81,6 +81,12 @@ __device__ __forceinline__ double2 ld_gather2(const double* p) {
 #endif
 }
 
+__device__ __forceinline__ double ld_gather_hot(const double* p, bool hot, uint64_t pol_last, uint64_t pol_first) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(hot ? pol_last : pol_first));
+    return v;
+}
+
 // Batched gathers with an L2 residency split: the degree-sorted hot prefix of
 // the iterate (rows < hot) is loaded evict_last, the cold tail evict_first.
 __device__ __forceinline__ double2 ld_gather2_hot(const double* p, bool hot, uint64_t pol_last, uint64_t pol_first) {
@@ -184,9 +190,19 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
         if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
     }
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int j = i * THREADS + threadIdx.x;
-        if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[i]);
+    if (a.hot_rows) {
+        const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = i * THREADS + threadIdx.x;
+            if (j < cnt) sm.vals[j] = ld_gather_hot(a.w_cur + idx[i], idx[i] < a.hot_rows, pol_last, pol_first);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = i * THREADS + threadIdx.x;
+            if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[i]);
+        }
     }
     __syncthreads();
 
