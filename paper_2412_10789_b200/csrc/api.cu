@@ -298,29 +298,6 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev
 }
 
 // One tile of up to B sources (q0 .. q0+count) through the batched step.
-// Column-sweep launches of one chunk (rows [t.sw_begin, t.sw_begin + t.n_sw)):
-// pacing counters zeroed, then one launch per batch of t.sw_cap rows.
-uint32_t run_sweep(cpg_graph* g, const ItemTable& t, const BatchArgs& b, int B, cudaStream_t st) {
-    if (!t.n_sw) return 0;
-    CPG_CUDA(cudaMemsetAsync(t.sw_cnt, 0, sizeof(unsigned int) * t.sw_launches * t.sw_nb, st));
-    static const int drift = [] {
-        const char* e = std::getenv("CPG_SWEEP_DRIFT");
-        return e ? std::max(1, std::min(2, std::atoi(e))) : 1;
-    }();
-    BatchArgs s = b;
-    s.sw_nb = t.sw_nb;
-    s.sw_drift = drift;
-    s.sw_end = t.sw_begin + t.n_sw;
-    for (uint32_t l = 0; l < t.sw_launches; ++l) {
-        s.sw_bnd = t.sw_bnd + static_cast<size_t>(l) * (t.sw_nb + 1) * t.sw_cap;
-        s.sw_cnt = t.sw_cnt + static_cast<size_t>(l) * t.sw_nb;
-        s.sw_first = t.sw_begin + l * t.sw_cap;
-        launch_batch_sweep(s, B, t.sw_grid, st);
-    }
-    (void)g;
-    return t.sw_launches;
-}
-
 uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
                    cudaStream_t st, StepProf* prof, const double* seeds_dev = nullptr, double gp_a = 0.0) {
     uint32_t launches = 0;
@@ -359,8 +336,6 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
             const ItemTable& t = g->btables[c];
             b.hub_items = t.items;
             b.n_hub_items = t.n_hub_items;
-            b.cb_meta = t.cb_meta;
-            b.cb_row_begin = t.row_begin;
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
@@ -379,7 +354,6 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                         launch_batch_pieces(h, static_cast<int>(B), hgrid, st);
                     ++launches;
                 }
-                launches += run_sweep(g, t, b, static_cast<int>(B), st);
                 if (t.row_end > b.hub_rows) {
                     launch_batch_rows(b, static_cast<int>(B), occ * g->sm_count, st);
                     ++launches;
@@ -387,11 +361,6 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                 if (prof) prof->after(st);
             } else {
                 const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
-                if (t.n_sw) {
-                    if (prof) prof->before(st);
-                    launches += run_sweep(g, t, b, static_cast<int>(B), st);
-                    if (prof) prof->after(st);
-                }
                 if (jobs) {
                     const int grid = occ * g->sm_count;
                     if (prof) prof->before(st);
@@ -676,8 +645,7 @@ int cpg_graph_destroy(cpg_graph* g) {
         if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
         for (auto& t : g->tables) cudaFree(t.items);
         for (auto& t : g->btables)
-            for (void* p : {(void*)t.items, (void*)t.cb_meta, (void*)t.sw_bnd, (void*)t.sw_cnt})
-                if (p) cudaFree(p);
+            if (t.items) cudaFree(t.items);
         for (auto e : g->chunk_ev)
             if (e) cudaEventDestroy(e);
         if (g->comm_stream) cudaStreamDestroy(g->comm_stream);

@@ -16,13 +16,6 @@ struct ItemTable {
     WorkItem* items = nullptr;
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0;
     uint32_t row_begin = 0, row_end = 0;
-    uint2* cb_meta = nullptr;      // batched: column-blocked hub rows [row_begin, row_begin + n_cb)
-    uint32_t n_cb = 0, n_cb_items = 0;
-    // batched column sweep: rows [sw_begin, sw_begin + n_sw) in launches of sw_cap rows
-    uint32_t* sw_bnd = nullptr;    // [launch][nb+1][sw_cap] relative bounds (kernel layout)
-    unsigned int* sw_cnt = nullptr; // [launch][nb] pacing counters
-    uint32_t sw_begin = 0, n_sw = 0, sw_cap = 0, sw_launches = 0, sw_nb = 0;
-    int sw_grid = 0;
 };
 } // namespace cpg
 
@@ -98,9 +91,6 @@ int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
 void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st);
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st);
-int sweep_grid(int B);
-int sweep_slots_per_cta(int B);
-void launch_batch_sweep(const BatchArgs& a, int B, int grid, cudaStream_t st);
 
 void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q, cudaStream_t st);

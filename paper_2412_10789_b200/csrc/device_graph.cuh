@@ -48,9 +48,6 @@ struct __align__(16) WorkItem {
     uint64_t c;
 };
 constexpr uint64_t kHubBit = 1ull << 63;
-// Column-blocked hub piece (batched step): b = the piece's own partial slot;
-// the row's {first slot, piece count} come from BatchArgs::cb_meta.
-constexpr uint64_t kCbBit = 1ull << 62;
 __host__ __device__ inline uint64_t tile_code(uint64_t e0, uint32_t cnt, uint32_t lg) {
     return e0 | (static_cast<uint64_t>(cnt) << 40) | (static_cast<uint64_t>(lg) << 54);
 }
@@ -84,8 +81,6 @@ struct BatchArgs {
     const uint32_t* col;
     const WorkItem* hub_items;  // hub pieces (row, partial slot base, first edge | count | hub bit)
     uint32_t n_hub_items;
-    const uint2* cb_meta = nullptr;  // column-blocked hub rows: {first partial slot, pieces}, by row - cb_row_begin
-    uint32_t cb_row_begin = 0;
     uint32_t hub_rows;          // rows [0, hub_rows) are hubs
     uint32_t n_loc;
     const double* w_cur;        // [n_pad][64]
@@ -98,15 +93,6 @@ struct BatchArgs {
     uint32_t row0;
     uint32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last); 0 = off
     int k, first, last;
-    // Column sweep (cheby_batch_sweep_kernel), one launch = one batch of rows:
-    const uint32_t* sw_bnd = nullptr;  // [nb+1][grid][slots/CTA][kSweepRows] block bounds, relative to rowptr[row]
-    unsigned int* sw_cnt = nullptr;    // [nb] pacing counters of this launch (zeroed before it)
-    uint32_t sw_first = 0, sw_end = 0; // local rows of this launch: sw_first + rank, < sw_end
-    uint32_t sw_nb = 0;                // column blocks
-    int sw_drift = 1;                  // CTAs may run this many blocks ahead of the slowest
 };
-
-// Rows per row slot in the column sweep (accumulators kept in registers).
-constexpr int kSweepRows = 4;
 
 } // namespace cpg

@@ -6,7 +6,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -334,242 +333,22 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
     CPG_CUDA(cudaGetLastError());
 }
 
-// Column blocks of the neighbour lists of the CB hubs (rows [row0, row0+n_cb)):
-// bnd[h*(nb+1)+b] = first edge of hub h whose column is >= b*S (sorted lists).
-__global__ void k_cb_bounds(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t n_cb, uint32_t S,
-                            uint32_t nb, int64_t* bnd) {
-    const uint64_t total = static_cast<uint64_t>(n_cb) * (nb + 1);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t h = static_cast<uint32_t>(i / (nb + 1)), b = static_cast<uint32_t>(i % (nb + 1));
-        int64_t lo = rowptr[row0 + h], hi = rowptr[row0 + h + 1];
-        const uint64_t key = static_cast<uint64_t>(b) * S;
-        while (lo < hi) {
-            const int64_t mid = lo + (hi - lo) / 2;
-            if (col[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        bnd[i] = lo;
-    }
-}
-
-// Column-blocked hub pieces for the largest hubs of [row0, row1): rows with
-// degree > thr are cut at column-block boundaries (blocks of S rows of the
-// B-wide iterate, sized to stay L2-resident) and each block segment into
-// pieces of <= hb edges.  Pieces are ordered block-major, so the warps in
-// flight gather from one window of the iterate at a time.  Returns the number
-// of CB rows; items/meta are allocated here (null when none).
-static uint32_t build_cb_items(const cpg_graph* g, uint32_t row0, uint32_t row1, int64_t thr, int64_t hb, uint32_t S,
-                        uint32_t slot_off, WorkItem** items_out, uint2** meta_out, uint32_t* n_items_out,
-                        uint32_t* n_slots_out, cudaStream_t st) {
-    *items_out = nullptr;
-    *meta_out = nullptr;
-    *n_items_out = *n_slots_out = 0;
-    const uint32_t n_rows = row1 - row0;
-    if (!n_rows) return 0;
-    unsigned int* d_cnt = dalloc<unsigned int>(1);
-    CPG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned int), st));
-    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(g->rowptr + row0, n_rows, thr, d_cnt);
-    unsigned int n_cb = 0;
-    CPG_CUDA(cudaMemcpyAsync(&n_cb, d_cnt, sizeof(n_cb), cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_cnt);
-    const uint32_t nb = static_cast<uint32_t>((static_cast<uint64_t>(g->n_pad) + S - 1) / S);
-    if (!n_cb || nb < 2) return 0;
-    const size_t nbnd = static_cast<size_t>(n_cb) * (nb + 1);
-    int64_t* d_bnd = dalloc<int64_t>(nbnd);
-    k_cb_bounds<<<grid_for(nbnd), kT, 0, st>>>(g->rowptr, g->col, row0, n_cb, S, nb, d_bnd);
-    std::vector<int64_t> bnd(nbnd);
-    CPG_CUDA(cudaMemcpyAsync(bnd.data(), d_bnd, sizeof(int64_t) * nbnd, cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_bnd);
-    // per hub: pieces per block, first slot, piece count
-    std::vector<uint32_t> first_piece(nbnd);  // piece index of (h, b) within hub h
-    std::vector<uint2> meta(n_cb);
-    uint32_t slots = slot_off;
-    uint64_t n_items = 0;
-    for (uint32_t h = 0; h < n_cb; ++h) {
-        const int64_t* bh = bnd.data() + static_cast<size_t>(h) * (nb + 1);
-        uint32_t p = 0;
-        for (uint32_t b = 0; b < nb; ++b) {
-            first_piece[static_cast<size_t>(h) * (nb + 1) + b] = p;
-            p += static_cast<uint32_t>((bh[b + 1] - bh[b] + hb - 1) / hb);
-        }
-        meta[h] = make_uint2(slots, p);
-        slots += p;
-        n_items += p;
-    }
-    if (n_items > 0xffffffffull) throw Error(CPG_ENOMEM, "column-blocked hub pieces overflow");
-    std::vector<WorkItem> items;
-    items.reserve(n_items);
-    for (uint32_t b = 0; b < nb; ++b)
-        for (uint32_t h = 0; h < n_cb; ++h) {
-            const size_t i = static_cast<size_t>(h) * (nb + 1) + b;
-            const int64_t e_begin = bnd[i], e_end = bnd[i + 1];
-            uint32_t slot = meta[h].x + first_piece[i];
-            for (int64_t e = e_begin; e < e_end; e += hb, ++slot) {
-                const uint32_t cnt = static_cast<uint32_t>(std::min<int64_t>(hb, e_end - e));
-                items.push_back(WorkItem{row0 + h, slot, tile_code(static_cast<uint64_t>(e), cnt, 0) | kHubBit | kCbBit});
-            }
-        }
-    WorkItem* d_items = dalloc<WorkItem>(items.size());
-    uint2* d_meta = dalloc<uint2>(n_cb);
-    CPG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(WorkItem) * items.size(), cudaMemcpyHostToDevice, st));
-    CPG_CUDA(cudaMemcpyAsync(d_meta, meta.data(), sizeof(uint2) * n_cb, cudaMemcpyHostToDevice, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    *items_out = d_items;
-    *meta_out = d_meta;
-    *n_items_out = static_cast<uint32_t>(items.size());
-    *n_slots_out = slots - slot_off;
-    if (std::getenv("CPG_CB_DEBUG")) {
-        const int64_t e0 = bnd[0], e1 = bnd[nbnd - 1];
-        std::fprintf(stderr, "[cpg] column-blocked hubs: rows %u (deg > %lld), blocks %u x %u rows, pieces %zu, edges %lld\n",
-                     n_cb, static_cast<long long>(thr), nb, S, items.size(), static_cast<long long>(e1 - e0));
-    }
-    return n_cb;
-}
-
-// Column-blocking parameters: CPG_CB_DEG (min degree, 0 = off), CPG_CB_MB
-// (window of the iterate, MB).
-static int64_t cb_min_degree() {
-    const char* e = std::getenv("CPG_CB_DEG");
-    return e ? std::atoll(e) : 32768;
-}
-static uint32_t cb_rows(int B) {
-    const char* e = std::getenv("CPG_CB_MB");
-    const double mb = e ? std::atof(e) : 48.0;
-    return static_cast<uint32_t>(std::max(1024.0, mb * 1048576.0 / (8.0 * B)));
-}
-
-// Sweep bounds: for row rank i of the sweep range (launch l = i / cap, rank j
-// in the launch) and block boundary b, the first edge of the row whose column
-// is >= b*S, relative to the row start.  Written at the kernel's position of
-// the row: j -> (p = j / (G*SL), slot sl, CTA snake(c)) as in
-// cheby_batch_sweep_kernel.
-__global__ void k_sweep_bounds(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t n_rows, uint32_t S,
-                               uint32_t nb, uint32_t G, uint32_t SL, uint32_t cap, uint32_t* out) {
-    const uint64_t total = static_cast<uint64_t>(n_rows) * (nb + 1);
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = static_cast<uint32_t>(x / (nb + 1)), b = static_cast<uint32_t>(x % (nb + 1));
-        const int64_t rs = rowptr[row0 + i], re = rowptr[row0 + i + 1];
-        int64_t lo = rs, hi = re;
-        const uint64_t key = static_cast<uint64_t>(b) * S;
-        if (b == nb) lo = re;
-        while (lo < hi) {
-            const int64_t mid = lo + (hi - lo) / 2;
-            if (col[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        const uint32_t l = i / cap, j = i % cap;
-        const uint32_t p = j / (G * SL), r = j % (G * SL);
-        const uint32_t sl = r / G, c = r % G;
-        const uint32_t cta = (sl & 1) ? G - 1 - c : c;
-        const size_t pos = ((static_cast<size_t>(l) * (nb + 1) + b) * G + cta) * SL * kSweepRows +
-                           static_cast<size_t>(sl) * kSweepRows + p;
-        out[pos] = static_cast<uint32_t>(lo - rs);
-    }
-}
-
-// Rows of [row0, row1) with degree > thr (a prefix: rows are degree-descending).
-static uint32_t count_prefix_above(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t thr, cudaStream_t st) {
-    const uint32_t n_rows = row1 - row0;
-    if (!n_rows) return 0;
-    unsigned int* d_cnt = dalloc<unsigned int>(1);
-    CPG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned int), st));
-    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, thr, d_cnt);
-    unsigned int n = 0;
-    CPG_CUDA(cudaMemcpyAsync(&n, d_cnt, sizeof(n), cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_cnt);
-    return n;
-}
-
-// Column-sweep setting: CPG_SWEEP=0/1 forces it off/on (default: on when the
-// B-wide iterate is >= 512 MB, i.e. far larger than L2); CPG_SWEEP_MB is the
-// column window (MB of the iterate), CPG_SWEEP_DEG the minimum degree.
-static bool sweep_enabled(const cpg_graph* g, int B) {
-    const char* e = std::getenv("CPG_SWEEP");
-    (void)g;
-    (void)B;
-    return e && e[0] != '0';
-}
-static uint32_t sweep_rows_per_block(int B) {
-    const char* e = std::getenv("CPG_SWEEP_MB");
-    const double mb = e ? std::atof(e) : 40.0;
-    return static_cast<uint32_t>(std::max(256.0, mb * 1048576.0 / (8.0 * B)));
-}
-static int64_t sweep_min_degree(int B) {
-    const char* e = std::getenv("CPG_SWEEP_DEG");
-    return e ? std::atoll(e) : batch_hub_edges(B);
-}
-
-static void build_sweep(const cpg_graph* g, ItemTable& t, uint32_t n_sw, int B, cudaStream_t st) {
-    t.n_sw = n_sw;
-    if (!n_sw) return;
-    const uint32_t S = sweep_rows_per_block(B);
-    t.sw_nb = static_cast<uint32_t>((static_cast<uint64_t>(g->n_pad) + S - 1) / S);
-    t.sw_grid = sweep_grid(B);
-    const uint32_t SL = static_cast<uint32_t>(sweep_slots_per_cta(B));
-    t.sw_cap = static_cast<uint32_t>(t.sw_grid) * SL * kSweepRows;
-    t.sw_launches = (n_sw + t.sw_cap - 1) / t.sw_cap;
-    const size_t n_bnd = static_cast<size_t>(t.sw_launches) * (t.sw_nb + 1) * t.sw_cap;
-    t.sw_bnd = dalloc<uint32_t>(n_bnd);
-    t.sw_cnt = dalloc<unsigned int>(static_cast<size_t>(t.sw_launches) * t.sw_nb);
-    CPG_CUDA(cudaMemsetAsync(t.sw_bnd, 0, sizeof(uint32_t) * n_bnd, st));
-    k_sweep_bounds<<<grid_for(static_cast<uint64_t>(n_sw) * (t.sw_nb + 1)), kT, 0, st>>>(
-        g->rowptr, g->col, t.sw_begin, n_sw, S, t.sw_nb, static_cast<uint32_t>(t.sw_grid), SL, t.sw_cap, t.sw_bnd);
-    CPG_CUDA(cudaStreamSynchronize(st));
-    if (std::getenv("CPG_CB_DEBUG"))
-        std::fprintf(stderr, "[cpg] column sweep: rows %u, blocks %u x %u rows, grid %d, %u launches of %u rows\n",
-                     n_sw, t.sw_nb, S, t.sw_grid, t.sw_launches, t.sw_cap);
-}
-
 void ensure_batch_tables(cpg_graph* g, int B) {
     if (!g->btables.empty() && g->bitems_width == B) return;
     for (auto& t : g->btables)
-        for (void* p : {(void*)t.items, (void*)t.cb_meta, (void*)t.sw_bnd, (void*)t.sw_cnt})
-            if (p) cudaFree(p);
+        if (t.items) cudaFree(t.items);
     g->btables.clear();
     uint32_t slots = 0;
     const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
     const int64_t hb = batch_hub_edges(B);
-    const int64_t cb_deg = cb_min_degree();
     for (uint32_t c = 0; c < C; ++c) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
-        WorkItem* cb_items = nullptr;
-        uint32_t cb_slots = 0;
-        if (cb_deg > 0)
-            t.n_cb = build_cb_items(g, t.row_begin, t.row_end, std::max<int64_t>(cb_deg - 1, hb), hb, cb_rows(B), slots,
-                                    &cb_items, &t.cb_meta, &t.n_cb_items, &cb_slots, g->stream);
-        slots += cb_slots;
-        t.sw_begin = t.row_begin + t.n_cb;
-        if (sweep_enabled(g, B))
-            build_sweep(g, t,
-                        count_prefix_above(g->rowptr, t.sw_begin, t.row_end,
-                                           std::max<int64_t>(sweep_min_degree(B), 0), g->stream),
-                        B, g->stream);
-        WorkItem* rest = nullptr;
-        uint32_t n_rest_hubs = 0, n_rest_items = 0;
-        build_hub_items(g->rowptr, t.sw_begin + t.n_sw, t.row_end, hb, hb, slots, &rest, &n_rest_hubs,
-                        &n_rest_items, 0, g->stream);
-        slots += n_rest_items;
-        t.n_hubs = t.n_cb + t.n_sw + n_rest_hubs;
-        t.n_hub_items = t.n_cb_items + n_rest_items;
-        if (t.n_cb_items) {
-            t.items = dalloc<WorkItem>(t.n_hub_items);
-            CPG_CUDA(cudaMemcpyAsync(t.items, cb_items, sizeof(WorkItem) * t.n_cb_items, cudaMemcpyDeviceToDevice,
-                                     g->stream));
-            if (n_rest_items)
-                CPG_CUDA(cudaMemcpyAsync(t.items + t.n_cb_items, rest, sizeof(WorkItem) * n_rest_items,
-                                         cudaMemcpyDeviceToDevice, g->stream));
-            CPG_CUDA(cudaStreamSynchronize(g->stream));
-            cudaFree(cb_items);
-            cudaFree(rest);
-        } else {
-            t.items = rest;
-        }
+        build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0,
+                        g->stream);
         t.n_items = t.n_hub_items;
+        slots += t.n_hub_items;
         g->btables.push_back(t);
     }
     g->n_bpartials = slots;

@@ -345,22 +345,15 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
         const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + job);
         j.hub = true;
         j.r = raw.x;
+        j.slot = raw.y;
         const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
         j.e0 = code_e0(c);
         j.e1 = j.e0 + code_cnt(c);
         const int64_t rs = a.rowptr[j.r], re = a.rowptr[j.r + 1];
         j.d = re - rs;
-        if (c & kCbBit) {  // column-blocked piece: own slot in the item, row meta in cb_meta
-            const uint2 m = a.cb_meta[j.r - a.cb_row_begin];
-            j.slot = m.x;
-            j.piece = raw.y - m.x;
-            j.P = m.y;
-        } else {
-            constexpr int HB = batch_hub_edges(B);
-            j.slot = raw.y;
-            j.piece = static_cast<uint32_t>((j.e0 - rs) / HB);
-            j.P = static_cast<uint32_t>((j.d + HB - 1) / HB);
-        }
+        constexpr int HB = batch_hub_edges(B);
+        j.piece = static_cast<uint32_t>((j.e0 - rs) / HB);
+        j.P = static_cast<uint32_t>((j.d + HB - 1) / HB);
     } else {
         j.r = a.hub_rows + (job - a.n_hub_items);
         j.e0 = a.rowptr[j.r];
@@ -606,8 +599,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     const uint32_t n_jobs = a.n_hub_items;
     const uint32_t stride = nw * RPW;
     uint32_t job = wg * RPW + slot;
-    // sb: partial slot base (plain piece) or the piece's own slot (column-blocked, cb = true)
-    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& sb, int64_t& e0, int64_t& e1, bool& cb) {
+    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& sb, int64_t& e0, int64_t& e1) {
         if (jb < n_jobs) {
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + jb);
             const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
@@ -615,11 +607,9 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             sb = raw.y;
             e0 = code_e0(c);
             e1 = e0 + code_cnt(c);
-            cb = (c & kCbBit) != 0;
         } else {
             r = sb = 0;
             e0 = e1 = 0;
-            cb = false;
         }
     };
     uint32_t c[V], cn[V];
@@ -633,14 +623,12 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     };
     uint32_t r, sb;
     int64_t e0, e1;
-    bool cb;
-    load_item(job, r, sb, e0, e1, cb);
+    load_item(job, r, sb, e0, e1);
     load_chunk(c, e0, e1);
     while (__any_sync(0xffffffffu, job < n_jobs)) {
         uint32_t nr, nsb;
         int64_t ne0, ne1;
-        bool ncb;
-        load_item(job + stride, nr, nsb, ne0, ne1, ncb);  // in flight during this piece
+        load_item(job + stride, nr, nsb, ne0, ne1);  // in flight during this piece
         int64_t rs = 0, re = 0;
         if (job < n_jobs) {
             rs = a.rowptr[r];
@@ -677,19 +665,9 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         load_chunk(c, ne0, ne1);  // next piece's first chunk
         const bool live = job < n_jobs;
         const int64_t d = re - rs;
-        uint32_t P = 0, own = 0;
-        if (live) {
-            if (cb) {  // column-blocked piece: own slot given, row meta = {first slot, pieces}
-                const uint2 m = a.cb_meta[r - a.cb_row_begin];
-                own = sb;
-                sb = m.x;
-                P = m.y;
-            } else {
-                P = static_cast<uint32_t>((d + HB - 1) / HB);
-                own = sb + static_cast<uint32_t>((e0 - rs) / HB);
-            }
-            reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(own) * B)[cl] = s;
-        }
+        const uint32_t P = live ? static_cast<uint32_t>((d + HB - 1) / HB) : 0u;
+        const uint32_t piece = live ? static_cast<uint32_t>((e0 - rs) / HB) : 0u;
+        if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[cl] = s;
         __threadfence();
         __syncwarp();
         unsigned prev = 0;
@@ -715,122 +693,6 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         sb = nsb;
         e0 = ne0;
         e1 = ne1;
-        cb = ncb;
-    }
-}
-
-// Column sweep over the mid-degree hub rows (batched step).
-//
-// A launch owns one batch of rows: every row slot (B/2 lanes) of every CTA
-// holds kSweepRows rows with their B-wide sums in registers.  The columns are
-// cut into blocks of S iterate rows sized to stay L2-resident; all CTAs sweep
-// the blocks in order, summing for each of their rows the neighbours that fall
-// in the current block (the per-row neighbour lists are sorted, so each block
-// is a contiguous segment; bounds precomputed in sw_bnd).  A pacing counter
-// per block keeps every CTA within sw_drift blocks of the slowest, so the
-// gathers of the whole GPU hit one window of the iterate at a time and are
-// served from L2 instead of HBM.  The pacing is a locality device only: the
-// sums do not depend on it (a bounded spin falls through).  Each row is summed
-// in edge order, then the usual fused epilogue runs once after the last block.
-template <int B, int U = 8, int MINB = 2>
-__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_sweep_kernel(const BatchArgs a) {
-    constexpr int L = B / 2;
-    constexpr int RPW = 32 / L;
-    constexpr int V = 32 / L;
-    constexpr int NW = kBatchThreads / 32;
-    constexpr int SL = NW * RPW;  // row slots per CTA
-    constexpr int RPS = kSweepRows;
-    static_assert(RPS == 4, "bounds are loaded as one uint4");
-    __shared__ unsigned int warps_done[4];
-    if (threadIdx.x < 4) warps_done[threadIdx.x] = 0u;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slot = lane / L, cl = lane % L;
-    const uint32_t G = gridDim.x, cta = blockIdx.x;
-    const uint32_t sl = warp * RPW + slot;
-    const uint32_t cc = (sl & 1) ? G - 1 - cta : cta;  // snake: balance degree ranks over CTAs
-    const uint32_t row_base = a.sw_first + sl * G + cc;  // row p = row_base + p * G * SL
-    const size_t stride = static_cast<size_t>(G) * SL * RPS;
-    const uint32_t* bnd = a.sw_bnd + (static_cast<size_t>(cta) * SL + sl) * RPS;
-    int64_t cur[RPS];  // absolute first edge of the row's next segment
-    double2 acc[RPS];
-#pragma unroll
-    for (int p = 0; p < RPS; ++p) {
-        const uint32_t r = row_base + static_cast<uint32_t>(p) * G * SL;
-        cur[p] = r < a.sw_end ? a.rowptr[r] : 0;
-        acc[p] = make_double2(0.0, 0.0);
-    }
-    uint4 lo4 = make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t drift = static_cast<uint32_t>(a.sw_drift);
-    for (uint32_t b = 0; b < a.sw_nb; ++b) {
-        if (b >= drift) {  // pacing: wait until every CTA finished block b - drift
-            if (lane == 0) {
-                const volatile unsigned int* f = a.sw_cnt + (b - drift);
-                for (int it = 0; *f < G && it < (1 << 16); ++it) __nanosleep(100);
-            }
-            __syncwarp();
-        }
-        const uint4 h4 = __ldg(reinterpret_cast<const uint4*>(bnd + static_cast<size_t>(b + 1) * stride));
-        // segment p covers positions [o_p, o_{p+1}) of the concatenated block list
-        const uint32_t o1 = h4.x - lo4.x, o2 = o1 + (h4.y - lo4.y), o3 = o2 + (h4.z - lo4.z);
-        const uint32_t m = o3 + (h4.w - lo4.w);
-        const int64_t s0 = cur[0], s1 = cur[1] - o1, s2 = cur[2] - o2, s3 = cur[3] - o3;
-        for (uint32_t e = 0; __any_sync(0xffffffffu, e < m); e += 32) {
-            uint32_t c[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const uint32_t pos = e + static_cast<uint32_t>(v * L + cl);
-                const int64_t ad = pos < o1 ? s0 + pos : pos < o2 ? s1 + pos : pos < o3 ? s2 + pos : s3 + pos;
-                c[v] = pos < m ? ld_index(a.col + ad) : 0u;
-            }
-#pragma unroll
-            for (int t0 = 0; t0 < 32; t0 += U) {
-                if (!__any_sync(0xffffffffu, e + t0 < m)) break;
-                double2 val[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int t = t0 + q;
-                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    val[q] = e + t < m ? ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl)
-                                       : make_double2(0.0, 0.0);
-                }
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const uint32_t pos = e + static_cast<uint32_t>(t0 + q);
-                    if (pos >= m) break;
-                    const int p = (pos >= o1) + (pos >= o2) + (pos >= o3);
-#pragma unroll
-                    for (int k = 0; k < RPS; ++k)
-                        if (p == k) {
-                            acc[k].x += val[q].x;
-                            acc[k].y += val[q].y;
-                        }
-                }
-            }
-        }
-        cur[0] += h4.x - lo4.x;
-        cur[1] += h4.y - lo4.y;
-        cur[2] += h4.z - lo4.z;
-        cur[3] += h4.w - lo4.w;
-        lo4 = h4;
-        __syncwarp();
-        if (lane == 0) {  // the CTA's last warp through block b signals it
-            const unsigned prev = atomicAdd(&warps_done[b & 3], 1u);
-            if (prev == NW - 1) {
-                warps_done[b & 3] = 0u;
-                atomicAdd(a.sw_cnt + b, 1u);
-            }
-        }
-    }
-#pragma unroll
-    for (int p = 0; p < RPS; ++p) {
-        const uint32_t r = row_base + static_cast<uint32_t>(p) * G * SL;
-        if (r < a.sw_end) {
-            const int64_t d = a.rowptr[r + 1] - a.rowptr[r];
-            double2 wp, ac;
-            batch_prefetch<B>(a, r, cl, wp, ac);
-            batch_epilogue<B>(a, r, acc[p], d, cl, wp, ac);
-        }
     }
 }
 
@@ -983,43 +845,6 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
     default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
     }
 }
-// Sweep kernel variant: CPG_SWEEP_CFG = U*10 + MINB (B = 16 tuning hook; default 82).
-static int sweep_cfg() {
-    static const int cfg = [] {
-        const char* e = std::getenv("CPG_SWEEP_CFG");
-        return e ? std::atoi(e) : 82;
-    }();
-    return cfg;
-}
-using BatchKernelFn = void (*)(const BatchArgs);
-static BatchKernelFn sweep_fn(int B) {
-    switch (B) {
-    case 4: return cheby_batch_sweep_kernel<4>;
-    case 8: return cheby_batch_sweep_kernel<8>;
-    case 16:
-        switch (sweep_cfg()) {
-        case 43: return cheby_batch_sweep_kernel<16, 4, 3>;
-        case 83: return cheby_batch_sweep_kernel<16, 8, 3>;
-        case 42: return cheby_batch_sweep_kernel<16, 4, 2>;
-        default: return cheby_batch_sweep_kernel<16>;
-        }
-    case 32: return cheby_batch_sweep_kernel<32>;
-    default: return cheby_batch_sweep_kernel<64>;
-    }
-}
-// Resident CTAs of the sweep kernel (the launch grid; the bounds layout depends on it).
-int sweep_grid(int B) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_fn(B), kBatchThreads, 0);
-    return std::max(1, occ) * sms;
-}
-int sweep_slots_per_cta(int B) { return (kBatchThreads / 32) * (64 / B); }
-void launch_batch_sweep(const BatchArgs& a, int B, int grid, cudaStream_t st) {
-    sweep_fn(B)<<<grid, kBatchThreads, 0, st>>>(a);
-}
-
 // Split path: hub pieces through cheby_batch_kernel, then plain rows through
 // cheby_batch_rows_kernel.  Faster on every graph with >= 8M local edges
 // (profiles/r01/batch_split_ab.txt); tiny graphs keep the single fused launch.

@@ -479,72 +479,3 @@ def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
     for j, s in enumerate(src):
         want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
         assert_parity(got[j], want)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("split", ["0", "1"])
-@pytest.mark.parametrize("tile", [4, 16, 64])
-def test_batched_column_blocked_hubs(cpg, gpu, split, tile, monkeypatch):
-    """Column-blocked hub pieces (big hubs cut at column-block boundaries, pieces
-    ordered block-major, combined through per-row slot metadata) forced on a
-    mid-size graph with a tiny column window, against the reference."""
-    monkeypatch.setenv("CPG_BATCH_SPLIT", split)
-    monkeypatch.setenv("CPG_CB_DEG", "300")
-    monkeypatch.setenv("CPG_CB_MB", "0.01")  # 1024-row blocks -> ~49 blocks
-    off, nb = cpg.gen_chunglu(50000, 600000, 2.0, 24.0, 15000, seed=12)
-    g = cpg.Graph.from_csr(off, nb)
-    ref = _ref_graph(off, nb)
-    src = ref.select_sources_uniform(min(tile, 9), 6)
-    kern = cpg.Kernel.ppr(0.2)
-    got, _ = cpg.cheby_power_many(g, kern, src, 26, batched=True, tile=tile)
-    for j, s in enumerate(src):
-        want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
-        assert_parity(got[j], want)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("split", ["0", "1"])
-@pytest.mark.parametrize("tile", [4, 16, 64])
-@pytest.mark.parametrize("cb", ["0", "300"])
-def test_batched_column_sweep(cpg, gpu, split, tile, cb, monkeypatch):
-    """Column sweep of the hub rows (rows held in registers per slot, column
-    blocks swept in paced order, several row batches per step) forced on a
-    mid-size graph with tiny column blocks, with and without column-blocked
-    pieces for the largest hubs, against the reference."""
-    monkeypatch.setenv("CPG_BATCH_SPLIT", split)
-    monkeypatch.setenv("CPG_SWEEP", "1")
-    monkeypatch.setenv("CPG_SWEEP_MB", "0.001")  # 256-row blocks
-    monkeypatch.setenv("CPG_SWEEP_DEG", "4")     # most rows swept -> several launches
-    monkeypatch.setenv("CPG_CB_DEG", cb)
-    monkeypatch.setenv("CPG_CB_MB", "0.01")
-    off, nb = cpg.gen_chunglu(60000, 700000, 2.0, 24.0, 15000, seed=13)
-    g = cpg.Graph.from_csr(off, nb)
-    ref = _ref_graph(off, nb)
-    src = ref.select_sources_uniform(min(tile, 9), 7)
-    kern = cpg.Kernel.ppr(0.2)
-    got, _ = cpg.cheby_power_many(g, kern, src, 26, batched=True, tile=tile)
-    for j, s in enumerate(src):
-        want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
-        assert_parity(got[j], want)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("chunks", ["1", "3"])
-def test_batched_column_sweep_chunked_hkpr(cpg, gpu, chunks, monkeypatch):
-    """Column sweep per chunk of the chunked layout, HKPR, B = 16."""
-    from oracle import Port
-
-    monkeypatch.setenv("CPG_CHUNKS", chunks)
-    monkeypatch.setenv("CPG_SWEEP", "1")
-    monkeypatch.setenv("CPG_SWEEP_MB", "0.002")
-    monkeypatch.setenv("CPG_SWEEP_DEG", "16")
-    off, nb = cpg.gen_chunglu(40000, 400000, 2.1, 20.0, 9000, seed=8)
-    dg = cpg.DeviceGraph.from_host(off, nb, 0)
-    k = cpg.Kernel.hkpr(5.0)
-    c = k.cheby_coeffs(15)
-    src = [0, 3, 20000, len(off) - 2]
-    got, st = cpg.cheby_power_many(dg, k, src, 15, batched=True, tile=16)
-    for j, s in enumerate(src):
-        want, _, _ = Port.cheby_power(off, nb, c, 15, s)
-        assert_parity(got[j], want)
-    assert st.mass_err_max <= 1e-9
