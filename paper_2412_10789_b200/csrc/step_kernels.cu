@@ -312,168 +312,6 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
-// Software-pipelined variant: the index stream of the CTA's NEXT item is
-// loaded into registers at the start of the current item, so its DRAM latency
-// overlaps this item's gathers, sums and epilogue (the same next-job prefetch
-// that sped up the batched kernels).  Hub pieces stage their gathers through
-// shared memory like tiles, to leave registers for the prefetch buffer.
-constexpr int kStepPF = kHubPieceEdges / kStepThreads;  // 16 indices per thread
-
-template <int THREADS>
-__device__ __forceinline__ void load_item_indices(const StepArgs& a, const WorkItem& it, bool valid,
-                                                  uint32_t (&idx)[kStepPF]) {
-    const int64_t e0 = code_e0(it.c);
-    const int cnt = valid ? code_cnt(it.c) : 0;
-#pragma unroll
-    for (int i = 0; i < kStepPF; ++i) {
-        const int j = i * THREADS + threadIdx.x;
-        idx[i] = j < cnt ? ld_index(a.col + e0 + j) : 0u;
-    }
-}
-
-template <int THREADS, int TILE>
-__device__ __forceinline__ void process_tile_pf(const StepArgs& a, const WorkItem it, const uint32_t (&idx)[kStepPF],
-                                                TileSmem<TILE>& sm, double& mass) {
-    constexpr int PER = TILE / THREADS;
-    constexpr int RPT = kTileMaxRows / THREADS;
-    const uint32_t rb = it.a;
-    const int nrows = static_cast<int>(it.b - it.a);
-    const int64_t e0 = code_e0(it.c);
-    const int cnt = code_cnt(it.c);
-    const int lg = static_cast<int>((it.c >> 54) & 7);
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int j = i * THREADS + threadIdx.x;
-        if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[i]);
-    }
-    for (int j = threadIdx.x; j <= nrows; j += THREADS) sm.rp[j] = static_cast<int>(a.rowptr[rb + j] - e0);
-    double w_prev[RPT], acc_old[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = q * THREADS + threadIdx.x;
-        if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
-    }
-    __syncthreads();
-    const int g = 1 << lg;
-    const int sub = threadIdx.x & (g - 1);
-    const int grp = threadIdx.x >> lg;
-    const int ngrp = THREADS >> lg;
-    for (int base = 0; base < nrows; base += ngrp) {
-        const int r = base + grp;
-        double s = 0.0;
-        if (r < nrows) {
-            const int b1 = sm.rp[r + 1];
-            for (int j = sm.rp[r] + sub; j < b1; j += g) s += sm.vals[j];
-        }
-        for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (r < nrows && sub == 0) sm.ysum[r] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = q * THREADS + threadIdx.x;
-        if (r < nrows)
-            step_epilogue(a, rb + r, sm.ysum[r], sm.rp[r + 1] - sm.rp[r], w_prev[q], acc_old[q], mass);
-    }
-    __syncthreads();
-}
-
-template <int THREADS, int TILE>
-__device__ __forceinline__ void process_hub_pf(const StepArgs& a, const WorkItem it, const uint32_t (&idx)[kStepPF],
-                                               TileSmem<TILE>& sm, double* red, int* flag, double& mass) {
-    const uint32_t r = it.a, slot_base = it.b, hub = it.a;
-    const int64_t p0 = code_e0(it.c);
-    const int cnt = code_cnt(it.c);
-    const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1];
-    const int64_t d = re - rs;
-    const uint32_t piece = static_cast<uint32_t>((p0 - rs) / kHubPieceEdges);
-    const uint32_t P = static_cast<uint32_t>((d + kHubPieceEdges - 1) / kHubPieceEdges);
-    // gathers in flight, summed in index order per thread (same order as process_hub)
-    double s = 0.0;
-    constexpr int H = 8;  // gathers per batch
-#pragma unroll
-    for (int i0 = 0; i0 < kStepPF; i0 += H) {
-        double v[H];
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-            const int j = (i0 + i) * THREADS + threadIdx.x;
-            v[i] = j < cnt ? ld_gather(a.w_cur + idx[i0 + i]) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < H; ++i) s += v[i];
-    }
-    s = block_sum<THREADS>(s, red);
-    (void)sm;
-    if (P == 1) {
-        if (threadIdx.x == 0) {
-            double wp, ao;
-            load_prev(a, r, wp, ao);
-            step_epilogue(a, r, s, d, wp, ao, mass);
-        }
-        return;
-    }
-    if (threadIdx.x == 0) {
-        a.hub_partial[slot_base + piece] = s;
-        __threadfence();
-        const unsigned prev = atomicAdd(&a.hub_count[hub], 1u);
-        *flag = (prev == P - 1);
-    }
-    __syncthreads();
-    if (*flag && threadIdx.x < 32) {
-        __threadfence();
-        double y = 0.0;
-        for (uint32_t p = threadIdx.x; p < P; p += 32) y += __ldcg(a.hub_partial + slot_base + p);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-        if (threadIdx.x == 0) {
-            a.hub_count[hub] = 0u;
-            double wp, ao;
-            load_prev(a, r, wp, ao);
-            step_epilogue(a, r, y, d, wp, ao, mass);
-        }
-    }
-    __syncthreads();
-}
-
-template <int THREADS, int TILE, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) cheby_step_pf_kernel(const StepArgs a) {
-    __shared__ TileSmem<TILE> sm;
-    __shared__ double red[THREADS / 32];
-    __shared__ int flag;
-    double mass = 0.0;
-    auto load_item = [&](uint32_t i) {
-        WorkItem it;
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
-        it.a = raw.x;
-        it.b = raw.y;
-        it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        return it;
-    };
-    uint32_t i = blockIdx.x;
-    uint32_t idx[kStepPF];
-    WorkItem it{0u, 0u, 0ull};
-    if (i < a.n_items) it = load_item(i);
-    load_item_indices<THREADS>(a, it, i < a.n_items, idx);
-    while (i < a.n_items) {
-        const uint32_t ni = i + gridDim.x;
-        const bool has_next = ni < a.n_items;
-        WorkItem nit{0u, 0u, 0ull};
-        if (has_next) nit = load_item(ni);
-        uint32_t nidx[kStepPF];
-        load_item_indices<THREADS>(a, nit, has_next, nidx);  // in flight during this item
-        if (it.c & kHubBit)
-            process_hub_pf<THREADS, TILE>(a, it, idx, sm, red, &flag, mass);
-        else
-            process_tile_pf<THREADS, TILE>(a, it, idx, sm, mass);
-#pragma unroll
-        for (int k = 0; k < kStepPF; ++k) idx[k] = nidx[k];
-        it = nit;
-        i = ni;
-    }
-    mass = block_sum<THREADS>(mass, red);
-    if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
-}
-
 // ---------------------------------------------------------------------------
 // Batched step: B sources per tile (B in {4,8,16,32,64}), iterates row-major
 // [n_pad][B] fp64.  A row is owned by a lane sub-group of L = B/2 lanes (one
@@ -951,22 +789,7 @@ __global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, d
 }
 
 // Host-side launch wrappers ---------------------------------------------------
-// CPG_STEP_PF=1 selects the software-pipelined step (A/B hook).
-static bool step_pf() {
-    static const bool on = [] {
-        const char* e = std::getenv("CPG_STEP_PF");
-        return e && e[0] != '0';
-    }();
-    return on;
-}
 void launch_step(const StepArgs& a, int grid, cudaStream_t st) {
-    if (step_pf()) {
-        if (a.tile == kTileLarge)
-            cheby_step_pf_kernel<kStepThreads, kTileLarge, 3><<<grid, kStepThreads, 0, st>>>(a);
-        else
-            cheby_step_pf_kernel<kStepThreads, kTileSmall, 3><<<grid, kStepThreads, 0, st>>>(a);
-        return;
-    }
     if (a.tile == kTileLarge)
         cheby_step_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a);
     else
@@ -974,15 +797,6 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st) {
 }
 int step_occupancy(int tile) {
     int blocks = 0;
-    if (step_pf()) {
-        if (tile == kTileLarge)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_pf_kernel<kStepThreads, kTileLarge, 3>,
-                                                          kStepThreads, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_pf_kernel<kStepThreads, kTileSmall, 3>,
-                                                          kStepThreads, 0);
-        return blocks;
-    }
     if (tile == kTileLarge)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileLarge>,
                                                       kStepThreads, 0);
