@@ -389,7 +389,11 @@ def run_ours(args, cfg):
         P._check(L.cpg_chebypower(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), None, ctypes.byref(s)))
     L.cpg_set_profiling(0)
     launches_per_step = int(s.launches)  # kernels the library launched for one step (its own count)
-    bytes_launch = dg.bytes_per_step(tile if batched else 1)
+    # one timed launch = one step of a source tile (batched) or of a query group (single-source:
+    # several queries per launch on small graphs), so scale the per-step bytes by the steps it ran
+    units = (-(-len(sources) // tile) if batched else len(sources)) * K
+    steps_per_launch = units / max(1, s.step_launches)
+    bytes_launch = dg.bytes_per_step(tile if batched else 1) * steps_per_launch
     per_launch_ms = max_over_ranks(s.step_ms / max(1, s.step_launches))
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
@@ -452,7 +456,7 @@ def run_ours(args, cfg):
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full, per step)",
                          "kernel": ("cheby_batch_kernel (hub pieces) + cheby_batch_rows_kernel, timed as one step"
                                     if batched else "cheby_step_kernel"),
-                         "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms,
+                         "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms, "steps_per_launch": steps_per_launch,
                          "step_share_of_device_time": step_share},
             "e2e": {"value": e2e_gteps, "unit": "GTEPS",
                     "h2d_bytes_per_step": int(src_np.nbytes + c_np.nbytes),

@@ -144,13 +144,47 @@ void ensure_ws(cpg_graph* g, size_t cols) {
     g->ws_cols = cols;
 }
 
+// Mass-partial columns per (step, chunk) of a query group of Q queries: the
+// launch grid of the group (single queries keep the per-graph step_grid).
+uint32_t mass_cols(const cpg_graph* g, uint32_t Q) {
+    if (Q <= 1) return static_cast<uint32_t>(g->step_grid);
+    return static_cast<uint32_t>(std::max(1, step_occupancy(g->tile)) * g->sm_count);
+}
+
+// Per-query device state for a group of Q single-source queries: hub partial
+// slots and tickets, and the mass arrays.
+void ensure_group(cpg_graph* g, uint32_t K, uint32_t Q) {
+    if (g->hub_q < Q) {
+        dfree(g->hub_partial);
+        cudaFree(g->hub_count);
+        g->hub_partial = dalloc<double>(static_cast<size_t>(g->n_partials) * Q);
+        g->hub_count = dalloc<unsigned int>(static_cast<size_t>(g->n_loc) * Q);
+        CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<size_t>(1, static_cast<size_t>(g->n_loc) * Q)));
+        g->hub_q = Q;
+    }
+    const size_t need = static_cast<size_t>(K) * g->chunks * mass_cols(g, Q) * Q;
+    if (g->mass_cap < need) {
+        dfree(g->d_mass_partial);
+        g->d_mass_partial = dalloc<double>(need);
+        g->mass_cap = need;
+    }
+    if (g->step_mass_cap < static_cast<size_t>(K) * Q) {
+        dfree(g->d_step_mass);
+        g->d_step_mass = dalloc<double>(static_cast<size_t>(K) * Q);
+        g->step_mass_cap = static_cast<size_t>(K) * Q;
+    }
+}
+
 void ensure_params(cpg_graph* g, uint32_t K, uint32_t n_sources) {
     if (g->coeff_cap < K + 1) {
         dfree(g->d_coeffs);
-        dfree(g->d_step_mass);
         g->d_coeffs = dalloc<double>(K + 1);
-        g->d_step_mass = dalloc<double>(K + 1);
         g->coeff_cap = K + 1;
+    }
+    if (g->step_mass_cap < K + 1) {
+        dfree(g->d_step_mass);
+        g->d_step_mass = dalloc<double>(K + 1);
+        g->step_mass_cap = K + 1;
     }
     if (g->src_cap < n_sources) {
         dfree(g->d_sources);
@@ -228,10 +262,11 @@ uint32_t single_hot_rows(const cpg_graph* g) {
 }
 
 uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
-                   cudaStream_t st, StepProf* prof, bool taylor = false) {
+                   cudaStream_t st, StepProf* prof, bool taylor = false, uint32_t Q = 1) {
     uint32_t launches = 0;
     const int occ = std::max(1, step_occupancy(g->tile));
     const uint32_t C = static_cast<uint32_t>(g->chunks);
+    const uint32_t MG = mass_cols(g, Q);
     for (uint32_t k = k_first; k <= k_last; ++k) {
         StepArgs a;
         a.rowptr = g->rowptr;
@@ -249,17 +284,24 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
         a.first = k == 1;
         a.taylor = taylor;
         a.last = last_writes_out && k == K;
+        StepGroup gq;
+        gq.nq = Q;
+        gq.vec_stride = g->n_pad;
+        gq.acc_stride = g->n_loc;
+        gq.part_stride = g->n_partials;
+        gq.cnt_stride = g->n_loc;
+        gq.mass_stride = K * C * MG;
         if (k > 1) wait_gathers(g, st);
         for (uint32_t c = 0; c < C; ++c) {
             const ItemTable& t = g->tables[c];
             a.items = t.items;
             a.n_items = t.n_items;
             a.row0 = chunk_row0(g, c);
-            a.mass_partial = g->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * g->step_grid;
+            a.mass_partial = g->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * MG;
             if (t.n_items) {
-                const int grid = table_grid(g, t.n_items, occ);
+                const int grid = table_grid(g, t.n_items * Q, occ);
                 if (prof) prof->before(st);
-                launch_step(a, grid, st);
+                launch_step(a, grid, st, &gq);
                 if (prof) prof->after(st);
                 ++launches;
             }
@@ -270,27 +312,30 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
     return launches;
 }
 
-// One single-source (or dense-seed, when seed_dev != null) query; result
-// d*acc unpermuted into d_dst[n] (caller ids) if non-null.
-uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q, const double* seed_dev, double mass0, double* d_dst,
-                    cudaStream_t st, StepProf* prof, bool taylor = false, double gp_a = 0.0) {
+// A group of Q single-source queries (sources q0 .. q0+Q-1) in one launch per
+// step, or one dense-seed query (seed_dev != null, Q = 1); results d*acc
+// unpermuted into d_dst[Q][n] (caller ids) if non-null.
+uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t Q, const double* seed_dev, double mass0,
+                    double* d_dst, cudaStream_t st, StepProf* prof, bool taylor = false, double gp_a = 0.0) {
     uint32_t launches = 0;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
-    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad, st));
-    CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * C * g->step_grid, st));
+    ensure_group(g, K, Q);
+    const size_t mstride = static_cast<size_t>(K) * C * mass_cols(g, Q);
+    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * Q, st));
+    CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * mstride * Q, st));
     if (seed_dev)
         launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, gp_a, st);
     else
-        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q, st);
+        launch_init_onehot(g->w_a, g->n_pad, g->gdeg, g->new_of_old, g->d_sources, q0, Q, st);
     ++launches;
-    launches += run_steps(g, 1, K, K, true, st, prof, taylor);
-    launch_mass_steps(g->d_mass_partial, C * g->step_grid, K, g->d_step_mass, st);
+    launches += run_steps(g, 1, K, K, true, st, prof, taylor, Q);
+    launch_mass_steps(g->d_mass_partial, C * mass_cols(g, Q), mstride, K, Q, g->d_step_mass, st);
     ++launches;
     if (g->nccl_comm) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
-    launch_mass_err(g->d_step_mass, K, mass0, g->d_mass_err, st);
+    launch_mass_err(g->d_step_mass, K * Q, mass0, g->d_mass_err, st);
     ++launches;
     if (d_dst) {
-        launch_unpermute(d_dst, gather_result(g, 1, st), g->new_of_old, g->n, g->gdeg, gp_a, st);
+        launch_unpermute(d_dst, gather_result(g, 1, st), g->n_loc, g->new_of_old, g->n, Q, g->gdeg, gp_a, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -409,6 +454,26 @@ void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, do
 // Shared driver for host / device outputs.  mode 0 = one-hot single source,
 // 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources,
 // 3 = power method (Taylor), 4 = batched dense seed columns (general_gp_matrix).
+// Single-source queries per launch: enough to give every resident CTA several
+// work items when the graph alone cannot (small graphs are latency-bound at
+// one query per launch), capped at 16 and by a 2 GB workspace.  One rank only
+// (the all-gathers move one iterate).  CPG_GROUP_Q overrides (tests).
+uint32_t single_group(const cpg_graph* g, uint32_t nq) {
+    if (nq <= 1 || g->nccl_comm) return 1;
+    uint32_t Q;
+    if (const char* e = std::getenv("CPG_GROUP_Q")) {
+        Q = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+    } else {
+        // measured: config 1 (0.95 M edges) best at 16, config 2 (2.1 M) at 8, config 3 (86 M) at 1
+        Q = static_cast<uint32_t>(std::min<uint64_t>(16, std::max<uint64_t>(1, (16ull << 20) / std::max<uint64_t>(1, g->nnz_loc))));
+        const uint64_t bytes_per_q = 8ull * (2ull * g->n_pad + g->n_loc);
+        Q = static_cast<uint32_t>(std::min<uint64_t>(Q, std::max<uint64_t>(1, (2ull << 30) / bytes_per_q)));
+    }
+    Q = std::max(1u, std::min(Q, nq));
+    const uint32_t groups = (nq + Q - 1) / Q;  // balance the group sizes (no ragged tail group)
+    return (nq + groups - 1) / groups;
+}
+
 int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
           uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
           cpg_stats* stats, double gp_a = 0.0) {
@@ -450,10 +515,10 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
                 CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
             }
         }
-        ensure_ws(g, cols);
+        const uint32_t per = batched ? tile : (mode == 0 || mode == 3) ? single_group(g, nq) : 1;
+        ensure_ws(g, batched ? cols : per);
         upload_params(g, coeffs, K, sources, dense ? 0 : nq, st);
         const size_t n = g->n;
-        const uint32_t per = batched ? tile : 1;
         const uint32_t nbatches = (nq + per - 1) / per;
         const size_t slot = n * per;  // doubles per result slot
         double* seed_dev = nullptr;
@@ -473,13 +538,13 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
                 CPG_CUDA(cudaStreamWaitEvent(st, g->ev[b & 1], 0));  // slot free (copy of b-2 done)
             }
             if (mode == 0 || mode == 3) {
-                launches += run_single(g, K, q0, nullptr, 1.0, dst, st, prof.get(), mode == 3);
+                launches += run_single(g, K, q0, count, nullptr, 1.0, dst, st, prof.get(), mode == 3);
             } else if (mode == 1) {
                 const double* sh = seeds_host + static_cast<size_t>(q0) * n;
                 double mass0 = 0.0;  // sum of the D^a-scaled seed: the conserved mass
                 for (size_t v = 0; v < n; ++v) mass0 += sh[v];
                 CPG_CUDA(cudaMemcpyAsync(seed_dev, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-                launches += run_single(g, K, q0, seed_dev, gp_a == 0.0 ? mass0 : std::nan(""), dst, st, prof.get(),
+                launches += run_single(g, K, q0, 1, seed_dev, gp_a == 0.0 ? mass0 : std::nan(""), dst, st, prof.get(),
                                        false, gp_a);
             } else if (mode == 4) {
                 CPG_CUDA(cudaMemcpyAsync(seed_dev, seeds_host + static_cast<size_t>(q0) * n,
@@ -786,7 +851,7 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
             if (est_trace) est_trace[v] = v == source ? coeffs[0] : 0.0;
         }
         CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * np, st));
-        launch_init_onehot(g->w_a, g->gdeg, g->new_of_old, g->d_sources, 0, st);
+        launch_init_onehot(g->w_a, g->n_pad, g->gdeg, g->new_of_old, g->d_sources, 0, 1, st);
         CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * g->chunks * g->step_grid, st));
         for (uint32_t k = 1; k <= K; ++k) {
             run_steps(g, k, k, K, false, st, nullptr);

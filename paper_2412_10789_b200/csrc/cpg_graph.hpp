@@ -41,7 +41,8 @@ struct cpg_graph {
     size_t bhub_items_cap = 0;
 
     double* hub_partial = nullptr;  // [n_partials]
-    unsigned int* hub_count = nullptr;  // [n_loc], indexed by local row
+    unsigned int* hub_count = nullptr;  // [hub_q][n_loc], indexed by local row
+    uint32_t hub_q = 1;                 // query-group capacity of hub_partial / hub_count
     double* bhub_partial = nullptr; // [n_bpartials][B]
     unsigned int* bhub_count = nullptr; // [n_loc]
 
@@ -65,7 +66,8 @@ struct cpg_graph {
     double* d_mass_partial = nullptr;
     size_t mass_cap = 0;
     double* d_mass_err = nullptr;   // [2]: running max, scratch
-    double* d_step_mass = nullptr;  // [coeff_cap]
+    double* d_step_mass = nullptr;  // [step_mass_cap]
+    size_t step_mass_cap = 0;
     double* d_stage = nullptr;      // device result staging for host output (2 slots)
     size_t stage_cap = 0;           // doubles per slot
     // ev[0..1]: slot copied out; ev[2..3]: slot computed; ev[4]: caller-stream join
@@ -84,7 +86,7 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
                            int64_t piece, uint32_t slot_off, cudaStream_t st);
 
 // step_kernels.cu
-void launch_step(const StepArgs& a, int grid, cudaStream_t st);
+void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr);
 int step_occupancy(int tile);
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
 int batch_occupancy();
@@ -92,19 +94,20 @@ bool batch_split(uint64_t nnz_loc);
 void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st);
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st);
 
-void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                        uint32_t q, cudaStream_t st);
+void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                        uint32_t q0, uint32_t count, cudaStream_t st);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                               uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st);
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
                        uint32_t n, double a, cudaStream_t st);
 void launch_init_dense_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const double* X, uint32_t n,
                              uint32_t count, uint32_t B, double a, cudaStream_t st);
-void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, const uint32_t* gdeg,
-                      double a, cudaStream_t st);
+void launch_unpermute(double* out, const double* full, uint64_t stride, const uint32_t* no, uint32_t n,
+                      uint32_t count, const uint32_t* gdeg, double a, cudaStream_t st);
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
                             uint32_t count, uint32_t B, const uint32_t* gdeg, double a, cudaStream_t st);
-void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st);
+void launch_mass_steps(const double* mp, uint32_t n_part, uint64_t q_stride, uint32_t K, uint32_t count,
+                       double* steps, cudaStream_t st);
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
 
 // topk.cu

@@ -76,6 +76,18 @@ struct StepArgs {
     int last;              // write out = d * acc instead of acc
 };
 
+// Query group (cheby_step_group_kernel): nq single-source queries in one
+// launch; query q uses the slices w + q*vec_stride, acc/out + q*acc_stride,
+// hub_partial + q*part_stride, hub_count + q*cnt_stride, mass_partial +
+// q*mass_stride of the StepArgs arrays.  (A separate parameter block, so the
+// one-query kernel's StepArgs and its code are unchanged.)
+struct StepGroup {
+    uint32_t nq;
+    uint64_t vec_stride, acc_stride;
+    uint32_t part_stride, cnt_stride, mass_stride;
+};
+
+
 struct BatchArgs {
     const int64_t* rowptr;
     const uint32_t* col;

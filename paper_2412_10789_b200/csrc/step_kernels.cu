@@ -189,7 +189,6 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
         const int r = q * THREADS + threadIdx.x;
         if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
     }
-#pragma unroll
     if (a.hot_rows) {
         const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
 #pragma unroll
@@ -310,6 +309,51 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
+}
+
+// Query group: nq single-source queries per launch (small graphs, where one
+// query cannot fill the GPU).  Items x queries: job x = q * n_items + i, so a
+// CTA's queries are nondecreasing and its mass partial is flushed once per
+// query it touched.  The one-query launch keeps cheby_step_kernel: sharing its
+// code measured 2.6% slower on config 3 (instruction schedule).
+template <int THREADS, int TILE>
+__global__ void __launch_bounds__(THREADS) cheby_step_group_kernel(const StepArgs a, const StepGroup gq) {
+    __shared__ TileSmem<TILE> sm;
+    __shared__ double red[THREADS / 32];
+    __shared__ int flag;
+    double mass = 0.0;
+    const uint32_t total = a.n_items * gq.nq;
+    uint32_t q_cur = 0u;
+    for (uint32_t x = blockIdx.x; x < total; x += gridDim.x) {
+        WorkItem it;
+        const uint32_t q = x / a.n_items;
+        const uint32_t i = x - q * a.n_items;
+        if (q != q_cur) {  // CTA-uniform
+            mass = block_sum<THREADS>(mass, red);
+            if (threadIdx.x == 0) a.mass_partial[static_cast<size_t>(q_cur) * gq.mass_stride + blockIdx.x] = mass;
+            mass = 0.0;
+            q_cur = q;
+        }
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
+        it.a = raw.x;
+        it.b = raw.y;
+        it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        {  // the query's slices
+            StepArgs aq = a;
+            aq.w_cur = a.w_cur + q_cur * gq.vec_stride;
+            aq.w_io = a.w_io + q_cur * gq.vec_stride;
+            aq.acc = a.acc + q_cur * gq.acc_stride;
+            aq.out = a.out + q_cur * gq.acc_stride;
+            aq.hub_partial = a.hub_partial + static_cast<size_t>(q_cur) * gq.part_stride;
+            aq.hub_count = a.hub_count + static_cast<size_t>(q_cur) * gq.cnt_stride;
+            if (it.c & kHubBit)
+                process_hub<THREADS>(aq, it, red, &flag, mass);
+            else
+                process_tile<THREADS, TILE>(aq, it, sm, mass);
+        }
+    }
+    mass = block_sum<THREADS>(mass, red);
+    if (threadIdx.x == 0) a.mass_partial[static_cast<size_t>(q_cur) * gq.mass_stride + blockIdx.x] = mass;
 }
 
 // ---------------------------------------------------------------------------
@@ -701,10 +745,13 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
 // ---------------------------------------------------------------------------
 
 // w_0 = D^-1 e_s in the global (relabelled) ids; vector pre-zeroed.
-__global__ void init_onehot_kernel(double* w, const uint32_t* gdeg, const uint32_t* new_of_old,
-                                   const uint32_t* sources, uint32_t q) {
-    const uint32_t s = new_of_old[sources[q]];
-    w[s] = 1.0 / static_cast<double>(gdeg[s]);
+// Query group: thread t seeds slice t (w + t*stride) for source q0 + t.
+__global__ void init_onehot_kernel(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* new_of_old,
+                                   const uint32_t* sources, uint32_t q0, uint32_t count) {
+    const uint32_t t = threadIdx.x;
+    if (t >= count) return;
+    const uint32_t s = new_of_old[sources[q0 + t]];
+    w[t * stride + s] = 1.0 / static_cast<double>(gdeg[s]);
 }
 
 // Batched: column j of W_0 = D^-1 e_{s_j}; matrix [n_pad][B] pre-zeroed.
@@ -745,11 +792,16 @@ __global__ void init_dense_batch_kernel(double* W, const uint32_t* gdeg, const u
 
 // out[v] = d_v^-a full[new_of_old[v]]  (back to the caller's ids; a != 0 only
 // for general_gp_vector, solvers.cpp:400-401).
-__global__ void unpermute_kernel(double* out, const double* full, const uint32_t* new_of_old, uint32_t n,
-                                 const uint32_t* gdeg, double a) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+// out[q][v] = full[q*stride + new_of_old[v]] for the count queries of a group.
+__global__ void unpermute_kernel(double* out, const double* full, uint64_t stride, const uint32_t* new_of_old,
+                                 uint32_t n, uint32_t count, const uint32_t* gdeg, double a) {
+    const uint64_t total = static_cast<uint64_t>(n) * count;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t q = static_cast<uint32_t>(i / n), v = static_cast<uint32_t>(i - static_cast<uint64_t>(q) * n);
         const uint32_t s = new_of_old[v];
-        out[v] = a == 0.0 ? full[s] : pow(static_cast<double>(gdeg[s]), -a) * full[s];
+        const double y = full[q * stride + s];
+        out[i] = a == 0.0 ? y : pow(static_cast<double>(gdeg[s]), -a) * y;
     }
 }
 
@@ -772,13 +824,16 @@ __global__ void unpermute_batch_kernel(double* out, const double* full, const ui
 }
 
 // steps[k] = sum_b mass_partial[k][b]  (ordered, one CTA per step).
-__global__ void mass_steps_kernel(const double* mass_partial, uint32_t n_part, double* steps) {
+// (query group: blockIdx.y = q, partials at q*q_stride, steps at q*K)
+__global__ void mass_steps_kernel(const double* mass_partial, uint32_t n_part, uint64_t q_stride, double* steps,
+                                  uint32_t K) {
     __shared__ double red[kStepThreads / 32];
-    const uint32_t k = blockIdx.x;
+    const uint32_t k = blockIdx.x, q = blockIdx.y;
+    const double* mp = mass_partial + q * q_stride;
     double s = 0.0;
-    for (uint32_t b = threadIdx.x; b < n_part; b += blockDim.x) s += mass_partial[static_cast<size_t>(k) * n_part + b];
+    for (uint32_t b = threadIdx.x; b < n_part; b += blockDim.x) s += mp[static_cast<size_t>(k) * n_part + b];
     s = block_sum<kStepThreads>(s, red);
-    if (threadIdx.x == 0) steps[k] = s;
+    if (threadIdx.x == 0) steps[static_cast<size_t>(q) * K + k] = s;
 }
 
 // err = max(err, max_k |steps[k] - mass0|).
@@ -786,22 +841,30 @@ __global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, d
     double worst = *err;
     for (uint32_t k = 0; k < K; ++k) worst = fmax(worst, fabs(steps[k] - mass0));
     *err = worst;
-}
+}  // (over all K*count entries of a query group: called with K*count)
 
 // Host-side launch wrappers ---------------------------------------------------
-void launch_step(const StepArgs& a, int grid, cudaStream_t st) {
-    if (a.tile == kTileLarge)
-        cheby_step_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a);
-    else
-        cheby_step_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a);
+void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq) {
+    const bool group = gq && gq->nq > 1;
+    if (a.tile == kTileLarge) {
+        if (group)
+            cheby_step_group_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a, *gq);
+        else
+            cheby_step_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a);
+    } else {
+        if (group)
+            cheby_step_group_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a, *gq);
+        else
+            cheby_step_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a);
+    }
 }
-int step_occupancy(int tile) {
+int step_occupancy(int tile) {  // same for both instances (64 registers, same shared memory)
     int blocks = 0;
     if (tile == kTileLarge)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileLarge>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_group_kernel<kStepThreads, kTileLarge>,
                                                       kStepThreads, 0);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_kernel<kStepThreads, kTileSmall>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_group_kernel<kStepThreads, kTileSmall>,
                                                       kStepThreads, 0);
     return blocks;
 }
@@ -913,9 +976,9 @@ int batch_occupancy() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel<64>, kBatchThreads, 0);
     return blocks;
 }
-void launch_init_onehot(double* w, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                        uint32_t q, cudaStream_t st) {
-    init_onehot_kernel<<<1, 1, 0, st>>>(w, gdeg, no, src, q);
+void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
+                        uint32_t q0, uint32_t count, cudaStream_t st) {
+    init_onehot_kernel<<<1, 32, 0, st>>>(w, stride, gdeg, no, src, q0, count);
 }
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                               uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st) {
@@ -929,16 +992,17 @@ void launch_init_dense_batch(double* W, const uint32_t* gdeg, const uint32_t* no
                              uint32_t count, uint32_t B, double a, cudaStream_t st) {
     init_dense_batch_kernel<<<2368, 256, 0, st>>>(W, gdeg, no, X, n, count, B, a);
 }
-void launch_unpermute(double* out, const double* full, const uint32_t* no, uint32_t n, const uint32_t* gdeg,
-                      double a, cudaStream_t st) {
-    unpermute_kernel<<<1184, 256, 0, st>>>(out, full, no, n, gdeg, a);
+void launch_unpermute(double* out, const double* full, uint64_t stride, const uint32_t* no, uint32_t n,
+                      uint32_t count, const uint32_t* gdeg, double a, cudaStream_t st) {
+    unpermute_kernel<<<1184, 256, 0, st>>>(out, full, stride, no, n, count, gdeg, a);
 }
 void launch_unpermute_batch(double* out, const double* full, const uint32_t* no, uint32_t n,
                             uint32_t count, uint32_t B, const uint32_t* gdeg, double a, cudaStream_t st) {
     unpermute_batch_kernel<<<2368, 256, 0, st>>>(out, full, no, n, count, B, gdeg, a);
 }
-void launch_mass_steps(const double* mp, uint32_t n_part, uint32_t K, double* steps, cudaStream_t st) {
-    mass_steps_kernel<<<K, kStepThreads, 0, st>>>(mp, n_part, steps);
+void launch_mass_steps(const double* mp, uint32_t n_part, uint64_t q_stride, uint32_t K, uint32_t count,
+                       double* steps, cudaStream_t st) {
+    mass_steps_kernel<<<dim3(K, count), kStepThreads, 0, st>>>(mp, n_part, q_stride, steps, K);
 }
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st) {
     mass_err_kernel<<<1, 1, 0, st>>>(steps, K, mass0, err);

@@ -479,3 +479,25 @@ def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
     for j, s in enumerate(src):
         want, _, _ = ref.cheby_power(PPR, 0.2, int(s), 26)
         assert_parity(got[j], want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("group", ["1", "3", "16"])
+def test_single_source_query_groups(cpg, gpu, group, monkeypatch):
+    """Query groups of the single-source step (several queries per launch, each
+    with its own iterate slices, hub partial slots and tickets, and mass
+    partials), on a graph with multi-piece hubs: PPR and HKPR against the
+    reference, and the mass check."""
+    monkeypatch.setenv("CPG_GROUP_Q", group)
+    off, nb = cpg.gen_chunglu(30000, 500000, 2.0, 30.0, 12000, seed=21)
+    assert np.diff(off).max() > 4096  # hubs split into several pieces
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    src = ref.select_sources_uniform(19, 3)  # 19 = groups of 16 + 3 (ragged tail)
+    for fam, param, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15)):
+        kern = cpg.Kernel.ppr(param) if fam == PPR else cpg.Kernel.hkpr(param)
+        got, st = cpg.cheby_power_many(g, kern, src, K)
+        assert st.mass_err_max <= 1e-9
+        for j, s in enumerate(src):
+            want, _, _ = ref.cheby_power(fam, param, int(s), K)
+            assert_parity(got[j], want)
