@@ -83,6 +83,9 @@ typedef struct {
     uint32_t max_degree;
     int rank, nranks, device;
     uint64_t structure_hash; /* FNV-1a of (n, m, offsets, neighbors), graph.cpp:97-102 */
+    int chunks;            /* row chunks per rank (one all-gather each)      */
+    int fused_allgather;   /* 1: batched steps store rows into every rank's replica
+                              (CPG_P2P=1, NCCL symmetric windows); 0: NCCL all-gather */
 } cpg_graph_info;
 
 const char* cpg_last_error(void);

@@ -29,6 +29,21 @@ HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp"
     os.path.join(INCLUDE, "cpg.h")]
 
 
+def _nccl_device_include():
+    """Include dir of an NCCL with the device API (nccl_device.h): the pip
+    nvidia-nccl package torch loads at run time.  None if absent."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        inc = os.path.join(d, "include")
+        if os.path.exists(os.path.join(inc, "nccl_device.h")):
+            return inc
+    return None
+
+
 def _sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
@@ -45,6 +60,9 @@ def _compile(src: str) -> tuple[str, str]:
     if not _stale(obj, src):
         return obj, ""
     flags = COMMON + (CU_FLAGS if src.endswith(".cu") else ARCH + ["-x", "cu"] if False else [])
+    if os.path.basename(src) == "nccl_sym.cu":
+        inc = _nccl_device_include()
+        flags = flags + ([f"-I{inc}", "-DCPG_NCCL_DEVICE_API=1"] if inc else ["-DCPG_NCCL_DEVICE_API=0"])
     cmd = [NVCC] + flags + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC] + COMMON + ["-c", src, "-o", obj]

@@ -30,7 +30,7 @@ class cpg_graph_info(ctypes.Structure):
     _fields_ = [("n", c_uint32), ("nnz", c_uint64), ("n_local", c_uint32), ("nnz_local", c_uint64),
                 ("row_begin", c_uint32), ("n_padded", c_uint32), ("n_hubs", c_uint32),
                 ("n_items", c_uint32), ("max_degree", c_uint32), ("rank", c_int), ("nranks", c_int),
-                ("device", c_int), ("structure_hash", c_uint64)]
+                ("device", c_int), ("structure_hash", c_uint64), ("chunks", c_int), ("fused_allgather", c_int)]
 
 
 _u64p = POINTER(c_uint64)

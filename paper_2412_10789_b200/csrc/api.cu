@@ -95,12 +95,12 @@ int table_grid(const cpg_graph* g, uint32_t n_items, int occ) {
 }
 
 cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t n, uint64_t nnz, int device,
-                         int rank, int nranks) {
+                         int rank, int nranks, int chunks = 0) {
     auto g = std::make_unique<cpg_graph>();
     g->device = device;
     g->rank = rank;
     g->nranks = nranks;
-    g->chunks = default_chunks(nranks);
+    g->chunks = chunks > 0 ? chunks : default_chunks(nranks);
     g->n = n;
     g->nnz = nnz;
     CPG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
@@ -129,14 +129,50 @@ uint32_t batch_width(uint32_t tile) {
     return B;
 }
 
+// The replicated iterates as NCCL symmetric windows (p2p graphs; collective:
+// every rank calls this in the same order with the same size).
+void free_iterates(cpg_graph* g) {
+    if (g->p2p) {
+        nccl_sym_deregister(g->nccl_comm, g->win_a);
+        nccl_sym_deregister(g->nccl_comm, g->win_b);
+        nccl_sym_free(g->w_a);
+        nccl_sym_free(g->w_b);
+        g->win_a = g->win_b = nullptr;
+        g->w_a = g->w_b = nullptr;
+    } else {
+        dfree(g->w_a);
+        dfree(g->w_b);
+    }
+}
+
+void alloc_iterates(cpg_graph* g, size_t cols) {
+    const size_t bytes = sizeof(double) * g->n_pad * cols;
+    if (!g->p2p) {
+        g->w_a = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+        g->w_b = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+        return;
+    }
+    g->w_a = static_cast<double*>(nccl_sym_alloc(bytes));
+    g->w_b = static_cast<double*>(nccl_sym_alloc(bytes));
+    g->win_a = nccl_sym_register(g->nccl_comm, g->w_a, bytes);
+    g->win_b = nccl_sym_register(g->nccl_comm, g->w_b, bytes);
+    if (!g->d_peers_a) {
+        g->d_peers_a = dalloc<double*>(static_cast<size_t>(g->nranks));
+        g->d_peers_b = dalloc<double*>(static_cast<size_t>(g->nranks));
+        g->d_barrier = dalloc<double>(1);
+        CPG_CUDA(cudaMemset(g->d_barrier, 0, sizeof(double)));
+    }
+    nccl_sym_peer_ptrs(g->win_a, g->nranks, g->d_peers_a, g->stream);
+    nccl_sym_peer_ptrs(g->win_b, g->nranks, g->d_peers_b, g->stream);
+    CPG_CUDA(cudaStreamSynchronize(g->stream));
+}
+
 void ensure_ws(cpg_graph* g, size_t cols) {
     if (g->ws_cols == cols) return;
-    dfree(g->w_a);
-    dfree(g->w_b);
+    free_iterates(g);
     dfree(g->acc);
     dfree(g->full);
-    g->w_a = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
-    g->w_b = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    alloc_iterates(g, cols);
     g->acc = dalloc<double>(static_cast<size_t>(g->n_loc) * cols);
     if (g->nccl_comm) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
     CPG_CUDA(cudaMemset(g->w_a, 0, sizeof(double) * g->n_pad * cols));
@@ -376,7 +412,15 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.k = static_cast<int>(k);
         b.first = k == 1;
         b.last = k == K;
-        if (k > 1) wait_gathers(g, st);
+        PeerArgs peer_args{nullptr, 0, 0};
+        const PeerArgs* pa = nullptr;
+        if (g->p2p) {  // fused all-gather: the epilogue stores into every replica
+            peer_args.peer_io = (k & 1) ? g->d_peers_b : g->d_peers_a;
+            peer_args.n_peer = g->nranks;
+            peer_args.self = g->p2p_self ? -1 : g->rank;
+            pa = &peer_args;
+        }
+        if (k > 1 && !g->p2p) wait_gathers(g, st);
         for (uint32_t c = 0; c < C; ++c) {
             const ItemTable& t = g->btables[c];
             b.hub_items = t.items;
@@ -394,13 +438,13 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
                         1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
                     if (std::getenv("CPG_PIECES_FUSED"))  // A/B hook: hub pieces through the fused kernel
-                        launch_batch(h, static_cast<int>(B), hgrid, st);
+                        launch_batch(h, static_cast<int>(B), hgrid, st, pa);
                     else
-                        launch_batch_pieces(h, static_cast<int>(B), hgrid, st);
+                        launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
                     ++launches;
                 }
                 if (t.row_end > b.hub_rows) {
-                    launch_batch_rows(b, static_cast<int>(B), occ * g->sm_count, st);
+                    launch_batch_rows(b, static_cast<int>(B), occ * g->sm_count, st, pa);
                     ++launches;
                 }
                 if (prof) prof->after(st);
@@ -409,15 +453,17 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                 if (jobs) {
                     const int grid = occ * g->sm_count;
                     if (prof) prof->before(st);
-                    launch_batch(b, static_cast<int>(B), grid, st);
+                    launch_batch(b, static_cast<int>(B), grid, st, pa);
                     if (prof) prof->after(st);
                     ++launches;
                 }
             }
-            gather_chunk(g, b.w_io, c, cols, st);
+            if (!g->p2p) gather_chunk(g, b.w_io, c, cols, st);
         }
+        // iteration barrier: every rank's rows of w_k are in every replica before step k+1
+        if (g->p2p) nccl_allreduce_sum_f64(g->d_barrier, g->d_barrier, 1, g->nccl_comm, st);
     }
-    wait_gathers(g, st);
+    if (!g->p2p) wait_gathers(g, st);
     if (d_dst) {
         launch_unpermute_batch(d_dst, gather_result(g, cols, st), g->new_of_old, g->n, count, B, g->gdeg, gp_a, st);
         ++launches;
@@ -667,11 +713,23 @@ int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors,
             d_nbr = t_nbr;
         }
         cpg_graph* g = nullptr;
+        void* comm = nullptr;
         try {
-            g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks);
             // NCCL whenever an id is given (also for one rank: exercises the collective path)
-            if (nccl_unique_id) g->nccl_comm = nccl_comm_init(nccl_unique_id, nranks, rank);
+            if (nccl_unique_id) comm = nccl_comm_init(nccl_unique_id, nranks, rank);
+            // CPG_P2P=1: fused all-gather through NCCL symmetric windows when the
+            // NCCL in the process has the device API and all ranks share one
+            // NVLink domain (one chunk: no separate collective to overlap)
+            const char* pe = std::getenv("CPG_P2P");
+            const bool p2p = comm && pe && pe[0] == '1' && nccl_sym_supported(comm, nranks);
+            g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks,
+                              p2p && !std::getenv("CPG_CHUNKS") ? 1 : 0);
+            g->nccl_comm = comm;
+            comm = nullptr;
+            g->p2p = p2p;
+            if (const char* ps = std::getenv("CPG_P2P_SELF")) g->p2p_self = ps[0] == '1';
         } catch (...) {
+            if (comm) nccl_comm_destroy(comm);
             if (t_off) cudaFree(t_off);
             if (t_nbr) cudaFree(t_nbr);
             if (g) cpg_graph_destroy(g);
@@ -699,6 +757,8 @@ int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info) {
         info->nranks = g->nranks;
         info->device = g->device;
         info->structure_hash = g->hash;
+        info->chunks = g->chunks;
+        info->fused_allgather = g->p2p ? 1 : 0;
     });
 }
 
@@ -707,6 +767,11 @@ int cpg_graph_destroy(cpg_graph* g) {
     return guarded([&] {
         DeviceGuard dg(g->device);
         cudaDeviceSynchronize();
+        if (g->p2p) {  // windows are deregistered through the communicator, before it goes
+            free_iterates(g);
+            for (void* p : {(void*)g->d_peers_a, (void*)g->d_peers_b, (void*)g->d_barrier})
+                if (p) cudaFree(p);
+        }
         if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
         for (auto& t : g->tables) cudaFree(t.items);
         for (auto& t : g->btables)

@@ -74,6 +74,16 @@ struct cpg_graph {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     void* nccl_comm = nullptr;      // ncclComm_t when sharded
+    // Fused all-gather (CPG_P2P=1 on a sharded graph): w_a / w_b are NCCL
+    // symmetric windows and the batched epilogue stores each computed row into
+    // every rank's replica through the LSA peer pointers.
+    bool p2p = false;
+    int p2p_self = 0;               // test hook: also store through this rank's own LSA alias
+    void* win_a = nullptr;
+    void* win_b = nullptr;
+    double** d_peers_a = nullptr;   // [nranks] peer pointers of w_a's window
+    double** d_peers_b = nullptr;
+    double* d_barrier = nullptr;    // one-element all-reduce per iteration (the barrier)
     std::mutex mu;                  // one query at a time per handle
 };
 
@@ -88,11 +98,11 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr);
 int step_occupancy(int tile);
-void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st);
+void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
 int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
-void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st);
-void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st);
+void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
+void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
 
 void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q0, uint32_t count, cudaStream_t st);
@@ -119,5 +129,12 @@ void* nccl_comm_init(const void* id128, int nranks, int rank);
 void nccl_allgather_f64(const double* send, double* recv, size_t count, void* comm, cudaStream_t st);
 void nccl_allreduce_sum_f64(const double* send, double* recv, size_t count, void* comm, cudaStream_t st);
 void nccl_comm_destroy(void* comm);
+// nccl_sym.cu (NCCL symmetric windows; see there)
+bool nccl_sym_supported(void* comm, int nranks);
+void* nccl_sym_alloc(size_t bytes);
+void nccl_sym_free(void* p);
+void* nccl_sym_register(void* comm, void* buf, size_t bytes);
+void nccl_sym_deregister(void* comm, void* win);
+void nccl_sym_peer_ptrs(void* win, int n, double** d_out, cudaStream_t st);
 
 } // namespace cpg

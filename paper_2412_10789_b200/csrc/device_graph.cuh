@@ -107,4 +107,12 @@ struct BatchArgs {
     int k, first, last;
 };
 
+// Fused all-gather (second parameter of the PEER instances of the batched
+// kernels): w_io's row also goes to peer_io[p] for p in [0, n_peer), p != self.
+// A separate block keeps BatchArgs, and the code of the plain instances, as is.
+struct PeerArgs {
+    double* const* peer_io;     // device array of the ranks' w_io replicas (LSA pointers)
+    int n_peer, self;
+};
+
 } // namespace cpg

@@ -407,9 +407,9 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
     return j;
 }
 
-template <int B>
-__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, double2 y, int64_t d, int cl,
-                                               double2 wp, double2 ac) {
+template <int B, bool PEER = false>
+__device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArgs& pa, uint32_t r, double2 y,
+                                               int64_t d, int cl, double2 wp, double2 ac) {
     const uint32_t gr = a.row0 + r;
     double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
     if (d > 0) {
@@ -428,6 +428,10 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, uint32_t r, d
         }
     }
     reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl] = w_new;
+    if (PEER) {  // fused all-gather: the row into every other rank's replica (NVLink stores)
+        for (int p = 0; p < pa.n_peer; ++p)
+            if (p != pa.self) reinterpret_cast<double2*>(pa.peer_io[p] + static_cast<size_t>(gr) * B)[cl] = w_new;
+    }
     if (a.last) {
         const double dd = static_cast<double>(d);
         reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * B)[cl] = make_double2(dd * acc_new.x, dd * acc_new.y);
@@ -450,8 +454,8 @@ __device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, i
 
 // Occupancy over registers: 4 CTAs x 8 warps per SM (64 regs) measured best
 // for B = 16 and 64 (profiles/r01/slot_sweep.txt), even with small spills.
-template <int B, int U = 8, int MINB = 4>
-__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const BatchArgs a) {
+template <int B, int U = 8, int MINB = 4, bool PEER = false>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;      // lanes per row slot
     constexpr int RPW = 32 / L;   // row slots per warp
     constexpr int V = 32 / L;     // indices per lane per 32-edge chunk
@@ -533,16 +537,17 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             }
         }
         (void)smask;
-        if (do_epi) batch_epilogue<B>(a, j.r, y, j.d, cl, wp, ac);
+        if (do_epi) batch_epilogue<B, PEER>(a, pa, j.r, y, j.d, cl, wp, ac);
     }
+    if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
 }
 
 // Plain-row batched step (rows [hub_rows, n_loc) of the chunk; hub pieces run
 // in cheby_batch_kernel first).  Without the hub path the kernel fits more
 // warps, and the next row's range and first index chunk are prefetched while
 // the current row's gathers and epilogue are in flight.
-template <int B, int U = 8, int MINB = 4>
-__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(const BatchArgs a) {
+template <int B, int U = 8, int MINB = 4, bool PEER = false>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;     // lanes per row slot
     constexpr int RPW = 32 / L;  // row slots per warp
     constexpr int V = 32 / L;    // indices per lane per 32-edge chunk
@@ -616,11 +621,12 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
             }
         }
         load_chunk(ne0, ne1);  // next row's first chunk, overlapping this epilogue
-        if (r < r_end) batch_epilogue<B>(a, r, s, e1 - e0, cl, wp, ac);
+        if (r < r_end) batch_epilogue<B, PEER>(a, pa, r, s, e1 - e0, cl, wp, ac);
         r = rn;
         e0 = ne0;
         e1 = ne1;
     }
+    if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
 }
 
 // Hub-piece batched step (split path): the jobs are the hub pieces of the
@@ -628,8 +634,8 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
 // piece's item and first index chunk are prefetched while the current piece's
 // gathers are in flight (as in cheby_batch_rows_kernel); pieces are combined
 // by the ordered last-arriver reduction.
-template <int B, int U = 8, int MINB = 4>
-__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel(const BatchArgs a) {
+template <int B, int U = 8, int MINB = 4, bool PEER = false>
+__global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;
     constexpr int RPW = 32 / L;
     constexpr int V = 32 / L;
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             if (cl == 0) a.hub_count[r] = 0u;
             double2 wp, ac;
             batch_prefetch<B>(a, r, cl, wp, ac);
-            batch_epilogue<B>(a, r, y, d, cl, wp, ac);
+            batch_epilogue<B, PEER>(a, pa, r, y, d, cl, wp, ac);
         }
         (void)smask;
         job += stride;
@@ -738,6 +744,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         e0 = ne0;
         e1 = ne1;
     }
+    if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
 }
 
 // ---------------------------------------------------------------------------
@@ -874,7 +881,7 @@ void launch_slot(const BatchArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_kernel<B, U, MINB>, kBatchThreads, 0);
-    cheby_batch_kernel<B, U, MINB><<<occ * sms, kBatchThreads, 0, st>>>(a);
+    cheby_batch_kernel<B, U, MINB><<<occ * sms, kBatchThreads, 0, st>>>(a, PeerArgs{});
 }
 
 template <int B>
@@ -899,18 +906,32 @@ bool launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
     }
 }
 
-void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+// PEER instances (fused all-gather), default geometry.
+#define CPG_PEER_SWITCH(KERNEL, B, grid, st, a, pa)                                                        \
+    switch (B) {                                                                                            \
+    case 4: KERNEL<4, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                            \
+    case 8: KERNEL<8, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                            \
+    case 16: KERNEL<16, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                          \
+    case 32: KERNEL<32, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                          \
+    default: KERNEL<64, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                          \
+    }
+
+void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+    if (pa) {
+        CPG_PEER_SWITCH(cheby_batch_kernel, B, grid, st, a, *pa);
+        return;
+    }
     static const int cfg = [] {  // tuning hook: CPG_SLOT_CFG = U*10 + MINB
         const char* e = std::getenv("CPG_SLOT_CFG");
         return e ? std::atoi(e) : 0;
     }();
     if (cfg && launch_slot_cfg(a, B, cfg, st)) return;
     switch (B) {
-    case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 16: cheby_batch_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 32: cheby_batch_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
-    default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 16: cheby_batch_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 32: cheby_batch_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
 }
 // Split path: hub pieces through cheby_batch_kernel, then plain rows through
@@ -923,7 +944,11 @@ bool batch_split(uint64_t nnz_loc) {
     return nnz_loc >= (8ull << 20);
 }
 
-void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+    if (pa) {
+        CPG_PEER_SWITCH(cheby_batch_pieces_kernel, B, grid, st, a, *pa);
+        return;
+    }
     static const int cfg = [] {  // tuning hook: CPG_PIECES_CFG = U*10 + MINB (B = 16)
         const char* e = std::getenv("CPG_PIECES_CFG");
         return e ? std::atoi(e) : 0;
@@ -935,39 +960,43 @@ void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st) {
         switch (cfg) {
         case 83:
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 8, 3>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 8, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            cheby_batch_pieces_kernel<16, 8, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
             return;
         case 163:
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 16, 3>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 16, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            cheby_batch_pieces_kernel<16, 16, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
             return;
         case 44:
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 4, 4>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 4, 4><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            cheby_batch_pieces_kernel<16, 4, 4><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
             return;
         case 65:
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 6, 5>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 6, 5><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a);
+            cheby_batch_pieces_kernel<16, 6, 5><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
             return;
         default: break;
         }
     }
     switch (B) {
-    case 4: cheby_batch_pieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 16: cheby_batch_pieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 32: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
-    default: cheby_batch_pieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 4: cheby_batch_pieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 16: cheby_batch_pieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 32: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    default: cheby_batch_pieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
 }
 
-void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st) {
+void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+    if (pa) {
+        CPG_PEER_SWITCH(cheby_batch_rows_kernel, B, grid, st, a, *pa);
+        return;
+    }
     switch (B) {
-    case 4: cheby_batch_rows_kernel<4><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 8: cheby_batch_rows_kernel<8><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 16: cheby_batch_rows_kernel<16><<<grid, kBatchThreads, 0, st>>>(a); break;
-    case 32: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a); break;
-    default: cheby_batch_rows_kernel<64><<<grid, kBatchThreads, 0, st>>>(a); break;
+    case 4: cheby_batch_rows_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 8: cheby_batch_rows_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 16: cheby_batch_rows_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 32: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    default: cheby_batch_rows_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
 }
 

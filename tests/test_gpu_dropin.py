@@ -65,6 +65,45 @@ def test_sharded_handle_single_rank_nccl(cpg, gpu):
     assert st.mass_err_max <= 1e-9
 
 
+@pytest.mark.parametrize("self_store", ["0", "1"])
+def test_sharded_fused_allgather(cpg, gpu, self_store, monkeypatch):
+    """Fused all-gather (CPG_P2P=1): the iterates are NCCL symmetric windows and
+    the batched epilogue stores every row into every rank's replica through the
+    LSA peer pointers, with a one-element all-reduce per iteration as the
+    barrier.  One rank: with CPG_P2P_SELF=1 the epilogue also stores through its
+    own LSA alias (the peer-store code path and the window mapping), with 0 it
+    runs the barrier path only.  Single-source queries on the same handle keep
+    the NCCL all-gather."""
+    import ctypes
+
+    import torch  # loads the torch-bundled NCCL (device API) into the process
+
+    from oracle import Port
+
+    assert torch.cuda.is_available()
+    monkeypatch.setenv("CPG_P2P", "1")
+    monkeypatch.setenv("CPG_P2P_SELF", self_store)
+    off, nb = cpg.gen_rmat(13, 16 << 13, seed=9)
+    offs = np.ascontiguousarray(off, np.uint64)
+    nbs = np.ascontiguousarray(nb, np.uint32)
+    dg = cpg.DeviceGraph.sharded(offs.ctypes.data_as(ctypes.c_void_p), nbs.ctypes.data_as(ctypes.c_void_p),
+                                 len(off) - 1, len(nb), False, 0, 0, 1, cpg.nccl_unique_id())
+    assert dg.info.fused_allgather == 1 and dg.info.chunks == 1
+    n = len(off) - 1
+    k = cpg.Kernel.ppr(0.2)
+    c = k.cheby_coeffs(26)
+    src = [0, 7, n // 3, n - 1, 11]
+    for tile in (4, 16):
+        got_b, st = cpg.cheby_power_many(dg, k, src, 26, batched=True, tile=tile)
+        for j, s in enumerate(src):
+            want, _, _ = Port.cheby_power(off, nb, c, 26, s)
+            assert_parity(got_b[j], want)
+    got, _ = cpg.cheby_power_many(dg, k, src[:2], 26)
+    for j, s in enumerate(src[:2]):
+        want, _, _ = Port.cheby_power(off, nb, c, 26, s)
+        assert_parity(got[j], want)
+
+
 @pytest.mark.parametrize("chunks", ["1", "3"])
 def test_sharded_single_rank_chunked(cpg, gpu, chunks, monkeypatch):
     """Chunked layout (CPG_CHUNKS) with per-chunk NCCL in-place all-gathers on the
