@@ -279,6 +279,9 @@ def main():
     ap.add_argument("--mode", default=None, choices=["single", "batched"], help="override the config's path")
     ap.add_argument("--tile", type=int, default=None, help="sources per batched tile (1..64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused-allgather", action="store_true",
+                    help="N>1 batched: epilogue stores into every rank's replica (NCCL symmetric windows) "
+                         "instead of the chunked NCCL all-gather")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -321,6 +324,8 @@ def run_ours(args, cfg):
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
         pg.broadcast(uid, 0)
+        if args.fused_allgather:
+            os.environ["CPG_P2P"] = "1"
         dg = P.DeviceGraph.sharded(csr.offsets_ptr, csr.neighbors_ptr, n, nnz, True, dev, rank, world,
                                    bytes(uid.cpu().numpy()))
     torch.cuda.synchronize()
@@ -449,6 +454,8 @@ def run_ours(args, cfg):
                        "sources_per_step": len(sources), "mode": cfg["mode"],
                        "tile": tile if batched else 1,
                        "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
+                       "allgather": (("fused NVLink stores" if dg.info.fused_allgather else
+                                      f"NCCL, {dg.info.chunks} chunks overlapped") if world > 1 else None),
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,

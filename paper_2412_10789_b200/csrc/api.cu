@@ -721,7 +721,7 @@ int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors,
             // NCCL in the process has the device API and all ranks share one
             // NVLink domain (one chunk: no separate collective to overlap)
             const char* pe = std::getenv("CPG_P2P");
-            const bool p2p = comm && pe && pe[0] == '1' && nccl_sym_supported(comm, nranks);
+            const bool p2p = comm && pe && pe[0] == '1' && nccl_sym_supported(comm, nranks, rank);
             g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks,
                               p2p && !std::getenv("CPG_CHUNKS") ? 1 : 0);
             g->nccl_comm = comm;

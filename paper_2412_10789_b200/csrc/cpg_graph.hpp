@@ -130,7 +130,7 @@ void nccl_allgather_f64(const double* send, double* recv, size_t count, void* co
 void nccl_allreduce_sum_f64(const double* send, double* recv, size_t count, void* comm, cudaStream_t st);
 void nccl_comm_destroy(void* comm);
 // nccl_sym.cu (NCCL symmetric windows; see there)
-bool nccl_sym_supported(void* comm, int nranks);
+bool nccl_sym_supported(void* comm, int nranks, int rank);
 void* nccl_sym_alloc(size_t bytes);
 void nccl_sym_free(void* p);
 void* nccl_sym_register(void* comm, void* buf, size_t bytes);

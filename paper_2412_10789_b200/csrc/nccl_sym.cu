@@ -76,16 +76,15 @@ void check(ncclResult_t r, const char* what) {
 }
 
 __global__ void k_lsa_ptrs(ncclWindow_t w, int n, double** out) {
-    const int p = threadIdx.x;
-    if (p < n) out[p] = static_cast<double*>(ncclGetLsaPointer(w, 0, p));
+    for (int p = threadIdx.x; p < n; p += blockDim.x) out[p] = static_cast<double*>(ncclGetLsaPointer(w, 0, p));
 }
 
 } // namespace
 
-bool nccl_sym_supported(void* comm, int nranks) {
+bool nccl_sym_supported(void* comm, int nranks, int rank) {
     if (!comm || !sym().ok) return false;
     const ncclTeam_t t = sym().team_lsa(static_cast<ncclComm_t>(comm));
-    return t.nRanks == nranks && t.stride == 1;  // one NVLink domain: LSA rank == world rank
+    return t.nRanks == nranks && t.rank == rank && t.stride == 1;  // one NVLink domain: LSA rank == world rank
 }
 
 void* nccl_sym_alloc(size_t bytes) {
@@ -116,7 +115,7 @@ void nccl_sym_peer_ptrs(void* win, int n, double** d_out, cudaStream_t st) {
 
 #else  // built without the NCCL device headers
 
-bool nccl_sym_supported(void*, int) { return false; }
+bool nccl_sym_supported(void*, int, int) { return false; }
 void* nccl_sym_alloc(size_t) { fail(CPG_ENCCL, "built without NCCL symmetric memory"); }
 void nccl_sym_free(void*) {}
 void* nccl_sym_register(void*, void*, size_t) { fail(CPG_ENCCL, "built without NCCL symmetric memory"); }
