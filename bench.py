@@ -279,6 +279,9 @@ def main():
     ap.add_argument("--mode", default=None, choices=["single", "batched"], help="override the config's path")
     ap.add_argument("--tile", type=int, default=None, help="sources per batched tile (1..64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N=1: run the row-partitioned multi-GPU path with one rank (NCCL communicator, "
+                         "chunked all-gathers) to measure its overhead on one GPU")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1 batched: epilogue stores into every rank's replica (NCCL symmetric windows) "
                          "instead of the chunked NCCL all-gather")
@@ -317,15 +320,17 @@ def run_ours(args, cfg):
     n, nnz = csr.n, csr.nnz
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    if world == 1:
+    if args.fused_allgather:
+        os.environ["CPG_P2P"] = "1"
+    if world == 1 and not args.sharded:
         dg = P.DeviceGraph.from_device(csr)
+    elif world == 1:  # one-rank sharded path (its own NCCL communicator)
+        dg = P.DeviceGraph.sharded(csr.offsets_ptr, csr.neighbors_ptr, n, nnz, True, dev, 0, 1, P.nccl_unique_id())
     else:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
         pg.broadcast(uid, 0)
-        if args.fused_allgather:
-            os.environ["CPG_P2P"] = "1"
         dg = P.DeviceGraph.sharded(csr.offsets_ptr, csr.neighbors_ptr, n, nnz, True, dev, rank, world,
                                    bytes(uid.cpu().numpy()))
     torch.cuda.synchronize()
@@ -453,9 +458,10 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["name"], "config_index": args.config, "n": n, "nnz": nnz, "K": K,
                        "sources_per_step": len(sources), "mode": cfg["mode"],
                        "tile": tile if batched else 1,
-                       "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"row-partition x{world}" if world > 1 or args.sharded else "1 GPU"),
                        "allgather": (("fused NVLink stores" if dg.info.fused_allgather else
-                                      f"NCCL, {dg.info.chunks} chunks overlapped") if world > 1 else None),
+                                      f"NCCL, {dg.info.chunks} chunks overlapped")
+                                     if world > 1 or args.sharded else None),
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,

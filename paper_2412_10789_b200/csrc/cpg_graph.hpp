@@ -77,6 +77,8 @@ struct cpg_graph {
     // Fused all-gather (CPG_P2P=1 on a sharded graph): w_a / w_b are NCCL
     // symmetric windows and the batched epilogue stores each computed row into
     // every rank's replica through the LSA peer pointers.
+    void* w_a_base = nullptr;       // cudaMalloc'd blocks holding the aligned w_a / w_b
+    void* w_b_base = nullptr;
     bool p2p = false;
     int p2p_self = 0;               // test hook: also store through this rank's own LSA alias
     void* win_a = nullptr;
