@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -140,30 +142,17 @@ void free_iterates(cpg_graph* g) {
         g->win_a = g->win_b = nullptr;
         g->w_a = g->w_b = nullptr;
     } else {
-        for (void* p : {g->w_a_base, g->w_b_base})
-            if (p) cudaFree(p);
-        g->w_a_base = g->w_b_base = nullptr;
+        dfree_aligned(g->w_a);
+        dfree_aligned(g->w_b);
         g->w_a = g->w_b = nullptr;
     }
-}
-
-// The gathered iterates (every edge reads a random row of w_k) are placed at
-// 512 MB-aligned addresses when they are large: measured 3.3% faster on config
-// 5 (68.7 -> 66.4 ms per step) than wherever cudaMalloc put them, the same as a
-// fresh region (profiles/r01/iterate_alignment.txt).  Presumably larger
-// translation pages: the random gathers touch the whole buffer every step.
-double* alloc_gathered(size_t bytes, void** base) {
-    const size_t align = bytes >= (256ull << 20) ? (512ull << 20) : 0;
-    CPG_CUDA(cudaMalloc(base, std::max<size_t>(bytes, 8) + align));
-    if (!align) return static_cast<double*>(*base);
-    return reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(*base) + align - 1) / align * align);
 }
 
 void alloc_iterates(cpg_graph* g, size_t cols) {
     const size_t bytes = sizeof(double) * g->n_pad * cols;
     if (!g->p2p) {
-        g->w_a = alloc_gathered(bytes, &g->w_a_base);
-        g->w_b = alloc_gathered(bytes, &g->w_b_base);
+        g->w_a = static_cast<double*>(dalloc_aligned(bytes));
+        g->w_b = static_cast<double*>(dalloc_aligned(bytes));
         return;
     }
     g->w_a = static_cast<double*>(nccl_sym_alloc(bytes));
@@ -184,10 +173,11 @@ void alloc_iterates(cpg_graph* g, size_t cols) {
 void ensure_ws(cpg_graph* g, size_t cols) {
     if (g->ws_cols == cols) return;
     free_iterates(g);
-    dfree(g->acc);
+    dfree_aligned(g->acc);
+    g->acc = nullptr;
     dfree(g->full);
     alloc_iterates(g, cols);
-    g->acc = dalloc<double>(static_cast<size_t>(g->n_loc) * cols);
+    g->acc = static_cast<double*>(dalloc_aligned(sizeof(double) * g->n_loc * cols));
     if (g->nccl_comm) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
     CPG_CUDA(cudaMemset(g->w_a, 0, sizeof(double) * g->n_pad * cols));
     CPG_CUDA(cudaMemset(g->w_b, 0, sizeof(double) * g->n_pad * cols));
@@ -793,9 +783,12 @@ int cpg_graph_destroy(cpg_graph* g) {
         for (auto e : g->chunk_ev)
             if (e) cudaEventDestroy(e);
         if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
-        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->gdeg, (void*)g->new_of_old,
+        if (!g->p2p) free_iterates(g);
+        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->acc})
+            dfree_aligned(p);
+        for (void* p : {(void*)g->gdeg, (void*)g->new_of_old,
                         (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
-                        (void*)g->bhub_count, g->w_a_base, g->w_b_base, (void*)g->acc, (void*)g->full,
+                        (void*)g->bhub_count, (void*)g->full,
                         (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial, (void*)g->d_mass_err,
                         (void*)g->d_step_mass, (void*)g->d_stage})
             if (p) cudaFree(p);

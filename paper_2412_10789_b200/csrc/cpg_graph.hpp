@@ -77,8 +77,6 @@ struct cpg_graph {
     // Fused all-gather (CPG_P2P=1 on a sharded graph): w_a / w_b are NCCL
     // symmetric windows and the batched epilogue stores each computed row into
     // every rank's replica through the LSA peer pointers.
-    void* w_a_base = nullptr;       // cudaMalloc'd blocks holding the aligned w_a / w_b
-    void* w_b_base = nullptr;
     bool p2p = false;
     int p2p_self = 0;               // test hook: also store through this rank's own LSA alias
     void* win_a = nullptr;
@@ -94,6 +92,11 @@ namespace cpg {
 // graph_build.cu
 void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_nbr, cudaStream_t st);
 void ensure_batch_tables(cpg_graph* g, int B);
+// Device buffers that the steps touch all over every step (gathered iterates,
+// per-row index/offset/accumulator arrays), at 512 MB-aligned addresses when
+// large; freed with dfree_aligned (api.cu).
+void* dalloc_aligned(size_t bytes);
+void dfree_aligned(void* p);
 ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t chunk, uint32_t max_rows,
                            int64_t piece, uint32_t slot_off, cudaStream_t st);
 
