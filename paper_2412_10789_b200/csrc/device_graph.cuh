@@ -31,7 +31,10 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 // Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
-constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
+#ifndef CPG_BATCH_HUB_EDGES
+#define CPG_BATCH_HUB_EDGES 2048
+#endif
+constexpr int kBatchHubEdges = CPG_BATCH_HUB_EDGES;  // B = 64: rows above this are split
 // Hub piece for width B: one row slot (B/2 lanes) handles a piece, so the
 // piece shrinks with the slot width to keep pieces equally long in time.
 __host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges * B / 64; }
