@@ -432,7 +432,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
-            if (t.meta || batch_split(g->nnz_loc)) {  // block-ordered pieces exist only for the split path
+            if (batch_split(g->nnz_loc)) {
                 // hub pieces (fused kernel with no plain rows), then the plain rows
                 if (prof) prof->before(st);
                 if (t.n_hub_items) {
@@ -441,12 +441,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                     const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
                         1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
-                    if (t.meta)
-                        launch_batch_cbpieces(h, t.meta - t.row_begin, static_cast<int>(B), hgrid, st, pa);
-                    else if (std::getenv("CPG_PIECES_FUSED"))  // A/B hook: hub pieces through the fused kernel
-                        launch_batch(h, static_cast<int>(B), hgrid, st, pa);
-                    else
-                        launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
+                    launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
                     ++launches;
                 }
                 if (t.row_end > b.hub_rows) {
@@ -780,10 +775,8 @@ int cpg_graph_destroy(cpg_graph* g) {
         }
         if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
         for (auto& t : g->tables) cudaFree(t.items);
-        for (auto& t : g->btables) {
+        for (auto& t : g->btables)
             if (t.items) cudaFree(t.items);
-            if (t.meta) cudaFree(t.meta);
-        }
         for (auto e : g->chunk_ev)
             if (e) cudaEventDestroy(e);
         if (g->comm_stream) cudaStreamDestroy(g->comm_stream);

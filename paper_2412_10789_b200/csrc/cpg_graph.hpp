@@ -16,9 +16,6 @@ struct ItemTable {
     WorkItem* items = nullptr;
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0;
     uint32_t row_begin = 0, row_end = 0;
-    // batched hub pieces in column-block order (CPG_CB_MB): meta[j] = {first
-    // partial slot, pieces} of hub row row_begin + j; null = plain piece order
-    uint2* meta = nullptr;
 };
 } // namespace cpg
 
@@ -40,7 +37,7 @@ struct cpg_graph {
     int tile = 0;                   // kTileSmall / kTileLarge
     std::vector<cpg::ItemTable> btables;  // batched items per chunk
     int bitems_width = 0;           // B the batched tables were built for
-    uint64_t bitems_cbw = 0;        // their column-block window (rows; 0 = plain piece order)
+    bool bitems_split = false;      // ... and for which kernels (split: piece kernel, else fused)
     uint32_t n_bpartials = 0;
     size_t bhub_items_cap = 0;
 
@@ -112,8 +109,6 @@ int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
 void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
-void launch_batch_cbpieces(const BatchArgs& a, const uint2* meta, int B, int grid, cudaStream_t st,
-                           const PeerArgs* pa = nullptr);
 
 void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
                         uint32_t q0, uint32_t count, cudaStream_t st);

@@ -31,13 +31,17 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 // Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
-#ifndef CPG_BATCH_HUB_EDGES
-#define CPG_BATCH_HUB_EDGES 2048
-#endif
-constexpr int kBatchHubEdges = CPG_BATCH_HUB_EDGES;  // B = 64: rows above this are split
-// Hub piece for width B: one row slot (B/2 lanes) handles a piece, so the
-// piece shrinks with the slot width to keep pieces equally long in time.
+constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
+// Hub piece for width B in the fused batched kernel (small graphs): one row
+// slot (B/2 lanes) handles a piece, so the piece shrinks with the slot width to
+// keep pieces equally long in time (the longest job bounds a small step).
 __host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges * B / 64; }
+// Hub piece in the split path's piece kernel (large graphs): 64*B edges (B = 16:
+// 1024), capped at 2048 for B = 64.  A piece is a run of column-sorted
+// gathers; longer runs sweep the iterate more locally (config 5, B = 16:
+// 512 -> 1024 edges +2.9%; config 4, B = 64: 2048 -> 4096 -1%;
+// profiles/r01/hub_piece_size_c{4,5}.txt).
+__host__ __device__ constexpr int batch_piece_edges(int B) { return B >= 32 ? kBatchHubEdges : 64 * B; }
 
 // Work item (16 B, one vector load).
 //   tile: a = first row, b = end row,

@@ -6,7 +6,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <unordered_map>
@@ -193,60 +192,6 @@ void build_hub_items(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_
     *n_items_out = total;
 }
 
-// Column-block-ordered hub pieces (batched step, CPG_CB_MB).  Hub row j's
-// sorted neighbour list is cut where the column crosses a multiple of W rows
-// (S[j][b] = first edge with column >= b*W) and every `piece` edges within a
-// block.  Slots are numbered row-major (edge order within the row); items are
-// written block-major, so the pieces in flight share one window of the iterate.
-__global__ void k_seg_starts(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t n_hub, uint64_t W,
-                             uint32_t NB, int64_t min_deg, int64_t* S) {
-    const uint64_t total = static_cast<uint64_t>(n_hub) * (NB + 1);
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = static_cast<uint32_t>(x / (NB + 1)), b = static_cast<uint32_t>(x % (NB + 1));
-        int64_t lo = rowptr[row0 + j], hi = rowptr[row0 + j + 1];
-        if (b == NB || (b > 0 && hi - lo < min_deg)) {  // short hubs: one segment (block 0), plain pieces
-            lo = hi;
-        } else if (b > 0) {
-            const uint64_t key = static_cast<uint64_t>(b) * W;
-            while (lo < hi) {  // first edge with col >= key
-                const int64_t mid = lo + (hi - lo) / 2;
-                if (static_cast<uint64_t>(col[mid]) < key) lo = mid + 1; else hi = mid;
-            }
-        }
-        S[x] = lo;
-    }
-}
-
-__global__ void k_seg_pieces(const int64_t* S, uint32_t n_hub, uint32_t NB, int64_t piece, uint32_t* PR,
-                             uint32_t* PC) {
-    const uint64_t total = static_cast<uint64_t>(n_hub) * NB;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = static_cast<uint32_t>(x / NB), b = static_cast<uint32_t>(x % NB);
-        const int64_t len = S[static_cast<uint64_t>(j) * (NB + 1) + b + 1] - S[static_cast<uint64_t>(j) * (NB + 1) + b];
-        const uint32_t p = static_cast<uint32_t>((len + piece - 1) / piece);
-        PR[x] = p;
-        PC[static_cast<uint64_t>(b) * n_hub + j] = p;
-    }
-}
-
-__global__ void k_cb_items(const int64_t* S, const uint32_t* rpos, const uint32_t* ipos, uint32_t n_hub, uint32_t NB,
-                           int64_t piece, uint32_t row0, uint32_t slot_off, WorkItem* items, uint2* meta) {
-    const uint64_t total = static_cast<uint64_t>(n_hub) * NB;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = static_cast<uint32_t>(x / NB), b = static_cast<uint32_t>(x % NB);
-        const int64_t s0 = S[static_cast<uint64_t>(j) * (NB + 1) + b];
-        const int64_t len = S[static_cast<uint64_t>(j) * (NB + 1) + b + 1] - s0;
-        const uint32_t slot = slot_off + rpos[x];
-        const uint32_t at = ipos[static_cast<uint64_t>(b) * n_hub + j];
-        for (int64_t k = 0; k * piece < len; ++k) {
-            const uint32_t cnt = static_cast<uint32_t>(min(piece, len - k * piece));
-            items[at + k] = WorkItem{row0 + j, slot + static_cast<uint32_t>(k),
-                                     tile_code(static_cast<uint64_t>(s0 + k * piece), cnt, 0) | kHubBit};
-        }
-        if (b == 0) meta[j] = make_uint2(slot, rpos[static_cast<uint64_t>(j + 1) * NB] - rpos[x]);
-    }
-}
-
 } // namespace
 
 // Work table over local rows [row0, row1): hub pieces (rows with deg > chunk,
@@ -426,92 +371,28 @@ void dfree_aligned(void* p) {
     cudaFree(base);
 }
 
-// Column-block window (rows of the B-wide iterate) for the block-ordered hub
-// pieces: CPG_CB_MB megabytes of iterate per window (0 / unset = off); only
-// where the split kernels run and the iterate spans more than two windows.
-uint64_t cb_window_rows(const cpg_graph* g, int B) {
-    const char* e = std::getenv("CPG_CB_MB");
-    const uint64_t mb = e ? static_cast<uint64_t>(std::atoll(e)) : 0;
-    if (!mb || !batch_split(g->nnz_loc)) return 0;
-    const uint64_t W = (mb << 20) / (8ull * static_cast<uint64_t>(B));
-    if (W == 0 || static_cast<uint64_t>(g->n_pad) <= 2 * W) return 0;
-    return W;
-}
-
-// Hubs with fewer edges than this keep whole-row pieces (in block 0): cutting
-// them at every block boundary makes pieces too short (CPG_CB_DEG).
-int64_t cb_min_degree() {
-    const char* e = std::getenv("CPG_CB_DEG");
-    return e ? std::atoll(e) : 16384;
-}
-
-void build_cb_items(cpg_graph* g, ItemTable& t, uint64_t W, int64_t hb, uint32_t slot_off) {
-    cudaStream_t st = g->stream;
-    const uint32_t n_hub = t.n_hubs;
-    const uint32_t NB = static_cast<uint32_t>((static_cast<uint64_t>(g->n_pad) + W - 1) / W);
-    const uint64_t segs = static_cast<uint64_t>(n_hub) * NB;
-    int64_t* S = dalloc<int64_t>(static_cast<uint64_t>(n_hub) * (NB + 1));
-    uint32_t* PR = dalloc<uint32_t>(segs + 1);
-    uint32_t* PC = dalloc<uint32_t>(segs + 1);
-    uint32_t* rpos = dalloc<uint32_t>(segs + 1);
-    uint32_t* ipos = dalloc<uint32_t>(segs + 1);
-    k_seg_starts<<<grid_for(static_cast<uint64_t>(n_hub) * (NB + 1)), kT, 0, st>>>(g->rowptr, g->col, t.row_begin,
-                                                                                  n_hub, W, NB, cb_min_degree(), S);
-    CPG_CUDA(cudaMemsetAsync(PR + segs, 0, sizeof(uint32_t), st));
-    CPG_CUDA(cudaMemsetAsync(PC + segs, 0, sizeof(uint32_t), st));
-    k_seg_pieces<<<grid_for(segs), kT, 0, st>>>(S, n_hub, NB, hb, PR, PC);
-    DevTemp tmp;
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, PR, rpos, segs + 1, st);
-    tmp.ensure(bytes);
-    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, PR, rpos, segs + 1, st));
-    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, PC, ipos, segs + 1, st));
-    uint32_t total = 0;
-    CPG_CUDA(cudaMemcpyAsync(&total, rpos + segs, sizeof(total), cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    t.items = dalloc<WorkItem>(std::max<uint32_t>(1, total));
-    t.meta = dalloc<uint2>(n_hub);
-    k_cb_items<<<grid_for(segs), kT, 0, st>>>(S, rpos, ipos, n_hub, NB, hb, t.row_begin, slot_off, t.items, t.meta);
-    CPG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(S);
-    cudaFree(PR);
-    cudaFree(PC);
-    cudaFree(rpos);
-    cudaFree(ipos);
-    t.n_hub_items = total;
-    if (std::getenv("CPG_CB_VERBOSE"))
-        std::fprintf(stderr, "[cpg] column-block pieces: hubs %u, window %llu rows x %u blocks, pieces %u\n", n_hub,
-                     static_cast<unsigned long long>(W), NB, total);
-}
-
 void ensure_batch_tables(cpg_graph* g, int B) {
-    if (!g->btables.empty() && g->bitems_width == B && g->bitems_cbw == cb_window_rows(g, B)) return;
-    for (auto& t : g->btables) {
+    const bool split = batch_split(g->nnz_loc);  // piece length depends on the kernel that runs them
+    if (!g->btables.empty() && g->bitems_width == B && g->bitems_split == split) return;
+    for (auto& t : g->btables)
         if (t.items) cudaFree(t.items);
-        if (t.meta) cudaFree(t.meta);
-    }
     g->btables.clear();
     uint32_t slots = 0;
     const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
-    const int64_t hb = batch_hub_edges(B);
-    const uint64_t W = cb_window_rows(g, B);
+    const int64_t hb = split ? batch_piece_edges(B) : batch_hub_edges(B);
     for (uint32_t c = 0; c < C; ++c) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
         build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0,
                         g->stream);
-        if (W && t.n_hubs) {  // re-cut the same hubs at column-block boundaries, block-major
-            cudaFree(t.items);
-            build_cb_items(g, t, W, hb, slots);
-        }
         t.n_items = t.n_hub_items;
         slots += t.n_hub_items;
         g->btables.push_back(t);
     }
     g->n_bpartials = slots;
     g->bitems_width = B;
-    g->bitems_cbw = W;
+    g->bitems_split = split;
     CPG_CUDA(cudaGetLastError());
 }
 

@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     constexpr int L = B / 2;
     constexpr int RPW = 32 / L;
     constexpr int V = 32 / L;
-    constexpr int HB = batch_hub_edges(B);
+    constexpr int HB = batch_piece_edges(B);
     const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
@@ -760,122 +760,6 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         job += stride;
         r = nr;
         sb = nsb;
-        e0 = ne0;
-        e1 = ne1;
-    }
-    if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
-}
-
-// Column-block-ordered hub pieces (CPG_CB_MB): hub rows are cut at the
-// boundaries of column blocks of the iterate (a window of a few hundred MB) as
-// well as every HB edges, and the pieces are ordered block-major, so the
-// gathers in flight on every SM stay inside one window of the iterate
-// (translation reach: random 128-B rows from per-SM windows of <= 512 MB run
-// 33% faster than from all 8 GB, profiles/r01/gather_pf/).  Each item carries
-// its own partial slot; meta[row] = {first slot of the row, pieces}; slots of
-// a row are numbered in edge order, so the last-arriver combine sums the
-// partials in edge order as in cheby_batch_pieces_kernel.
-template <int B, int U = 8, int MINB = 4, bool PEER = false>
-__global__ void __launch_bounds__(kBatchThreads, MINB)
-    cheby_batch_cbpieces_kernel(const BatchArgs a, const PeerArgs pa, const uint2* __restrict__ meta) {
-    constexpr int L = B / 2;
-    constexpr int RPW = 32 / L;
-    constexpr int V = 32 / L;
-    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
-    const int lane = threadIdx.x & 31;
-    const int slot = lane / L, cl = lane % L;
-    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t n_jobs = a.n_hub_items;
-    const uint32_t stride = nw * RPW;
-    uint32_t job = wg * RPW + slot;
-    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& ps, int64_t& e0, int64_t& e1) {
-        if (jb < n_jobs) {
-            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + jb);
-            const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-            r = raw.x;
-            ps = raw.y;
-            e0 = code_e0(c);
-            e1 = e0 + code_cnt(c);
-        } else {
-            r = ps = 0;
-            e0 = e1 = 0;
-        }
-    };
-    uint32_t c[V], cn[V];
-    auto load_chunk = [&](uint32_t (&dst)[V], int64_t e, int64_t end) {
-        const int m = static_cast<int>(e < end ? (end - e < 32 ? end - e : 32) : 0);
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const int t = v * L + cl;
-            dst[v] = t < m ? ld_index(a.col + e + t) : 0u;
-        }
-    };
-    uint32_t r, ps;
-    int64_t e0, e1;
-    load_item(job, r, ps, e0, e1);
-    load_chunk(c, e0, e1);
-    while (__any_sync(0xffffffffu, job < n_jobs)) {
-        uint32_t nr, nps;
-        int64_t ne0, ne1;
-        load_item(job + stride, nr, nps, ne0, ne1);  // in flight during this piece
-        uint2 m2 = make_uint2(0u, 0u);
-        if (job < n_jobs) m2 = __ldg(meta + r);
-        double2 s = {0.0, 0.0};
-        for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
-            const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
-            if (e != e0) {
-#pragma unroll
-                for (int v = 0; v < V; ++v) c[v] = cn[v];
-            }
-            if (__any_sync(0xffffffffu, e + 32 < e1)) load_chunk(cn, e + 32, e1);
-#pragma unroll
-            for (int t0 = 0; t0 < 32; t0 += U) {
-                if (!__any_sync(0xffffffffu, t0 < m)) break;
-                double2 val[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int t = t0 + q;
-                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                  u < a.hot_rows, pol_last, pol_first)
-                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                   : make_double2(0.0, 0.0);
-                }
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    s.x += val[q].x;
-                    s.y += val[q].y;
-                }
-            }
-        }
-        load_chunk(c, ne0, ne1);  // next piece's first chunk
-        const bool live = job < n_jobs;
-        const uint32_t P = m2.y;
-        if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(ps) * B)[cl] = s;
-        __threadfence();
-        __syncwarp();
-        unsigned prev = 0;
-        if (live && cl == 0) prev = atomicAdd(&a.hub_count[r], 1u);
-        prev = __shfl_sync(0xffffffffu, prev, slot * L);
-        if (live && prev == P - 1) {  // last piece of the row: ordered combine + epilogue
-            __threadfence();
-            double2 y = {0.0, 0.0};
-            for (uint32_t p = 0; p < P; ++p) {
-                const double2 v =
-                    __ldcg(reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(m2.x + p) * B) + cl);
-                y.x += v.x;
-                y.y += v.y;
-            }
-            if (cl == 0) a.hub_count[r] = 0u;
-            const int64_t d = a.rowptr[r + 1] - a.rowptr[r];
-            double2 wp, ac;
-            batch_prefetch<B>(a, r, cl, wp, ac);
-            batch_epilogue<B, PEER>(a, pa, r, y, d, cl, wp, ac);
-        }
-        job += stride;
-        r = nr;
-        ps = nps;
         e0 = ne0;
         e1 = ne1;
     }
@@ -1118,27 +1002,6 @@ void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, c
     case 16: cheby_batch_pieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     case 32: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     default: cheby_batch_pieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    }
-}
-
-void launch_batch_cbpieces(const BatchArgs& a, const uint2* meta, int B, int grid, cudaStream_t st,
-                           const PeerArgs* pa) {
-    if (pa) {
-        switch (B) {
-        case 4: cheby_batch_cbpieces_kernel<4, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, *pa, meta); break;
-        case 8: cheby_batch_cbpieces_kernel<8, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, *pa, meta); break;
-        case 16: cheby_batch_cbpieces_kernel<16, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, *pa, meta); break;
-        case 32: cheby_batch_cbpieces_kernel<32, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, *pa, meta); break;
-        default: cheby_batch_cbpieces_kernel<64, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, *pa, meta); break;
-        }
-        return;
-    }
-    switch (B) {
-    case 4: cheby_batch_cbpieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}, meta); break;
-    case 8: cheby_batch_cbpieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}, meta); break;
-    case 16: cheby_batch_cbpieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}, meta); break;
-    case 32: cheby_batch_cbpieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}, meta); break;
-    default: cheby_batch_cbpieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}, meta); break;
     }
 }
 

@@ -482,30 +482,6 @@ def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tile", [16, 64])
-def test_batched_column_block_pieces(cpg, gpu, tile, monkeypatch):
-    """Hub pieces cut at column-block boundaries and run block-major
-    (CPG_CB_MB; small windows so this graph spans several blocks): parity
-    with the reference, and bit-identical on a second run."""
-    monkeypatch.setenv("CPG_BATCH_SPLIT", "1")
-    monkeypatch.setenv("CPG_CB_MB", "1")
-    off, nb = cpg.gen_chunglu(50000, 600000, 2.0, 24.0, 15000, seed=11)
-    assert np.diff(off).max() > 512  # hubs at B = 16 and B = 64 (pieces of 512 / 2048 edges)
-    g = cpg.Graph.from_csr(off, nb)
-    ref = _ref_graph(off, nb)
-    src = ref.select_sources_uniform(11, 5)
-    for fam, param, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15)):
-        kern = cpg.Kernel.ppr(param) if fam == PPR else cpg.Kernel.hkpr(param)
-        got, st = cpg.cheby_power_many(g, kern, src, K, batched=True, tile=tile)
-        again, _ = cpg.cheby_power_many(g, kern, src, K, batched=True, tile=tile)
-        assert np.array_equal(got, again)
-        assert st.mass_err_max <= 1e-9
-        for j, s in enumerate(src):
-            want, _, _ = ref.cheby_power(fam, param, int(s), K)
-            assert_parity(got[j], want)
-
-
-@pytest.mark.gpu
 @pytest.mark.parametrize("group", ["1", "3", "16"])
 def test_single_source_query_groups(cpg, gpu, group, monkeypatch):
     """Query groups of the single-source step (several queries per launch, each
