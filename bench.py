@@ -465,9 +465,12 @@ def run_ours(args, cfg):
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": load_traffic(args.config, cfg["mode"], tile if batched else 1),
+                         # the committed ncu capture is of the one-GPU step; a rank's share differs
+                         "traffic": (load_traffic(args.config, cfg["mode"], tile if batched else 1)
+                                     if world == 1 and not args.sharded else None),
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full, per step)",
-                         "kernel": ("cheby_batch_kernel (hub pieces) + cheby_batch_rows_kernel, timed as one step"
+                         "kernel": (("cheby_batch_pieces_kernel (hub pieces) + cheby_batch_rows_kernel, timed as one "
+                                     "step" if nnz // world >= (8 << 20) else "cheby_batch_kernel")
                                     if batched else "cheby_step_kernel"),
                          "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms, "steps_per_launch": steps_per_launch,
                          "step_share_of_device_time": step_share},
