@@ -119,6 +119,9 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     const int occ = std::max(1, step_occupancy(g->tile));
     g->step_grid = 1;  // max over chunks: the mass-partial stride
     for (const auto& t : g->tables) g->step_grid = std::max(g->step_grid, table_grid(g.get(), t.n_items, occ));
+    // the split step's two grids share one mass-partial row
+    g->step_grid = std::max(g->step_grid, (std::max(1, step_hubs_occupancy()) +
+                                           std::max(1, step_tiles_occupancy(g->tile))) * g->sm_count);
     g->d_mass_err = dalloc<double>(2);
     CPG_CUDA(cudaDeviceSynchronize());
     return g.release();
@@ -301,6 +304,13 @@ uint32_t single_hot_rows(const cpg_graph* g) {
     return static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (static_cast<uint64_t>(std::atoll(e)) << 20) / 8));
 }
 
+// Single-source step as hub-piece + row-tile kernels: by default when the
+// iterate exceeds L2 (build_device_graph); CPG_STEP_SPLIT=1/0 forces (read per call).
+bool step_split(const cpg_graph* g) {
+    const char* e = std::getenv("CPG_STEP_SPLIT");
+    return e ? e[0] == '1' : g->step_split;
+}
+
 uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
                    cudaStream_t st, StepProf* prof, bool taylor = false, uint32_t Q = 1) {
     uint32_t launches = 0;
@@ -338,7 +348,26 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
             a.n_items = t.n_items;
             a.row0 = chunk_row0(g, c);
             a.mass_partial = g->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * MG;
-            if (t.n_items) {
+            if (t.n_items && Q == 1 && step_split(g)) {  // hub pieces, then row tiles at higher occupancy
+                if (prof) prof->before(st);
+                StepArgs h = a;
+                h.n_items = t.n_hub_items;
+                const int gh = t.n_hub_items ? table_grid(g, t.n_hub_items, std::max(1, step_hubs_occupancy())) : 0;
+                if (gh) {
+                    launch_step_hubs(h, gh, st);
+                    ++launches;
+                }
+                StepArgs r = a;
+                r.items = t.items + t.n_hub_items;
+                r.n_items = t.n_items - t.n_hub_items;
+                r.mass_partial = a.mass_partial + gh;
+                if (r.n_items) {
+                    launch_step_tiles(r, g->tile, table_grid(g, r.n_items, std::max(1, step_tiles_occupancy(g->tile))),
+                                      st);
+                    ++launches;
+                }
+                if (prof) prof->after(st);
+            } else if (t.n_items) {
                 const int grid = table_grid(g, t.n_items * Q, occ);
                 if (prof) prof->before(st);
                 launch_step(a, grid, st, &gq);

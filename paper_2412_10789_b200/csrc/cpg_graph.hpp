@@ -34,7 +34,8 @@ struct cpg_graph {
 
     std::vector<cpg::ItemTable> tables;   // single-source items, one table per chunk
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0, n_partials = 0;
-    int tile = 0;                   // kTileSmall / kTileLarge
+    int tile = 0;                   // kTileSmall / kTileMid / kTileLarge
+    bool step_split = false;        // single-source step as hub + tile kernels (iterate > L2)
     std::vector<cpg::ItemTable> btables;  // batched items per chunk
     int bitems_width = 0;           // B the batched tables were built for
     bool bitems_split = false;      // ... and for which kernels (split: piece kernel, else fused)
@@ -104,6 +105,10 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr);
 int step_occupancy(int tile);
+void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st);
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st);
+int step_tiles_occupancy(int tile);
+int step_hubs_occupancy();
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
 int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);

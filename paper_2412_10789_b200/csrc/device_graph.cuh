@@ -24,6 +24,7 @@ namespace cpg {
 // to give every SM several tiles, kTileSmall otherwise.
 constexpr int kStepThreads = 256;
 constexpr int kTileSmall = 1024;                 // edges staged per tile ( 8 KB smem)
+constexpr int kTileMid = 2048;                   // edges staged per tile (16 KB smem)
 constexpr int kTileLarge = 4096;                 // edges staged per tile (32 KB smem)
 constexpr int kTileMaxRows = 512;                // rows per tile (2 epilogue rows per thread)
 constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per thread)

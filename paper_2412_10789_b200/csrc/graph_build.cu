@@ -311,10 +311,17 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
 
     // 5. single-source work table: hub pieces, then row tiles.  Large tiles
     //    when every SM gets >= 8 of them, small tiles otherwise.
+    //    An iterate larger than L2 makes the gathers DRAM-latency bound: the
+    //    step then runs split (hub-piece kernel + 1024-edge tile kernel at 8
+    //    CTAs/SM; config 5: 146 -> 165 GTEPS, profiles/r01/single_split/).
+    int l2 = 0;
+    CPG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
+    g->step_split = static_cast<uint64_t>(g->n_pad) * sizeof(double) > static_cast<uint64_t>(l2);
     g->tile = g->nnz_loc >= static_cast<uint64_t>(kTileLarge) * g->sm_count * 8 ? kTileLarge : kTileSmall;
+    if (g->step_split) g->tile = kTileSmall;
     if (const char* force = std::getenv("CPG_TILE")) {  // test hook: exercise either width
         const int t = std::atoi(force);
-        if (t == kTileSmall || t == kTileLarge) g->tile = t;
+        if (t == kTileSmall || t == kTileMid || t == kTileLarge) g->tile = t;
     }
     g->tables.clear();
     uint32_t slots = 0;

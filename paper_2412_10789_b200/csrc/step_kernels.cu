@@ -330,6 +330,45 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
+// Split single-source step (CPG_STEP_SPLIT): the hub pieces of the table
+// (items [0, n_hub_items)) and the row tiles (the rest) in two kernels, so the
+// tile kernel drops the hub path's registers and fits more CTAs per SM.  Each
+// writes its own CTAs' mass partials (the tile kernel's start after the hub
+// kernel's grid).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs a) {
+    __shared__ double red[THREADS / 32];
+    __shared__ int flag;
+    double mass = 0.0;
+    for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+        WorkItem it;
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
+        it.a = raw.x;
+        it.b = raw.y;
+        it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        process_hub<THREADS>(a, it, red, &flag, mass);
+    }
+    mass = block_sum<THREADS>(mass, red);
+    if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
+}
+
+template <int THREADS, int TILE, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const StepArgs a) {
+    __shared__ TileSmem<TILE> sm;
+    __shared__ double red[THREADS / 32];
+    double mass = 0.0;
+    for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+        WorkItem it;
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
+        it.a = raw.x;
+        it.b = raw.y;
+        it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        process_tile<THREADS, TILE>(a, it, sm, mass);
+    }
+    mass = block_sum<THREADS>(mass, red);
+    if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
+}
+
 // Query group: nq single-source queries per launch (small graphs, where one
 // query cannot fill the GPU).  Items x queries: job x = q * n_items + i, so a
 // CTA's queries are nondecreasing and its mass partial is flushed once per
@@ -872,7 +911,12 @@ __global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, d
 // Host-side launch wrappers ---------------------------------------------------
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq) {
     const bool group = gq && gq->nq > 1;
-    if (a.tile == kTileLarge) {
+    if (a.tile == kTileMid) {
+        if (group)
+            cheby_step_group_kernel<kStepThreads, kTileMid><<<grid, kStepThreads, 0, st>>>(a, *gq);
+        else
+            cheby_step_kernel<kStepThreads, kTileMid><<<grid, kStepThreads, 0, st>>>(a);
+    } else if (a.tile == kTileLarge) {
         if (group)
             cheby_step_group_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a, *gq);
         else
@@ -884,9 +928,40 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* 
             cheby_step_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a);
     }
 }
+// Split step: tile kernel instance for a tile width (MINB CTAs per SM).
+#define CPG_TILES_SWITCH(X)                                  \
+    switch (tile) {                                          \
+    case kTileSmall: X(kTileSmall, 8); break;                \
+    case kTileMid: X(kTileMid, 6); break;                    \
+    default: X(kTileLarge, 5); break;                        \
+    }
+void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st) {
+    cheby_step_hubs_kernel<kStepThreads><<<grid, kStepThreads, 0, st>>>(a);
+}
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st) {
+#define CPG_L(T, M) cheby_step_tiles_kernel<kStepThreads, T, M><<<grid, kStepThreads, 0, st>>>(a)
+    CPG_TILES_SWITCH(CPG_L)
+#undef CPG_L
+}
+int step_tiles_occupancy(int tile) {
+    int blocks = 0;
+#define CPG_O(T, M) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_tiles_kernel<kStepThreads, T, M>, kStepThreads, 0)
+    CPG_TILES_SWITCH(CPG_O)
+#undef CPG_O
+    return blocks;
+}
+int step_hubs_occupancy() {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_hubs_kernel<kStepThreads>, kStepThreads, 0);
+    return blocks;
+}
+
 int step_occupancy(int tile) {  // same for both instances (64 registers, same shared memory)
     int blocks = 0;
-    if (tile == kTileLarge)
+    if (tile == kTileMid)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_group_kernel<kStepThreads, kTileMid>,
+                                                      kStepThreads, 0);
+    else if (tile == kTileLarge)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_group_kernel<kStepThreads, kTileLarge>,
                                                       kStepThreads, 0);
     else

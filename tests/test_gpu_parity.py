@@ -481,6 +481,32 @@ def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
         assert_parity(got[j], want)
 
 
+@pytest.mark.parametrize("tile", ["1024", "2048", "4096"])
+def test_single_source_split_step(cpg, gpu, tile, monkeypatch):
+    """The split single-source step (hub-piece kernel + tile kernel at higher
+    occupancy; default when the iterate exceeds L2) at every tile width, on a
+    graph with multi-piece hubs: PPR and HKPR against the reference, the mass
+    check, and bit-identical to the combined kernel (same reduction order)."""
+    monkeypatch.setenv("CPG_TILE", tile)
+    monkeypatch.setenv("CPG_GROUP_Q", "1")  # the split step runs one query per launch
+    off, nb = cpg.gen_chunglu(30000, 500000, 2.0, 30.0, 12000, seed=21)
+    assert np.diff(off).max() > 4096  # hubs split into several pieces
+    g = cpg.Graph.from_csr(off, nb)
+    ref = _ref_graph(off, nb)
+    src = ref.select_sources_uniform(5, 3)
+    for fam, param, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15)):
+        kern = cpg.Kernel.ppr(param) if fam == PPR else cpg.Kernel.hkpr(param)
+        monkeypatch.setenv("CPG_STEP_SPLIT", "1")
+        got, st = cpg.cheby_power_many(g, kern, src, K)
+        monkeypatch.setenv("CPG_STEP_SPLIT", "0")
+        combined, _ = cpg.cheby_power_many(g, kern, src, K)
+        assert np.array_equal(got, combined)
+        assert st.mass_err_max <= 1e-9
+        for j, s in enumerate(src):
+            want, _, _ = ref.cheby_power(fam, param, int(s), K)
+            assert_parity(got[j], want)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("group", ["1", "3", "16"])
 def test_single_source_query_groups(cpg, gpu, group, monkeypatch):
