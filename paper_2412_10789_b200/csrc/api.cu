@@ -362,8 +362,8 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
                 r.n_items = t.n_items - t.n_hub_items;
                 r.mass_partial = a.mass_partial + gh;
                 if (r.n_items) {
-                    launch_step_tiles(r, g->tile, g->n_pad,
-                                      table_grid(g, r.n_items, std::max(1, step_tiles_occupancy(g->tile))), st);
+                    launch_step_tiles(r, g->tile, table_grid(g, r.n_items, std::max(1, step_tiles_occupancy(g->tile))),
+                                      st);
                     ++launches;
                 }
                 if (prof) prof->after(st);

@@ -106,7 +106,7 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr);
 int step_occupancy(int tile);
 void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st);
-void launch_step_tiles(const StepArgs& a, int tile, uint32_t n_pad, int grid, cudaStream_t st);
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st);
 int step_tiles_occupancy(int tile);
 int step_hubs_occupancy();
 void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);

@@ -82,7 +82,6 @@ struct StepArgs {
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
     int taylor;            // power method (PwMethod, solvers.cpp:87-116): w_k = D^-1 A w_{k-1}
     int last;              // write out = d * acc instead of acc
-    uint32_t hot1;         // tile kernel A/B (CPG_L1_HOT): ids < hot1 gathered L1::evict_last, others L1::no_allocate
 };
 
 // Query group (cheby_step_group_kernel): nq single-source queries in one

@@ -106,19 +106,6 @@ __device__ __forceinline__ double ld_gather_hot(const double* p, bool hot, uint6
     return v;
 }
 
-// L1 residency split (single-source tile kernel, CPG_L1_HOT): gathers of the
-// hot prefix allocate in L1 with evict_last, the cold tail skips L1.
-__device__ __forceinline__ double ld_gather_l1last(const double* p) {
-    double v;
-    asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ld_gather_l1na(const double* p) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-
 // Batched gathers with an L2 residency split: the degree-sorted hot prefix of
 // the iterate (rows < hot) is loaded evict_last, the cold tail evict_first.
 __device__ __forceinline__ double2 ld_gather2_hot(const double* p, bool hot, uint64_t pol_last, uint64_t pol_first) {
@@ -196,9 +183,9 @@ struct TileSmem {
 // stream, the epilogue operands of the rows this thread finalises), then the
 // gathers; one barrier; lane-group row sums from shared memory; one barrier;
 // the fused epilogue with thread t owning rows t and t + 256.
-template <int THREADS, int TILE, int HOT = 0>
+template <int THREADS, int TILE>
 __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, TileSmem<TILE>& sm,
-                                             double& mass, const double* hot = nullptr) {
+                                             double& mass) {
     constexpr int PER = TILE / THREADS;
     constexpr int RPT = kTileMaxRows / THREADS;
     const uint32_t rb = it.a;
@@ -227,38 +214,6 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
         for (int i = 0; i < PER; ++i) {
             const int j = i * THREADS + threadIdx.x;
             if (j < cnt) sm.vals[j] = ld_gather_hot(a.w_cur + idx[i], idx[i] < a.hot_rows, pol_last, pol_first);
-        }
-    } else if (HOT < 0) {  // L1 residency split at a.hot1 ids
-        double v[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int j = i * THREADS + threadIdx.x;
-            v[i] = 0.0;
-            if (j < cnt) v[i] = idx[i] < a.hot1 ? ld_gather_l1last(a.w_cur + idx[i]) : ld_gather_l1na(a.w_cur + idx[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int j = i * THREADS + threadIdx.x;
-            if (j < cnt) sm.vals[j] = v[i];
-        }
-    } else if (HOT) {  // ids < HOT from the shared-memory copy of the iterate's hot prefix
-        double v[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {  // every global gather in flight first
-            const int j = i * THREADS + threadIdx.x;
-            const bool g = j < cnt && idx[i] >= static_cast<uint32_t>(HOT);
-            v[i] = 0.0;
-            if (g) v[i] = ld_gather(a.w_cur + idx[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int j = i * THREADS + threadIdx.x;
-            if (j < cnt && idx[i] < static_cast<uint32_t>(HOT)) v[i] = hot[idx[i]];
-        }
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int j = i * THREADS + threadIdx.x;
-            if (j < cnt) sm.vals[j] = v[i];
         }
     } else {
 #pragma unroll
@@ -397,20 +352,10 @@ __global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
-// HOT > 0: the first HOT entries of w_k (the highest-degree ids: the most
-// gathered) are copied into shared memory at kernel start and gathered from
-// there, so those gathers take a few shared-memory wavefronts per warp instead
-// of one L1TEX wavefront per lane (dynamic shared memory, HOT * 8 bytes).
-template <int THREADS, int TILE, int MINB, int HOT = 0>
+template <int THREADS, int TILE, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const StepArgs a) {
     __shared__ TileSmem<TILE> sm;
     __shared__ double red[THREADS / 32];
-    extern __shared__ double2 hot_sm[];
-    if (HOT > 0) {
-        const double2* src = reinterpret_cast<const double2*>(a.w_cur);
-        for (int i = threadIdx.x; i < HOT / 2; i += THREADS) hot_sm[i] = __ldcg(src + i);
-        __syncthreads();
-    }
     double mass = 0.0;
     for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
         WorkItem it;
@@ -418,7 +363,7 @@ __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const S
         it.a = raw.x;
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        process_tile<THREADS, TILE, HOT>(a, it, sm, mass, reinterpret_cast<const double*>(hot_sm));
+        process_tile<THREADS, TILE>(a, it, sm, mass);
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
@@ -993,61 +938,13 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* 
 void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st) {
     cheby_step_hubs_kernel<kStepThreads><<<grid, kStepThreads, 0, st>>>(a);
 }
-// Shared-memory hot prefix of the tile kernel (A/B hook CPG_SMEM_HOT = 4096 or
-// 8192 entries; 0 = off).  Only where the hot ids are the prefix (one rank, one chunk).
-int smem_hot() {
-    const char* e = std::getenv("CPG_SMEM_HOT");
-    const int h = e ? std::atoi(e) : 0;
-    return h == 4096 || h == 8192 ? h : 0;
-}
-template <int T, int M, int H>
-void launch_tiles_hot(const StepArgs& a, int grid, cudaStream_t st) {
-    const size_t bytes = static_cast<size_t>(H) * sizeof(double);
-    static bool attr = [] {
-        cudaFuncSetAttribute(cheby_step_tiles_kernel<kStepThreads, T, M, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             H * 8);
-        return true;
-    }();
-    (void)attr;
-    cheby_step_tiles_kernel<kStepThreads, T, M, H><<<grid, kStepThreads, bytes, st>>>(a);
-}
-int l1_hot() {
-    const char* e = std::getenv("CPG_L1_HOT");
-    return e ? std::atoi(e) : 0;
-}
-void launch_step_tiles(const StepArgs& a, int tile, uint32_t n_pad, int grid, cudaStream_t st) {
-    if (l1_hot() > 0) {
-        StepArgs b = a;
-        b.hot1 = static_cast<uint32_t>(l1_hot());
-#define CPG_L(T, M) cheby_step_tiles_kernel<kStepThreads, T, M, -1><<<grid, kStepThreads, 0, st>>>(b)
-        CPG_TILES_SWITCH(CPG_L)
-#undef CPG_L
-        return;
-    }
-    const int h = n_pad >= static_cast<uint32_t>(smem_hot()) ? smem_hot() : 0;  // the copy reads w_k[0, h)
-    if (h == 4096) {
-        if (tile == kTileLarge) launch_tiles_hot<kTileLarge, 3, 4096>(a, grid, st);
-        else if (tile == kTileMid) launch_tiles_hot<kTileMid, 4, 4096>(a, grid, st);
-        else launch_tiles_hot<kTileSmall, 4, 4096>(a, grid, st);
-        return;
-    }
-    if (h == 8192) {
-        if (tile == kTileLarge) launch_tiles_hot<kTileLarge, 2, 8192>(a, grid, st);
-        else if (tile == kTileMid) launch_tiles_hot<kTileMid, 2, 8192>(a, grid, st);
-        else launch_tiles_hot<kTileSmall, 3, 8192>(a, grid, st);
-        return;
-    }
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st) {
 #define CPG_L(T, M) cheby_step_tiles_kernel<kStepThreads, T, M><<<grid, kStepThreads, 0, st>>>(a)
     CPG_TILES_SWITCH(CPG_L)
 #undef CPG_L
 }
 int step_tiles_occupancy(int tile) {
     int blocks = 0;
-    const int h = smem_hot();
-    if (h) {  // the shared memory bounds it: (228 KB - 1 KB reserved per CTA) / (tile smem + hot)
-        const int per = (tile == kTileLarge ? 39 : tile == kTileMid ? 23 : 15) + h / 128 + 1;
-        return std::max(1, std::min(tile == kTileLarge ? 3 : 4, 227 / per));
-    }
 #define CPG_O(T, M) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_tiles_kernel<kStepThreads, T, M>, kStepThreads, 0)
     CPG_TILES_SWITCH(CPG_O)
 #undef CPG_O
