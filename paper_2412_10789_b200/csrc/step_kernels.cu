@@ -1038,45 +1038,54 @@ bool batch_split(uint64_t nnz_loc) {
     return nnz_loc >= (8ull << 20);
 }
 
+// Launch a persistent batched kernel instance with its grid capped at its own
+// occupancy x SMs (callers size `grid` for the default 4 CTAs/SM).
+template <typename Kern>
+void launch_capped(Kern kernel, const BatchArgs& a, int grid, cudaStream_t st) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 0;  // per kernel instance; the same on every B200
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBatchThreads, 0);
+    kernel<<<std::max(1, std::min(grid, std::max(1, occ) * sms)), kBatchThreads, 0, st>>>(a, PeerArgs{});
+}
+
+// Geometry of the split kernels (U row gathers in flight per lane, MINB CTAs
+// per SM).  B = 16 runs U = 8 at 3 CTAs/SM (80 registers, no spills; config 5:
+// 887 -> 911-916 GTEPS); B = 64 keeps 4 CTAs/SM (3 lost 6-9% on configs 3-4;
+// profiles/r01/split_occupancy/).  CPG_PIECES_CFG / CPG_ROWS_CFG = U*10 + MINB
+// select other instances.
+int split_cfg(const char* env, int B) {
+    if (const char* e = std::getenv(env)) return std::atoi(e);
+    return B == 16 ? 83 : 84;
+}
+
+#define CPG_SPLIT_CFG_SWITCH(KERNEL, B)                                                             \
+    switch (cfg) {                                                                                  \
+    case 83: launch_capped(KERNEL<B, 8, 3>, a, grid, st); return;                                   \
+    case 63: launch_capped(KERNEL<B, 6, 3>, a, grid, st); return;                                   \
+    case 162: launch_capped(KERNEL<B, 16, 2>, a, grid, st); return;                                 \
+    default: launch_capped(KERNEL<B, 8, 4>, a, grid, st); return;                                   \
+    }
+
 void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_pieces_kernel, B, grid, st, a, *pa);
         return;
     }
-    static const int cfg = [] {  // tuning hook: CPG_PIECES_CFG = U*10 + MINB (B = 16)
-        const char* e = std::getenv("CPG_PIECES_CFG");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (B == 16 && cfg) {
-        int occ = 0, dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        switch (cfg) {
-        case 83:
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 8, 3>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 8, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
-            return;
-        case 163:
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 16, 3>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 16, 3><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
-            return;
-        case 44:
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 4, 4>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 4, 4><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
-            return;
-        case 65:
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_pieces_kernel<16, 6, 5>, kBatchThreads, 0);
-            cheby_batch_pieces_kernel<16, 6, 5><<<std::min(grid, occ * sms), kBatchThreads, 0, st>>>(a, PeerArgs{});
-            return;
-        default: break;
-        }
+    static const int cfg16 = split_cfg("CPG_PIECES_CFG", 16), cfg64 = split_cfg("CPG_PIECES_CFG", 64);
+    if (B == 16) {
+        const int cfg = cfg16;
+        CPG_SPLIT_CFG_SWITCH(cheby_batch_pieces_kernel, 16)
+    }
+    if (B == 64) {
+        const int cfg = cfg64;
+        CPG_SPLIT_CFG_SWITCH(cheby_batch_pieces_kernel, 64)
     }
     switch (B) {
     case 4: cheby_batch_pieces_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 16: cheby_batch_pieces_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 32: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    default: cheby_batch_pieces_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    default: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
 }
 
@@ -1085,12 +1094,19 @@ void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, con
         CPG_PEER_SWITCH(cheby_batch_rows_kernel, B, grid, st, a, *pa);
         return;
     }
+    static const int cfg16 = split_cfg("CPG_ROWS_CFG", 16), cfg64 = split_cfg("CPG_ROWS_CFG", 64);
+    if (B == 16) {
+        const int cfg = cfg16;
+        CPG_SPLIT_CFG_SWITCH(cheby_batch_rows_kernel, 16)
+    }
+    if (B == 64) {
+        const int cfg = cfg64;
+        CPG_SPLIT_CFG_SWITCH(cheby_batch_rows_kernel, 64)
+    }
     switch (B) {
     case 4: cheby_batch_rows_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     case 8: cheby_batch_rows_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 16: cheby_batch_rows_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 32: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    default: cheby_batch_rows_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    default: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
 }
 
