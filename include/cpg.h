@@ -173,6 +173,18 @@ int cpg_chebypower_batched(cpg_graph* g, const double* coeffs, uint32_t K,
 int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K,
                                   const uint32_t* sources, uint32_t n_sources, uint32_t tile,
                                   double* d_out, void* stream, cpg_stats* stats);
+/* Pipelined host output (no reference counterpart; for throughput callers that
+ * issue query after query, like the reference bench's worker loop
+ * tools/chebyprop.cpp:305-334): same as cpg_chebypower_batched, but it returns
+ * once the steps are computed, with the device->host copy of the last tile into
+ * `out` still in flight on the handle's copy stream, so it overlaps the next
+ * call's steps.  `out` (pinned host memory for a true overlap) must stay valid
+ * and unread until cpg_graph_sync returns. */
+int cpg_chebypower_batched_async(cpg_graph* g, const double* coeffs, uint32_t K,
+                                 const uint32_t* sources, uint32_t n_sources, uint32_t tile,
+                                 double* out, cpg_stats* stats);
+/* Wait for every result copy the handle has in flight. */
+int cpg_graph_sync(cpg_graph* g);
 
 /* ChebyPower ranked on the device: for each source the
  * k best (caller id, score) pairs by (score desc, id asc), the order of the

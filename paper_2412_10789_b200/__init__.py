@@ -43,7 +43,7 @@ __all__ = [
     "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
     "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
     "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan", "cheby_power_topk",
-    "ingest_edges", "load_edge_list_file",
+    "ingest_edges", "load_edge_list_file", "cheby_power_many_pipelined", "sync",
 ]
 
 
@@ -426,6 +426,27 @@ def cheby_power_many(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int
     else:
         _check(L.lib().cpg_chebypower(dg.handle, _f64p(c), K, _u32p(src), len(src), ptr, ctypes.byref(s)))
     return out, _to_stats(s, K)
+
+
+def cheby_power_many_pipelined(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, out,
+                               tile: int = 64, device: int = 0):
+    """Batched queries whose result copy into ``out`` (a pinned host buffer) is left in
+    flight: it overlaps the next call's steps.  Call ``sync(g)`` before reading ``out``.
+    Returns the SolveStats of the compute."""
+    K = _steps(cheby_steps)
+    dg = _dev(g, device)
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    c = kernel.cheby_coeffs(K)
+    s = cpg_stats()
+    ptr = out.ctypes.data if isinstance(out, np.ndarray) else int(out)
+    _check(L.lib().cpg_chebypower_batched_async(dg.handle, _f64p(c), K, _u32p(src), len(src), tile, ptr,
+                                                ctypes.byref(s)))
+    return _to_stats(s, K)
+
+
+def sync(g, device: int = 0):
+    """Wait for every result copy in flight on the graph's device handle."""
+    _check(L.lib().cpg_graph_sync(_dev(g, device).handle))
 
 
 def cheby_power_topk(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, k: int = 50, device: int = 0):

@@ -68,6 +68,9 @@ SIGNATURES = {
                                        POINTER(cpg_stats)]),
     "cpg_chebypower_batched_device": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_uint32, c_void_p,
                                               c_void_p, POINTER(cpg_stats)]),
+    "cpg_chebypower_batched_async": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_uint32, c_void_p,
+                                             POINTER(cpg_stats)]),
+    "cpg_graph_sync": (c_int, [_G]),
     "cpg_chebypower_trace": (c_int, [_G, _f64p, c_uint32, c_uint32, c_void_p, c_void_p, c_void_p]),
     "cpg_apply_walk": (c_int, [_G, _f64p, _f64p]),
     "cpg_chebypower_topk": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_uint32, _u32p, _f64p,

@@ -122,7 +122,10 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     // the split step's two grids share one mass-partial row
     g->step_grid = std::max(g->step_grid, (std::max(1, step_hubs_occupancy()) +
                                            std::max(1, step_tiles_occupancy(g->tile))) * g->sm_count);
-    g->d_mass_err = dalloc<double>(2);
+    // the per-query mass check lives in mapped pinned host memory: the host reads it
+    // without a device->host copy, which would queue behind a pipelined result copy
+    CPG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->d_mass_err), 2 * sizeof(double), cudaHostAllocMapped));
+    g->d_mass_err[0] = g->d_mass_err[1] = 0.0;
     CPG_CUDA(cudaDeviceSynchronize());
     return g.release();
 }
@@ -244,6 +247,7 @@ void ensure_params(cpg_graph* g, uint32_t K, uint32_t n_sources) {
 
 void ensure_stage(cpg_graph* g, size_t doubles) {
     if (g->stage_cap >= doubles) return;
+    CPG_CUDA(cudaStreamSynchronize(g->copy_stream));  // a pipelined copy may still read the old slots
     dfree(g->d_stage);
     g->d_stage = dalloc<double>(2 * doubles);
     g->stage_cap = doubles;
@@ -507,14 +511,13 @@ void upload_params(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_
     ensure_params(g, K, std::max<uint32_t>(ns, 1));
     CPG_CUDA(cudaMemcpyAsync(g->d_coeffs, coeffs, sizeof(double) * (K + 1), cudaMemcpyHostToDevice, st));
     if (ns) CPG_CUDA(cudaMemcpyAsync(g->d_sources, sources, sizeof(uint32_t) * ns, cudaMemcpyHostToDevice, st));
-    CPG_CUDA(cudaMemsetAsync(g->d_mass_err, 0, sizeof(double), st));
+    launch_zero_f64(g->d_mass_err, st);
 }
 
 void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, double wall, float dev_ms,
                 uint32_t launches, uint32_t cols) {
     if (!stats) return;
-    double merr = 0.0;
-    CPG_CUDA(cudaMemcpy(&merr, g->d_mass_err, sizeof(double), cudaMemcpyDeviceToHost));
+    const double merr = *static_cast<volatile double*>(g->d_mass_err);  // mapped; the stream was synchronized
     stats->iterations = K;
     stats->push_work = static_cast<uint64_t>(K) * g->nnz * queries;
     stats->wall_seconds = wall;
@@ -552,7 +555,7 @@ uint32_t single_group(const cpg_graph* g, uint32_t nq) {
 
 int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
           uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
-          cpg_stats* stats, double gp_a = 0.0) {
+          cpg_stats* stats, double gp_a = 0.0, bool pipelined = false) {
     return guarded([&] {
         require(g != nullptr, "null graph handle");
         require(std::isfinite(gp_a), "general_gp: exponent must be finite");
@@ -610,8 +613,9 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             if (out && out_on_device) {
                 dst = out + static_cast<size_t>(q0) * n;
             } else if (out) {
-                dst = g->d_stage + (b & 1) * slot;
-                CPG_CUDA(cudaStreamWaitEvent(st, g->ev[b & 1], 0));  // slot free (copy of b-2 done)
+                const uint32_t sl = (g->stage_seq + b) & 1;
+                dst = g->d_stage + sl * slot;
+                CPG_CUDA(cudaStreamWaitEvent(st, g->ev[sl], 0));  // slot free (its previous copy done)
             }
             if (mode == 0 || mode == 3) {
                 launches += run_single(g, K, q0, count, nullptr, 1.0, dst, st, prof.get(), mode == 3);
@@ -631,25 +635,28 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             }
             if (out && !out_on_device) {
                 // compute of batch b is queued; now drain batch b-1 (overlaps b's steps)
-                CPG_CUDA(cudaEventRecord(g->ev[2 + (b & 1)], st));
+                const uint32_t sl = (g->stage_seq + b) & 1, ps = sl ^ 1u;
+                CPG_CUDA(cudaEventRecord(g->ev[2 + sl], st));
                 if (b >= 1) {
-                    CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + ((b - 1) & 1)], 0));
+                    CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + ps], 0));
                     const uint32_t pq0 = (b - 1) * per, pc = std::min<uint32_t>(per, nq - pq0);
-                    CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + ((b - 1) & 1) * slot,
+                    CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + ps * slot,
                                              sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
-                    CPG_CUDA(cudaEventRecord(g->ev[(b - 1) & 1], g->copy_stream));
+                    CPG_CUDA(cudaEventRecord(g->ev[ps], g->copy_stream));
                 }
             }
         }
         CPG_CUDA(cudaEventRecord(e1, st));
         if (out && !out_on_device && nbatches > 0) {
             const uint32_t b = nbatches - 1;
+            const uint32_t sl = (g->stage_seq + b) & 1;
             const uint32_t pq0 = b * per, pc = std::min<uint32_t>(per, nq - pq0);
-            CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + (b & 1)], 0));
-            CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + (b & 1) * slot,
+            CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + sl], 0));
+            CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + sl * slot,
                                      sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
-            CPG_CUDA(cudaEventRecord(g->ev[b & 1], g->copy_stream));
-            CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
+            CPG_CUDA(cudaEventRecord(g->ev[sl], g->copy_stream));
+            g->stage_seq += nbatches;
+            if (!pipelined) CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
         }
         if (user_stream) {
             CPG_CUDA(cudaEventRecord(g->ev[4], st));
@@ -815,9 +822,10 @@ int cpg_graph_destroy(cpg_graph* g) {
         for (void* p : {(void*)g->gdeg, (void*)g->new_of_old,
                         (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
                         (void*)g->bhub_count, (void*)g->full,
-                        (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial, (void*)g->d_mass_err,
+                        (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial,
                         (void*)g->d_step_mass, (void*)g->d_stage})
             if (p) cudaFree(p);
+        if (g->d_mass_err) cudaFreeHost(g->d_mass_err);
         for (auto e : g->ev)
             if (e) cudaEventDestroy(e);
         if (g->stream) cudaStreamDestroy(g->stream);
@@ -844,6 +852,21 @@ int cpg_chebypower_vec(cpg_graph* g, const double* coeffs, uint32_t K, const dou
 int cpg_chebypower_batched(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
                            uint32_t n_sources, uint32_t tile, double* out, cpg_stats* stats) {
     return drive(g, coeffs, K, sources, nullptr, n_sources, tile, 2, out, false, nullptr, stats);
+}
+
+int cpg_chebypower_batched_async(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                                 uint32_t n_sources, uint32_t tile, double* out, cpg_stats* stats) {
+    return drive(g, coeffs, K, sources, nullptr, n_sources, tile, 2, out, false, nullptr, stats, 0.0, true);
+}
+
+int cpg_graph_sync(cpg_graph* g) {
+    return guarded([&] {
+        require(g != nullptr, "null graph handle");
+        std::lock_guard<std::mutex> lock(g->mu);
+        DeviceGuard dg(g->device);
+        CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
+        CPG_CUDA(cudaStreamSynchronize(g->stream));
+    });
 }
 
 int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,

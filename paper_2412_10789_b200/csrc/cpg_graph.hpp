@@ -71,6 +71,8 @@ struct cpg_graph {
     double* d_step_mass = nullptr;  // [step_mass_cap]
     size_t step_mass_cap = 0;
     double* d_stage = nullptr;      // device result staging for host output (2 slots)
+    uint32_t stage_seq = 0;         // slot of the next batch: slots alternate across calls too,
+                                    // so a pipelined call's last copy overlaps the next call
     size_t stage_cap = 0;           // doubles per slot
     // ev[0..1]: slot copied out; ev[2..3]: slot computed; ev[4]: caller-stream join
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -129,6 +131,7 @@ void launch_unpermute_batch(double* out, const double* full, const uint32_t* no,
                             uint32_t count, uint32_t B, const uint32_t* gdeg, double a, cudaStream_t st);
 void launch_mass_steps(const double* mp, uint32_t n_part, uint64_t q_stride, uint32_t K, uint32_t count,
                        double* steps, cudaStream_t st);
+void launch_zero_f64(double* p, cudaStream_t st);
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st);
 
 // topk.cu

@@ -1143,6 +1143,8 @@ void launch_mass_steps(const double* mp, uint32_t n_part, uint64_t q_stride, uin
                        double* steps, cudaStream_t st) {
     mass_steps_kernel<<<dim3(K, count), kStepThreads, 0, st>>>(mp, n_part, q_stride, steps, K);
 }
+__global__ void zero_f64_kernel(double* p) { *p = 0.0; }
+void launch_zero_f64(double* p, cudaStream_t st) { zero_f64_kernel<<<1, 1, 0, st>>>(p); }
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st) {
     mass_err_kernel<<<1, 1, 0, st>>>(steps, K, mass0, err);
 }

@@ -481,6 +481,35 @@ def test_batched_split_and_fused_paths(cpg, gpu, split, tile, monkeypatch):
         assert_parity(got[j], want)
 
 
+def test_pipelined_batched_output(cpg, gpu):
+    """cpg_chebypower_batched_async: back-to-back calls whose result copies stay in
+    flight (alternating staging slots across calls, pinned and pageable outputs,
+    one and several tiles per call) give the synchronous call's results exactly."""
+    import torch
+
+    off, nb = cpg.gen_chunglu(20000, 200000, 2.2, 12.0, 4000, seed=31)
+    g = cpg.Graph.from_csr(off, nb)
+    n = g.node_count()
+    kern = cpg.Kernel.ppr(0.2)
+    calls = [([3, 5, 7, 11], 4), ([13, 17, 19], 16), (list(range(40, 50)), 4), ([23], 1)]
+    want = [cpg.cheby_power_many(g, kern, s, 26, batched=True, tile=t)[0] for s, t in calls]
+    outs = []
+    for j, (s, t) in enumerate(calls):
+        if j % 2 == 0:
+            o = torch.empty((len(s), n), dtype=torch.float64, pin_memory=True).numpy()
+        else:
+            o = np.empty((len(s), n))
+        o.fill(np.nan)
+        cpg.cheby_power_many_pipelined(g, kern, s, 26, o, tile=t)
+        outs.append(o)
+    cpg.sync(g)
+    for o, w in zip(outs, want):
+        assert np.array_equal(o, w)
+    # a synchronous call after pipelined ones waits for nothing stale
+    again, _ = cpg.cheby_power_many(g, kern, calls[0][0], 26, batched=True, tile=4)
+    assert np.array_equal(again, want[0])
+
+
 @pytest.mark.parametrize("tile", ["1024", "2048", "4096"])
 def test_single_source_split_step(cpg, gpu, tile, monkeypatch):
     """The split single-source step (hub-piece kernel + tile kernel at higher
