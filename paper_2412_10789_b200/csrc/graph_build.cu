@@ -317,7 +317,13 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
     int l2 = 0;
     CPG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
     g->step_split = static_cast<uint64_t>(g->n_pad) * sizeof(double) > static_cast<uint64_t>(l2);
-    g->tile = g->nnz_loc >= static_cast<uint64_t>(kTileLarge) * g->sm_count * 8 ? kTileLarge : kTileSmall;
+    //    Large tiles when a launch holds >= 8 of them per SM.  Small graphs run
+    //    several queries per launch (query groups, up to 16; one rank), which
+    //    counts here: configs 1/2 went from 121/101 to 198/135 GTEPS with
+    //    4096-edge tiles (profiles/r01/single_groups/tile_rule.txt).
+    const uint64_t q_max = g->nranks > 1 ? 1 : std::min<uint64_t>(16, std::max<uint64_t>(1, (16ull << 20) /
+                                                                      std::max<uint64_t>(1, g->nnz_loc)));
+    g->tile = g->nnz_loc * q_max >= static_cast<uint64_t>(kTileLarge) * g->sm_count * 8 ? kTileLarge : kTileSmall;
     if (g->step_split) g->tile = kTileSmall;
     if (const char* force = std::getenv("CPG_TILE")) {  // test hook: exercise either width
         const int t = std::atoi(force);
