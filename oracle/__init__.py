@@ -274,6 +274,8 @@ class Ref:
             L.ref_ground_truth_steps.argtypes = [c_int, c_double]
             L.ref_ground_truth_steps.restype = c_uint64
             L.ref_graph_from_csr.argtypes = [_u64p, _u32p, c_uint64, c_uint64, POINTER(c_void_p)]
+            L.ref_graph_adopt_csr.argtypes = [_u64p, _u32p, c_uint64, c_uint64, POINTER(c_void_p)]
+            L.ref_apply_walk_subset_pool.argtypes = [c_void_p, c_int, c_uint64, _u64p, _f64p]
             L.ref_graph_from_edge_text.argtypes = [c_char_p, POINTER(c_void_p)]
             L.ref_graph_free.argtypes = [c_void_p]
             L.ref_graph_free.restype = None
@@ -355,6 +357,26 @@ class RefGraph:
                                                 len(offsets) - 1, len(nbrs), ctypes.byref(h)),
                    "from_csr")
         return cls(h)
+
+    @classmethod
+    def adopt_csr(cls, offsets, nbrs):
+        """A reference Graph over an already-validated CSR without from_csr's O(nnz log d)
+        symmetry check (ref_shim.cpp: ref_graph_adopt_csr).  structure_hash() reads 0."""
+        offsets, nbrs = _csr(offsets, nbrs)
+        h = c_void_p()
+        Ref._check(Ref.lib().ref_graph_adopt_csr(_p(offsets, _u64p), _p(nbrs, _u32p),
+                                                 len(offsets) - 1, len(nbrs), ctypes.byref(h)),
+                   "adopt_csr")
+        return cls(h)
+
+    def apply_walk_subset_pool(self, n_threads, edges_per_thread):
+        """(wall seconds, edges) for n_threads concurrent reference apply_walk_from_subset
+        calls (graph.cpp:275-288), each over a contiguous run of ~edges_per_thread slots."""
+        done = np.zeros(1, dtype=np.uint64)
+        wall = np.zeros(1)
+        Ref._check(Ref.lib().ref_apply_walk_subset_pool(self.h, n_threads, edges_per_thread,
+                                                        _p(done, _u64p), _p(wall, _f64p)), "subset_pool")
+        return float(wall[0]), int(done[0])
 
     @classmethod
     def from_edge_text(cls, text):

@@ -127,6 +127,32 @@ def test_port_matches_reference_bit_exact(oracle_mod):
 
 
 @needs_ref
+def test_adopted_reference_graph_equals_from_csr(oracle_mod):
+    """bench.py's huge-graph CPU baseline builds the reference Graph without from_csr's
+    symmetry check; it must compute exactly what the validated Graph computes."""
+    pairs = Port.ring_chord_pairs(500, 900, 7)
+    off, nb = Port.edges_to_csr(pairs)
+    g, a = RefGraph.from_csr(off, nb), RefGraph.adopt_csr(off, nb)
+    assert (a.n, a.nnz) == (g.n, g.nnz)
+    roff, rnb = a.csr()
+    assert np.array_equal(off, roff) and np.array_equal(nb, rnb)
+    x = Port.random_vector(g.n, 5, -1.0, 1.0)
+    assert np.array_equal(a.apply_walk(x), g.apply_walk(x))
+    assert np.array_equal(a.cheby_power(PPR, 0.2, 3, 26)[0], g.cheby_power(PPR, 0.2, 3, 26)[0])
+    for threads, per in ((1, 0), (1, len(nb)), (4, 1000)):
+        wall, edges = a.apply_walk_subset_pool(threads, per)
+        assert wall >= 0.0
+        if per == 0:
+            assert edges == 0
+        elif threads == 1:
+            assert edges == len(nb)  # one run over every row is one full apply_walk
+        else:
+            assert 4 * 1000 <= edges <= 4 * (1000 + int(np.diff(off).max()))
+    with pytest.raises(oracle_mod.OracleError):
+        RefGraph.adopt_csr(np.array([0, 1, 1], dtype=np.uint64), np.array([1], dtype=np.uint32))
+
+
+@needs_ref
 def test_port_power_method_matches_ground_truth(oracle_mod):
     """eval.cpp:39-59: ground truth = PwMethod with N = 231 (PPR .2)."""
     off, nb = Port.make_graph(100, 150, 3)
