@@ -425,6 +425,7 @@ int cpo_edges_to_csr(const int64_t* pairs, uint64_t m, uint32_t* n_out, uint64_t
  * thread-specific offset until ~edges_per_thread edges are processed (0 =
  * the whole graph, i.e. one full iteration).  The scatter still targets the
  * full-length out vector, so the memory behaviour is the reference's.
+ * Vector allocation and fill run before a start barrier, outside the clock.
  * Returns wall seconds; *edges_done = edges processed by all threads. */
 typedef struct {
     uint32_t n;
@@ -435,6 +436,8 @@ typedef struct {
     uint64_t edge_budget;
     uint64_t edges;
     int failed;
+    pthread_barrier_t* start;
+    double t_end;
 } cpo_walk_job;
 
 static double now_secs(void) {
@@ -447,8 +450,10 @@ static void* walk_worker(void* arg) {
     cpo_walk_job* j = (cpo_walk_job*)arg;
     double* x = (double*)malloc((size_t)j->n * sizeof(double));
     double* out = (double*)calloc((size_t)j->n, sizeof(double));
-    if (!x || !out) { free(x); free(out); j->failed = 1; return NULL; }
-    cpo_random_vector(j->n, j->seed, 0.0, 1.0, x);
+    if (!x || !out) j->failed = 1;
+    else cpo_random_vector(j->n, j->seed, 0.0, 1.0, x);
+    pthread_barrier_wait(j->start);
+    if (j->failed) { free(x); free(out); return NULL; }
     uint64_t done = 0;
     uint32_t u = j->row0;
     for (uint32_t cnt = 0; cnt < j->n && done < j->edge_budget; ++cnt) {
@@ -461,6 +466,7 @@ static void* walk_worker(void* arg) {
         if (++u == j->n) u = 0;
     }
     j->edges = done;
+    j->t_end = now_secs();
     free(x); free(out);
     return NULL;
 }
@@ -471,17 +477,23 @@ double cpo_apply_walk_pool(uint32_t n, const uint64_t* offsets, const uint32_t* 
     if (edges_per_thread == 0) edges_per_thread = offsets[n];
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);
     cpo_walk_job* jobs = (cpo_walk_job*)calloc((size_t)n_threads, sizeof(cpo_walk_job));
-    double t = now_secs();
+    pthread_barrier_t start;
+    pthread_barrier_init(&start, NULL, (unsigned)n_threads + 1u);
     for (int i = 0; i < n_threads; ++i) {
         jobs[i] = (cpo_walk_job){n, offsets, nbrs, (uint64_t)(1000 + i),
-                                 (uint32_t)(((uint64_t)i * n) / (uint64_t)n_threads), edges_per_thread, 0, 0};
+                                 (uint32_t)(((uint64_t)i * n) / (uint64_t)n_threads), edges_per_thread, 0, 0,
+                                 &start, 0.0};
         pthread_create(&th[i], NULL, walk_worker, &jobs[i]);
     }
+    pthread_barrier_wait(&start);
+    const double t = now_secs();
     for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
-    double wall = now_secs() - t;
+    pthread_barrier_destroy(&start);
+    double wall = 0.0;
     uint64_t total = 0;
     for (int i = 0; i < n_threads; ++i) {
         if (jobs[i].failed) wall = -1;
+        else if (wall >= 0 && jobs[i].t_end - t > wall) wall = jobs[i].t_end - t;
         total += jobs[i].edges;
     }
     if (edges_done) *edges_done = total;

@@ -36,7 +36,10 @@ constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are 
 // Hub piece for width B in the fused batched kernel (small graphs): one row
 // slot (B/2 lanes) handles a piece, so the piece shrinks with the slot width to
 // keep pieces equally long in time (the longest job bounds a small step).
-__host__ __device__ constexpr int batch_hub_edges(int B) { return kBatchHubEdges * B / 64; }
+#ifndef CPG_FUSED_HUB_EDGES
+#define CPG_FUSED_HUB_EDGES 2048
+#endif
+__host__ __device__ constexpr int batch_hub_edges(int B) { return CPG_FUSED_HUB_EDGES * B / 64; }
 // Hub piece in the split path's piece kernel (large graphs): 64*B edges (B = 16:
 // 1024), capped at 2048 for B = 64.  A piece is a run of column-sorted
 // gathers; longer runs sweep the iterate more locally (config 5, B = 16:
