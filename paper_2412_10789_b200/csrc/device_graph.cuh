@@ -33,13 +33,17 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
 constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
-// Hub piece for width B in the fused batched kernel (small graphs): one row
-// slot (B/2 lanes) handles a piece, so the piece shrinks with the slot width to
-// keep pieces equally long in time (the longest job bounds a small step).
+// Hub piece in the fused batched kernel (small graphs): rows above this many
+// edges are split into pieces of this length.  One row slot (B/2 lanes) works
+// a piece U = 8 gathers per round, so a piece costs edges/8 dependent L2
+// round trips whatever B is, and on a small graph the longest job bounds the
+// step: the same edge count for every B.  96 edges measured best at B = 16
+// and 64 (config 1: 512 -> 96 edges 230 -> 512 GTEPS; config 2: 2048 -> 96
+// edges 295 -> 550; 64/128/192/256 slower; profiles/r01/fused_piece/).
 #ifndef CPG_FUSED_HUB_EDGES
-#define CPG_FUSED_HUB_EDGES 2048
+#define CPG_FUSED_HUB_EDGES 96
 #endif
-__host__ __device__ constexpr int batch_hub_edges(int B) { return CPG_FUSED_HUB_EDGES * B / 64; }
+__host__ __device__ constexpr int batch_hub_edges(int) { return CPG_FUSED_HUB_EDGES; }
 // Hub piece in the split path's piece kernel (large graphs): 64*B edges (B = 16:
 // 1024), capped at 2048 for B = 64.  A piece is a run of column-sorted
 // gathers; longer runs sweep the iterate more locally (config 5, B = 16:

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(THREADS) cheby_step_group_kernel(const StepArg
 // prefetched with the first index chunk, then 32-edge chunks: each lane loads
 // 32/L indices (coalesced within the sub-group), and U row gathers per lane are
 // kept in flight.  Edge order within a row is sequential, so results are
-// bit-reproducible.  Rows above kBatchHubEdges are split into pieces combined
+// bit-reproducible.  Rows above batch_hub_edges(B) are split into pieces combined
 // by the ordered last-arriver reduction.
 // ---------------------------------------------------------------------------
 template <int B>
