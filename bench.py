@@ -40,9 +40,9 @@ PPR, HKPR = 0, 1
 # Synthetic stand-ins for the paper's datasets (BASELINE.json configs).
 CONFIGS = {
     1: dict(name="rmat-s16-ef8 ppr", gen="rmat", scale=16, samples=8 << 16, seed=1,
-            family=PPR, param=0.2, eps=1e-8, sources=16, mode="single"),
+            family=PPR, param=0.2, eps=1e-8, sources=16, mode="batched"),
     2: dict(name="chunglu-dblp-size hkpr", gen="chunglu", n_ids=317_080, samples=1_050_000, exponent=2.5,
-            mean=6.6, cap=0, seed=2, family=HKPR, param=5.0, eps=1e-8, sources=64, mode="single"),
+            mean=6.6, cap=0, seed=2, family=HKPR, param=5.0, eps=1e-8, sources=64, mode="batched"),
     3: dict(name="chunglu-livejournal-size ppr", gen="chunglu", n_ids=4_846_609, samples=43_200_000,
             exponent=2.3, mean=17.8, cap=20_000, seed=3, family=PPR, param=0.2, eps=1e-8, sources=64,
             mode="single"),
@@ -52,6 +52,9 @@ CONFIGS = {
     5: dict(name="rmat-friendster-size ppr", gen="rmat", scale=27, samples=1_840_000_000, seed=5,
             family=PPR, param=0.2, eps=1e-8, sources=16, mode="batched", tile=16),
 }
+# Configs 1, 2, 4, 5 run their sources through the batched step (one tile of all of them; the
+# faster path for a multi-source workload: DESIGN.md 6); config 3 names the single-source SpMV
+# path.  --mode overrides either way.
 # Headline: config 5, the 1.8B-edge graph the metric is quoted on at 1/2/4/8 B200;
 # its 16 sources run as one 16-column tile through the batched step.
 DEFAULT_CONFIG = 5
