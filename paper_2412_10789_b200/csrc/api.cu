@@ -429,6 +429,22 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
     if (const char* e = std::getenv("CPG_HOT_MB")) hot_mb = static_cast<uint64_t>(std::atoll(e));
     const uint32_t hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (hot_mb << 20) / (8 * cols)));
     CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
+    // Fused kernel (small graphs): warps claim jobs from a counter instead of a static
+    // stride, so a warp that drew short rows takes more (CPG_DYN_JOBS=0: static).
+    static const bool dyn_jobs = [] {
+        const char* e = std::getenv("CPG_DYN_JOBS");
+        return !e || e[0] != '0';
+    }();
+    const bool use_ctr = dyn_jobs && B <= 16 && !batch_split(g->nnz_loc);
+    if (use_ctr) {
+        const size_t need = static_cast<size_t>(K) * C;
+        if (g->job_ctr_cap < need) {
+            dfree(g->d_job_ctr);
+            g->d_job_ctr = dalloc<unsigned int>(need);
+            g->job_ctr_cap = need;
+        }
+        CPG_CUDA(cudaMemsetAsync(g->d_job_ctr, 0, sizeof(unsigned int) * need, st));
+    }
     if (seeds_dev)
         launch_init_dense_batch(g->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
     else
@@ -449,6 +465,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         b.k = static_cast<int>(k);
         b.first = k == 1;
         b.last = k == K;
+        b.job_ctr = nullptr;
         PeerArgs peer_args{nullptr, 0, 0};
         const PeerArgs* pa = nullptr;
         if (g->p2p) {  // fused all-gather: the epilogue stores into every replica
@@ -486,6 +503,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                 const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
                 if (jobs) {
                     const int grid = occ * g->sm_count;
+                    if (use_ctr) b.job_ctr = g->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
                     if (prof) prof->before(st);
                     launch_batch(b, static_cast<int>(B), grid, st, pa);
                     if (prof) prof->after(st);
@@ -821,7 +839,7 @@ int cpg_graph_destroy(cpg_graph* g) {
             dfree_aligned(p);
         for (void* p : {(void*)g->gdeg, (void*)g->new_of_old,
                         (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
-                        (void*)g->bhub_count, (void*)g->full,
+                        (void*)g->bhub_count, (void*)g->d_job_ctr, (void*)g->full,
                         (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial,
                         (void*)g->d_step_mass, (void*)g->d_stage})
             if (p) cudaFree(p);

@@ -47,6 +47,8 @@ struct cpg_graph {
     uint32_t hub_q = 1;                 // query-group capacity of hub_partial / hub_count
     double* bhub_partial = nullptr; // [n_bpartials][B]
     unsigned int* bhub_count = nullptr; // [n_loc]
+    unsigned int* d_job_ctr = nullptr;  // fused batched kernel: one job counter per (step, chunk)
+    size_t job_ctr_cap = 0;
 
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;

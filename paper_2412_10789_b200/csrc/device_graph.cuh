@@ -120,6 +120,7 @@ struct BatchArgs {
     uint32_t row0;
     uint32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last); 0 = off
     int k, first, last;
+    unsigned int* job_ctr;      // fused kernel: zeroed job counter (warps claim RPW jobs each); null = static stride
 };
 
 // Fused all-gather (second parameter of the PEER instances of the batched

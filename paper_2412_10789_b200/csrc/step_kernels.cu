@@ -498,6 +498,13 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArg
     }
 }
 
+// Lane 0 claims the next n jobs of the launch for its warp (warp-uniform result).
+__device__ __forceinline__ uint32_t claim_jobs(unsigned int* ctr, int lane, uint32_t n) {
+    uint32_t j = 0;
+    if (lane == 0) j = atomicAdd(ctr, n);
+    return __shfl_sync(0xffffffffu, j, 0);
+}
+
 template <int B>
 __device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, int cl, double2& wp, double2& ac) {
     const uint32_t gr = a.row0 + r;
@@ -525,7 +532,12 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_jobs = a.n_hub_items + (a.n_loc - a.hub_rows);
-    for (uint32_t base_job = wg * RPW; base_job < n_jobs; base_job += nw * RPW) {
+    // Dynamic claiming only where a claim covers several rows (B <= 16: RPW >= 4).  At
+    // B = 64 (one row per warp) one counter took an atomic per row and lost 25% on config 2
+    // (profiles/r01/fused_piece/dyn_jobs_ab.txt); those instances keep the static stride.
+    unsigned int* const ctr = (B <= 16) ? a.job_ctr : nullptr;
+    for (uint32_t base_job = ctr ? claim_jobs(ctr, lane, RPW) : wg * RPW; base_job < n_jobs;
+         base_job = ctr ? claim_jobs(ctr, lane, RPW) : base_job + nw * RPW) {
         const BatchJob<B> j = batch_job<B>(a, base_job + slot, n_jobs);
         double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
         if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
