@@ -435,7 +435,7 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         const char* e = std::getenv("CPG_DYN_JOBS");
         return !e || e[0] != '0';
     }();
-    const bool use_ctr = dyn_jobs && B <= 16 && !batch_split(g->nnz_loc);
+    const bool use_ctr = dyn_jobs && !batch_split(g->nnz_loc);
     if (use_ctr) {
         const size_t need = static_cast<size_t>(K) * C;
         if (g->job_ctr_cap < need) {

@@ -532,12 +532,21 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_jobs = a.n_hub_items + (a.n_loc - a.hub_rows);
-    // Dynamic claiming only where a claim covers several rows (B <= 16: RPW >= 4).  At
-    // B = 64 (one row per warp) one counter took an atomic per row and lost 25% on config 2
-    // (profiles/r01/fused_piece/dyn_jobs_ab.txt); those instances keep the static stride.
-    unsigned int* const ctr = (B <= 16) ? a.job_ctr : nullptr;
-    for (uint32_t base_job = ctr ? claim_jobs(ctr, lane, RPW) : wg * RPW; base_job < n_jobs;
-         base_job = ctr ? claim_jobs(ctr, lane, RPW) : base_job + nw * RPW) {
+    // Dynamic claiming: a warp claims CLAIM consecutive jobs per atomic and works them RPW
+    // at a time.  CLAIM >= 4 rows: at B = 64 one atomic per row lost 25% on config 2
+    // (profiles/r01/fused_piece/dyn_jobs_ab.txt).
+#ifndef CPG_CLAIM_ROWS
+#define CPG_CLAIM_ROWS 4
+#endif
+    constexpr uint32_t CLAIM = RPW > CPG_CLAIM_ROWS ? RPW : (CPG_CLAIM_ROWS / RPW) * RPW;
+    unsigned int* const ctr = a.job_ctr;
+    uint32_t claim_end = 0;
+    uint32_t base_job = wg * RPW;
+    if (ctr) {
+        base_job = claim_jobs(ctr, lane, CLAIM);
+        claim_end = base_job + CLAIM;
+    }
+    for (; base_job < n_jobs;) {
         const BatchJob<B> j = batch_job<B>(a, base_job + slot, n_jobs);
         double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
         if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
@@ -608,6 +617,14 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
         }
         (void)smask;
         if (do_epi) batch_epilogue<B, PEER>(a, pa, j.r, y, j.d, cl, wp, ac);
+        if (!ctr) {
+            base_job += nw * RPW;
+        } else if (base_job + RPW < claim_end) {
+            base_job += RPW;
+        } else {
+            base_job = claim_jobs(ctr, lane, CLAIM);
+            claim_end = base_job + CLAIM;
+        }
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
 }
