@@ -103,6 +103,17 @@ class Port:
                                                c_uint64, _f64p, c_int]
             L.cpo_apply_walk_pool.argtypes = [c_uint32, _u64p, _u32p, c_int, c_uint64, _u64p]
             L.cpo_apply_walk_pool.restype = c_double
+            L.cpo_cheby_power_pull.argtypes = [c_uint32, _u64p, _u32p, _f64p, c_uint64, _u32p, c_uint32,
+                                               _f64p, c_int]
+            L.cpo_cheby_power_vec_pull.argtypes = [c_uint32, _u64p, _u32p, _f64p, c_uint64, _f64p, c_uint32,
+                                                   _f64p, c_int]
+            _pp = POINTER(c_void_p)
+            L.cpo_gen_rmat.argtypes = [c_uint32, c_uint64, c_double, c_double, c_double, c_uint64, c_int, _pp,
+                                       _pp, _u32p, _u64p]
+            L.cpo_gen_chunglu.argtypes = [c_uint32, c_uint64, c_double, c_double, c_uint32, c_uint64, c_int,
+                                          _pp, _pp, _u32p, _u64p]
+            L.cpo_gen_free.argtypes = [c_void_p, c_void_p]
+            L.cpo_gen_free.restype = None
             cls._lib = L
         return cls._lib
 
@@ -243,6 +254,58 @@ class Port:
         if t < 0:
             raise OracleError("apply_walk_pool: out of memory")
         return t, done.value
+
+    @classmethod
+    def cheby_power_pull(cls, offsets, nbrs, coeffs, K, sources, n_threads=None):
+        """values[S][n] for S unit seeds: the row-parallel pull restatement (bit-exact with
+        the reference's scatter loop on a valid CSR), S <= 64 columns interleaved."""
+        offsets, nbrs = _csr(offsets, nbrs)
+        n = len(offsets) - 1
+        src = np.ascontiguousarray(np.atleast_1d(sources), dtype=np.uint32)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.empty((len(src), n))
+        nt = n_threads or os.cpu_count() or 1
+        cls._check(cls.lib().cpo_cheby_power_pull(n, _p(offsets, _u64p), _p(nbrs, _u32p), _p(coeffs, _f64p), K,
+                                                  _p(src, _u32p), len(src), _p(out, _f64p), nt), "cheby_power_pull")
+        return out
+
+    @classmethod
+    def cheby_power_vec_pull(cls, offsets, nbrs, coeffs, K, seeds, n_threads=None):
+        offsets, nbrs = _csr(offsets, nbrs)
+        n = len(offsets) - 1
+        seeds = np.ascontiguousarray(np.atleast_2d(seeds), dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.empty_like(seeds)
+        nt = n_threads or os.cpu_count() or 1
+        cls._check(cls.lib().cpo_cheby_power_vec_pull(n, _p(offsets, _u64p), _p(nbrs, _u32p), _p(coeffs, _f64p), K,
+                                                      _p(seeds, _f64p), seeds.shape[0], _p(out, _f64p), nt),
+                   "cheby_power_vec_pull")
+        return out
+
+    @classmethod
+    def _gen_result(cls, rc, off, nbr, n, nnz, what):
+        cls._check(rc, what)
+        o = np.ctypeslib.as_array(ctypes.cast(off, _u64p), shape=(n.value + 1,)).copy()
+        b = np.ctypeslib.as_array(ctypes.cast(nbr, _u32p), shape=(nnz.value,)).copy()
+        cls.lib().cpo_gen_free(off, nbr)
+        return o, b
+
+    @classmethod
+    def gen_rmat(cls, scale, n_samples, a=0.57, b=0.19, c=0.19, seed=1, n_threads=None):
+        """Host restatement of the repo's R-MAT generator (graphgen_port.c): same CSR."""
+        off, nbr, n, nnz = c_void_p(), c_void_p(), c_uint32(), c_uint64()
+        rc = cls.lib().cpo_gen_rmat(scale, n_samples, a, b, c, seed, n_threads or os.cpu_count() or 1,
+                                    ctypes.byref(off), ctypes.byref(nbr), ctypes.byref(n), ctypes.byref(nnz))
+        return cls._gen_result(rc, off, nbr, n, nnz, "gen_rmat")
+
+    @classmethod
+    def gen_chunglu(cls, n_ids, n_samples, exponent, mean_degree, max_degree=0, seed=1, n_threads=None):
+        """Host restatement of the repo's Chung-Lu generator (graphgen_port.c): same CSR."""
+        off, nbr, n, nnz = c_void_p(), c_void_p(), c_uint32(), c_uint64()
+        rc = cls.lib().cpo_gen_chunglu(n_ids, n_samples, exponent, mean_degree, max_degree, seed,
+                                       n_threads or os.cpu_count() or 1, ctypes.byref(off), ctypes.byref(nbr),
+                                       ctypes.byref(n), ctypes.byref(nnz))
+        return cls._gen_result(rc, off, nbr, n, nnz, "gen_chunglu")
 
     @classmethod
     def select_sources_uniform(cls, n, count, seed):

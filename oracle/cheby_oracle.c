@@ -500,3 +500,170 @@ double cpo_apply_walk_pool(uint32_t n, const uint64_t* offsets, const uint32_t* 
     free(th); free(jobs);
     return wall;
 }
+
+/* ---- row-parallel pull restatement of cheby_power (multi-threaded) ---------
+ * Same arithmetic as cpo_cheby_power_vec / the reference, bit for bit, but the
+ * walk operator is evaluated row by row (pull) so the rows can be split over
+ * threads:
+ *
+ *   reference (graph.cpp:260-266): out[v] = 0; for u = 0..n-1 ascending, if
+ *   x[u] != 0: out[v] += x[u] * inv_degree(u) for every v in N(u).
+ *
+ * On a symmetric CSR with sorted rows (Graph::from_csr's invariants,
+ * graph.cpp:84-95) the u that add into out[v] are exactly N(v), met in
+ * ascending order, so out[v] = (((0 + y[u1]) + y[u2]) + ...) over N(v) sorted,
+ * with y[u] = x[u] * (1.0 / d_u).  A skipped zero x[u] is represented by
+ * y[u] = -0.0, which is an exact additive identity (s + -0.0 == s for every s,
+ * including +0.0), so skipping and adding agree bit for bit.
+ *
+ * The dense passes (solvers.cpp:209, 218, 221, 225) are per-element and are
+ * fused into the row pass with the same expressions:
+ *   values[v] += c_k * r_cur[v];  r_next[v] = 2.0 * tmp[v] - r_prev[v].
+ * S columns (sources or dense seeds) run interleaved ([n][S] layout) so one
+ * gathered cache line serves all of them; each column's arithmetic is the
+ * single-column arithmetic.  Pinned bit-for-bit against the reference library
+ * in tests/test_oracle_pin.py. */
+typedef struct {
+    uint32_t n, S;
+    const uint64_t* off;
+    const uint32_t* nb;
+    const double* y;     /* [n][S] gathered: x * inv_degree, -0.0 where x == 0 */
+    double* y_next;      /* [n][S] next step's y */
+    double* r_prev;      /* [n][S] in: T_{k-1}, out: T_{k+1} (in place) */
+    const double* r_cur; /* [n][S] T_k */
+    double* values;      /* [n][S] */
+    double ck;           /* c_k added before the walk (solvers.cpp:218) */
+    int mode;            /* 0: first walk (r_prev <- P seed), 1: recurrence step */
+    const uint32_t* chunk_rows; /* chunk boundaries (rows) */
+    uint32_t n_chunks;
+    uint32_t cursor;
+} pull_job;
+
+static inline double pull_y(double x, uint64_t d) {
+    return x == 0.0 ? -0.0 : x * (1.0 / (double)d); /* graph.cpp:79, :263-264 */
+}
+
+static void* pull_worker(void* arg) {
+    pull_job* j = (pull_job*)arg;
+    const uint32_t S = j->S;
+    double acc[64];
+    for (;;) {
+        const uint32_t c = __atomic_fetch_add(&j->cursor, 1, __ATOMIC_RELAXED);
+        if (c >= j->n_chunks) break;
+        for (uint32_t v = j->chunk_rows[c]; v < j->chunk_rows[c + 1]; ++v) {
+            for (uint32_t s = 0; s < S; ++s) acc[s] = 0.0; /* out.assign(n, 0.0), graph.cpp:260 */
+            const uint64_t b = j->off[v], e = j->off[v + 1];
+            for (uint64_t i = b; i < e; ++i) {
+                if (i + 16 < e) __builtin_prefetch(j->y + (size_t)j->nb[i + 16] * S);
+                const double* yu = j->y + (size_t)j->nb[i] * S;
+                for (uint32_t s = 0; s < S; ++s) acc[s] += yu[s]; /* :265 */
+            }
+            const uint64_t dv = e - b;
+            double* rp = j->r_prev + (size_t)v * S;
+            double* yn = j->y_next + (size_t)v * S;
+            if (j->mode == 0) { /* r_cur = apply_walk(seed), solvers.cpp:212 */
+                for (uint32_t s = 0; s < S; ++s) { rp[s] = acc[s]; yn[s] = pull_y(acc[s], dv); }
+            } else {
+                const double* rc = j->r_cur + (size_t)v * S;
+                double* val = j->values + (size_t)v * S;
+                for (uint32_t s = 0; s < S; ++s) {
+                    val[s] += j->ck * rc[s];                   /* :218 */
+                    const double r = 2.0 * acc[s] - rp[s];     /* :221 */
+                    rp[s] = r;
+                    yn[s] = pull_y(r, dv);
+                }
+            }
+        }
+    }
+    return NULL;
+}
+
+static void pull_run(pull_job* j, int n_threads) {
+    j->cursor = 0;
+    if (n_threads <= 1) { pull_worker(j); return; }
+    pthread_t th[256];
+    if (n_threads > 256) n_threads = 256;
+    for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, pull_worker, j);
+    for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+}
+
+/* values[S][n] <- cheby_power_vec for S dense seeds (seeds[S][n]), pull form. */
+int cpo_cheby_power_vec_pull(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs,
+                             const double* coeffs, uint64_t K, const double* seeds, uint32_t S,
+                             double* values_out, int n_threads) {
+    if (K < 1 || S < 1 || S > 64) return CPO_EINVAL; /* solvers.cpp:201 */
+    const size_t N = (size_t)n * S;
+    double* y0 = (double*)malloc(N * sizeof(double));
+    double* y1 = (double*)malloc(N * sizeof(double));
+    double* ra = (double*)malloc(N * sizeof(double));
+    double* rb = (double*)malloc(N * sizeof(double));
+    double* val = (double*)malloc(N * sizeof(double));
+    /* chunks of ~2^16 edges or 4096 rows, claimed dynamically (hub rows are long) */
+    uint32_t cap = 1024, nc = 0;
+    uint32_t* rows = (uint32_t*)malloc(sizeof(uint32_t) * (cap + 1));
+    if (!y0 || !y1 || !ra || !rb || !val || !rows) {
+        free(y0); free(y1); free(ra); free(rb); free(val); free(rows);
+        return CPO_ENOMEM;
+    }
+    rows[0] = 0;
+    for (uint32_t v = 0; v < n;) {
+        uint32_t e = v;
+        const uint64_t start = offsets[v];
+        while (e < n && e - v < 4096 && offsets[e + 1] - start < (1u << 16)) ++e;
+        if (e == v) ++e;
+        if (nc + 1 >= cap) {
+            cap *= 2;
+            uint32_t* nr = (uint32_t*)realloc(rows, sizeof(uint32_t) * (cap + 1));
+            if (!nr) { free(y0); free(y1); free(ra); free(rb); free(val); free(rows); return CPO_ENOMEM; }
+            rows = nr;
+        }
+        rows[++nc] = e;
+        v = e;
+    }
+    /* k = 0: values = c0 * seed (:209), r_prev = seed (:211), y0 = seed * inv_deg */
+    for (uint32_t u = 0; u < n; ++u) {
+        const uint64_t d = offsets[u + 1] - offsets[u];
+        for (uint32_t s = 0; s < S; ++s) {
+            const double x = seeds[(size_t)s * n + u];
+            val[(size_t)u * S + s] = coeffs[0] * x;
+            rb[(size_t)u * S + s] = x;
+            y0[(size_t)u * S + s] = pull_y(x, d);
+        }
+    }
+    pull_job j = {n, S, offsets, nbrs, y0, y1, ra, NULL, val, 0.0, 0, rows, nc, 0};
+    pull_run(&j, n_threads); /* ra = P seed = r_cur (:212); y1 = its y */
+    double* r_prev = rb;     /* T_{k-1} */
+    double* r_cur = ra;      /* T_k */
+    double* y_cur = y1;
+    double* y_nxt = y0;
+    for (uint64_t k = 1; k < K; ++k) { /* :217-224 */
+        j.y = y_cur; j.y_next = y_nxt; j.r_prev = r_prev; j.r_cur = r_cur;
+        j.ck = coeffs[k]; j.mode = 1;
+        pull_run(&j, n_threads);
+        double* t = r_prev; r_prev = r_cur; r_cur = t; /* :222 */
+        t = y_cur; y_cur = y_nxt; y_nxt = t;
+    }
+    const double cK = coeffs[K];
+    for (uint32_t u = 0; u < n; ++u)
+        for (uint32_t s = 0; s < S; ++s) {
+            const double v = val[(size_t)u * S + s] + cK * r_cur[(size_t)u * S + s]; /* :225 */
+            values_out[(size_t)s * n + u] = v;
+        }
+    free(y0); free(y1); free(ra); free(rb); free(val); free(rows);
+    return CPO_OK;
+}
+
+/* cheby_power for S unit seeds (solvers.cpp:236-239), pull form, values[S][n]. */
+int cpo_cheby_power_pull(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs,
+                         const double* coeffs, uint64_t K, const uint32_t* sources, uint32_t S,
+                         double* values_out, int n_threads) {
+    if (S < 1 || S > 64) return CPO_EINVAL;
+    for (uint32_t s = 0; s < S; ++s)
+        if (sources[s] >= n) return CPO_EINVAL; /* solvers.cpp:28-29 */
+    double* seeds = (double*)calloc((size_t)n * S, sizeof(double));
+    if (!seeds) return CPO_ENOMEM;
+    for (uint32_t s = 0; s < S; ++s) seeds[(size_t)s * n + sources[s]] = 1.0;
+    const int rc = cpo_cheby_power_vec_pull(n, offsets, nbrs, coeffs, K, seeds, S, values_out, n_threads);
+    free(seeds);
+    return rc;
+}

@@ -162,6 +162,53 @@ def test_port_power_method_matches_ground_truth(oracle_mod):
     assert np.array_equal(Port.power_method(off, nb, z, 231, 5), g.ground_truth(PPR, 0.2, 5))
 
 
+@needs_ref
+def test_pull_oracle_matches_reference_bit_exact(oracle_mod):
+    """The row-parallel pull restatement (the checker for configs 3-5 in
+    tests/test_gpu_fullsize.py) equals the reference's scatter-order cheby_power
+    bit for bit: ring+chord graphs, a star (one hub row), a path, and a seeded
+    R-MAT / Chung-Lu graph from the generator restatement; 1, 2, 3 and 17
+    interleaved columns; 1 and 5 threads; dense seeds with zeros and signs."""
+    graphs = {f"ring{a}": Port.make_graph(*a) for a in ((25, 35, 31), (200, 300, 1), (1000, 1500, 5))}
+    graphs["star"] = Port.edges_to_csr([[0, i] for i in range(1, 300)] + [[i, i + 1] for i in range(1, 299, 3)])
+    graphs["path3"] = Port.edges_to_csr([[0, 1], [1, 2]])
+    graphs["rmat"] = Port.gen_rmat(11, 8 << 11, seed=9, n_threads=3)
+    graphs["chunglu"] = Port.gen_chunglu(5000, 40000, 2.1, 12.0, 800, seed=4, n_threads=2)
+    for name, (off, nb) in graphs.items():
+        g = RefGraph.from_csr(off, nb)
+        for fam, p, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15), (PPR, 0.02, 3), (HKPR, 1.0, 1)):
+            c = Port.cheby_coeffs(fam, p, K)
+            src = [0, g.n - 1, g.n // 2][: min(3, g.n)]
+            for cols, threads in ((src[:1], 1), (src[:2], 5), (src, 5)):
+                got = Port.cheby_power_pull(off, nb, c, K, cols, n_threads=threads)
+                for j, s in enumerate(cols):
+                    want, _, _ = g.cheby_power(fam, p, s, K)
+                    assert np.array_equal(got[j], want), (name, fam, p, s, cols, threads)
+        seeds = np.stack([Port.random_vector(g.n, 11 + j, -1.0, 1.0) for j in range(17)])
+        seeds[:, ::3] = 0.0
+        got = Port.cheby_power_vec_pull(off, nb, Port.cheby_coeffs(PPR, 0.2, 26), 26, seeds, n_threads=4)
+        for j in (0, 7, 16):
+            assert np.array_equal(got[j], g.cheby_power_vec(PPR, 0.2, seeds[j], 26)), (name, j)
+    with pytest.raises(oracle_mod.OracleError):
+        Port.cheby_power_pull(*graphs["path3"], Port.cheby_coeffs(PPR, 0.2, 3), 3, [3])
+
+
+def test_generator_restatement_equals_product_generator(oracle_mod, cpg):
+    """oracle/graphgen_port.c (the reference arm's and the checkers' graph builder, no
+    product library loaded) builds the same CSR as the product's host generator
+    (csrc/graphgen.cu, whose device build tests/test_gpu_parity.py pins to the host
+    build), for any thread count, on both models."""
+    cases = [("rmat", (12, 8 << 12), dict(seed=3)), ("rmat", (16, 8 << 16), dict(seed=1)),
+             ("rmat", (10, 3000), dict(a=0.45, b=0.15, c=0.15, seed=7)),
+             ("chunglu", (20000, 200000, 2.1, 20.0, 12000), dict(seed=4)),
+             ("chunglu", (317_080, 1_050_000, 2.5, 6.6, 0), dict(seed=2))]
+    for kind, args, kw in cases:
+        want = getattr(cpg, f"gen_{kind}")(*args, **kw)
+        for threads in (1, 3, 8):
+            got = getattr(Port, f"gen_{kind}")(*args, n_threads=threads, **kw)
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), (kind, args, threads)
+
+
 # ---- golden vectors (committed; made by tests/golden/make_golden.py) -------------------
 def test_port_matches_golden(golden):
     for fam, params in ((PPR, (0.2, 0.1, 0.02)), (HKPR, (5.0, 20.0, 40.0))):
