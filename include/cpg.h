@@ -47,6 +47,7 @@ enum {
 enum { CPG_PPR = 0, CPG_HKPR = 1 };
 
 typedef struct cpg_graph cpg_graph;
+typedef struct cpg_loopback_group cpg_loopback_group;
 
 /* SolveStats (solvers.hpp:18-25) plus device-side evidence. */
 typedef struct {
@@ -131,6 +132,21 @@ int cpg_nccl_unique_id(void* out128);
 int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n,
                              uint64_t nnz, int on_device, int device, int rank, int nranks,
                              const void* nccl_unique_id, cpg_graph** out);
+
+/* TEST HOOK (no reference counterpart): a loopback data plane that runs the
+ * nranks shards of the row-partitioned path inside ONE process on ONE device.
+ * Rank r's handle comes from cpg_graph_create_loopback(..., rank, group); the
+ * exchange steps (per-chunk all-gathers, the mass all-reduce, the result
+ * gather) become peer-buffer copies between the handles, with host barriers
+ * between the ranks' threads.  Each rank must be driven by its own host thread
+ * making the same sequence of calls, as one process per GPU would.  This runs
+ * the product's own shard layout and exchange sequence (the same code as the
+ * NCCL path up to the data plane) on a single-GPU box. */
+int cpg_loopback_group_create(int nranks, cpg_loopback_group** out);
+int cpg_loopback_group_destroy(cpg_loopback_group* grp);
+int cpg_graph_create_loopback(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n,
+                              uint64_t nnz, int on_device, int device, int rank,
+                              cpg_loopback_group* grp, cpg_graph** out);
 
 /* Host restatement of the device relabel/partition (graph_build.cu): nodes
  * ordered by (degree desc, id asc); with cr = ceil(n / (nranks*chunks)),

@@ -43,7 +43,7 @@ __all__ = [
     "parse_kernel_spec", "cheby_power", "cheby_power_vec", "cheby_power_many", "apply_walk",
     "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
     "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan", "cheby_power_topk",
-    "ingest_edges", "load_edge_list_file", "cheby_power_many_pipelined", "sync",
+    "ingest_edges", "load_edge_list_file", "cheby_power_many_pipelined", "sync", "LoopbackGroup",
 ]
 
 
@@ -244,6 +244,7 @@ class DeviceGraph:
 
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
+        self._pending = []  # host outputs of pipelined calls whose copies may be in flight
         self.info = cpg_graph_info()
         _check(L.lib().cpg_graph_info_get(self._h, ctypes.byref(self.info)))
 
@@ -272,6 +273,19 @@ class DeviceGraph:
                                                 nranks, idbuf, ctypes.byref(h)), "cpg_graph_create_sharded")
         return cls(h)
 
+    @classmethod
+    def loopback(cls, offsets, neighbors, rank: int, group: "LoopbackGroup", device: int = 0) -> "DeviceGraph":
+        """Rank ``rank``'s shard of a row-partitioned graph whose data plane is the test-only
+        loopback group (every rank on ``device`` in this process; see include/cpg.h)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _check(L.lib().cpg_graph_create_loopback(off.ctypes.data, nbr.ctypes.data, len(off) - 1, len(nbr), 0, device,
+                                                 rank, group.handle, ctypes.byref(h)), "cpg_graph_create_loopback")
+        g = cls(h)
+        g._group = group  # the group outlives its handles
+        return g
+
     @property
     def handle(self):
         return self._h
@@ -285,12 +299,34 @@ class DeviceGraph:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            L.lib().cpg_graph_destroy(self._h)
+            L.lib().cpg_graph_destroy(self._h)  # synchronises the device first
             self._h = None
+            self._pending = []
 
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class LoopbackGroup:
+    """Test-only data plane joining ``nranks`` shard handles of one process on one GPU."""
+
+    def __init__(self, nranks: int):
+        self._h = ctypes.c_void_p()
+        _check(L.lib().cpg_loopback_group_create(int(nranks), ctypes.byref(self._h)), "loopback group")
+        self.nranks = int(nranks)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                L.lib().cpg_loopback_group_destroy(self._h)
+                self._h = None
         except Exception:
             pass
 
@@ -441,12 +477,15 @@ def cheby_power_many_pipelined(g, kernel: Kernel, sources: Sequence[int], cheby_
     ptr = out.ctypes.data if isinstance(out, np.ndarray) else int(out)
     _check(L.lib().cpg_chebypower_batched_async(dg.handle, _f64p(c), K, _u32p(src), len(src), tile, ptr,
                                                 ctypes.byref(s)))
+    dg._pending.append(out)  # the copy into `out` is in flight: keep it alive until sync()
     return _to_stats(s, K)
 
 
 def sync(g, device: int = 0):
     """Wait for every result copy in flight on the graph's device handle."""
-    _check(L.lib().cpg_graph_sync(_dev(g, device).handle))
+    dg = _dev(g, device)
+    _check(L.lib().cpg_graph_sync(dg.handle))
+    dg._pending.clear()
 
 
 def cheby_power_topk(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, k: int = 50, device: int = 0):

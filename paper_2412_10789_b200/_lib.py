@@ -57,6 +57,10 @@ SIGNATURES = {
     "cpg_nccl_unique_id": (c_int, [c_void_p]),
     "cpg_graph_create_sharded": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, c_int, c_int,
                                          c_int, c_void_p, POINTER(_G)]),
+    "cpg_loopback_group_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "cpg_loopback_group_destroy": (c_int, [c_void_p]),
+    "cpg_graph_create_loopback": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, c_int, c_int, c_void_p,
+                                          POINTER(_G)]),
     "cpg_shard_plan": (c_int, [_u64p, c_uint32, c_int, c_int, _u32p, _u32p]),
     "cpg_graph_info_get": (c_int, [_G, POINTER(cpg_graph_info)]),
     "cpg_graph_destroy": (c_int, [_G]),

@@ -8,6 +8,12 @@
 //   unpermute d*acc into the caller's ids
 // Host outputs are copied on a second stream, one query behind the compute
 // stream, so D2H of query q overlaps the K steps of query q+1.
+//
+// Concurrency: the graph handle is immutable after create (like the
+// reference's Graph); every call leases a Workspace
+// (streams + buffers) from the handle's pool, so calls from several host
+// threads on one handle run concurrently.  Sharded handles keep one workspace:
+// their collectives must be issued in the same order on every rank.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,7 +23,6 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
-#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -96,8 +101,110 @@ int table_grid(const cpg_graph* g, uint32_t n_items, int occ) {
         std::max<uint64_t>(1, std::min<uint64_t>(n_items, static_cast<uint64_t>(occ) * g->sm_count)));
 }
 
+// Mass-partial rows (one per warp) of one batched launch, at most.
+size_t batch_warp_cap(const cpg_graph* g) {
+    return static_cast<size_t>(kBatchMaxCtasPerSm) * g->sm_count * (kBatchThreads / 32);
+}
+
+// ---- workspace pool ---------------------------------------------------------------------
+Workspace* ws_create(cpg_graph* g) {
+    auto w = std::make_unique<Workspace>();
+    CPG_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    CPG_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+    CPG_CUDA(cudaStreamCreateWithFlags(&w->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : w->ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    w->chunk_ev.resize(2 * static_cast<size_t>(g->chunks));
+    for (auto& e : w->chunk_ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // the per-query mass check lives in mapped pinned host memory: the host reads it
+    // without a device->host copy, which would queue behind a pipelined result copy
+    CPG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->d_mass_err), 2 * sizeof(double), cudaHostAllocMapped));
+    w->d_mass_err[0] = w->d_mass_err[1] = 0.0;
+    return w.release();
+}
+
+void free_iterates(cpg_graph* g, Workspace* w) {
+    if (g->p2p && w->win_a) {
+        nccl_sym_deregister(g->comm->nccl(), w->win_a);
+        nccl_sym_deregister(g->comm->nccl(), w->win_b);
+        nccl_sym_free(w->w_a);
+        nccl_sym_free(w->w_b);
+        w->win_a = w->win_b = nullptr;
+    } else {
+        dfree_aligned(w->w_a);
+        dfree_aligned(w->w_b);
+    }
+    w->w_a = w->w_b = nullptr;
+}
+
+void ws_destroy(cpg_graph* g, Workspace* w) {
+    if (!w) return;
+    if (w->stream) cudaStreamSynchronize(w->stream);
+    if (w->copy_stream) cudaStreamSynchronize(w->copy_stream);
+    free_iterates(g, w);
+    dfree_aligned(w->acc);
+    w->acc = nullptr;
+    for (void* p : {(void*)w->full, (void*)w->hub_partial, (void*)w->hub_count, (void*)w->bhub_partial,
+                    (void*)w->bhub_count, (void*)w->d_job_ctr, (void*)w->d_coeffs, (void*)w->d_sources,
+                    (void*)w->d_mass_partial, (void*)w->d_step_mass, (void*)w->d_mass0, (void*)w->d_seeds,
+                    (void*)w->d_stage, (void*)w->d_topk, (void*)w->d_peers_a, (void*)w->d_peers_b,
+                    (void*)w->d_barrier})
+        if (p) cudaFree(p);
+    if (w->d_mass_err) cudaFreeHost(w->d_mass_err);
+    for (auto e : w->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto e : w->chunk_ev)
+        if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {w->stream, w->copy_stream, w->comm_stream})
+        if (s) cudaStreamDestroy(s);
+    delete w;
+}
+
+// A leased workspace, returned to the pool (and its waiters woken) on scope exit.
+struct WsLease {
+    cpg_graph* g;
+    Workspace* w;
+    explicit WsLease(cpg_graph* gg) : g(gg), w(nullptr) {
+        std::unique_lock<std::mutex> lock(g->ws_mu);
+        g->ws_cv.wait(lock, [&] { return !g->ws_free.empty() || g->ws_all.size() < g->max_ws; });
+        if (!g->ws_free.empty()) {
+            w = g->ws_free.back();
+            g->ws_free.pop_back();
+            return;
+        }
+        g->ws_all.push_back(nullptr);  // reserve the slot while creating outside the lock
+        lock.unlock();
+        Workspace* nw = nullptr;
+        try {
+            DeviceGuard dg(g->device);
+            nw = ws_create(g);
+        } catch (...) {
+            std::lock_guard<std::mutex> l2(g->ws_mu);
+            g->ws_all.erase(std::find(g->ws_all.begin(), g->ws_all.end(), nullptr));
+            g->ws_cv.notify_one();
+            throw;
+        }
+        std::lock_guard<std::mutex> l2(g->ws_mu);
+        *std::find(g->ws_all.begin(), g->ws_all.end(), nullptr) = nw;
+        w = nw;
+    }
+    ~WsLease() {
+        std::lock_guard<std::mutex> lock(g->ws_mu);
+        g->ws_free.push_back(w);
+        g->ws_cv.notify_one();
+    }
+    WsLease(const WsLease&) = delete;
+    WsLease& operator=(const WsLease&) = delete;
+};
+
+size_t default_max_ws(const cpg_graph* g) {
+    if (g->comm) return 1;
+    size_t m = 4;  // device memory bounds the pool, not host threads: config 5 batched needs ~39 GB each
+    if (const char* e = std::getenv("CPG_MAX_WORKSPACES")) m = static_cast<size_t>(std::max(1, std::atoi(e)));
+    return m;
+}
+
 cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t n, uint64_t nnz, int device,
-                         int rank, int nranks, int chunks = 0) {
+                         int rank, int nranks, Comm* comm, int chunks = 0) {
     auto g = std::make_unique<cpg_graph>();
     g->device = device;
     g->rank = rank;
@@ -106,27 +213,17 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     g->n = n;
     g->nnz = nnz;
     CPG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
-    CPG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
-    CPG_CUDA(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
-    for (auto& e : g->ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    g->chunk_ev.resize(2 * static_cast<size_t>(g->chunks));
-    for (auto& e : g->chunk_ev) CPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CPG_CUDA(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device));
     build_device_graph(g.get(), d_off, d_nbr, g->stream);
-    g->hub_partial = dalloc<double>(g->n_partials);
-    g->hub_count = dalloc<unsigned int>(g->n_loc);
-    CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
     const int occ = std::max(1, step_occupancy(g->tile));
     g->step_grid = 1;  // max over chunks: the mass-partial stride
     for (const auto& t : g->tables) g->step_grid = std::max(g->step_grid, table_grid(g.get(), t.n_items, occ));
     // the split step's two grids share one mass-partial row
     g->step_grid = std::max(g->step_grid, (std::max(1, step_hubs_occupancy()) +
                                            std::max(1, step_tiles_occupancy(g->tile))) * g->sm_count);
-    // the per-query mass check lives in mapped pinned host memory: the host reads it
-    // without a device->host copy, which would queue behind a pipelined result copy
-    CPG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->d_mass_err), 2 * sizeof(double), cudaHostAllocMapped));
-    g->d_mass_err[0] = g->d_mass_err[1] = 0.0;
-    CPG_CUDA(cudaDeviceSynchronize());
+    g->comm = comm;
+    g->max_ws = default_max_ws(g.get());
+    CPG_CUDA(cudaStreamSynchronize(g->stream));
     return g.release();
 }
 
@@ -137,57 +234,44 @@ uint32_t batch_width(uint32_t tile) {
     return B;
 }
 
-// The replicated iterates as NCCL symmetric windows (p2p graphs; collective:
+// The replicated iterates (NCCL symmetric windows on p2p graphs; collective:
 // every rank calls this in the same order with the same size).
-void free_iterates(cpg_graph* g) {
-    if (g->p2p) {
-        nccl_sym_deregister(g->nccl_comm, g->win_a);
-        nccl_sym_deregister(g->nccl_comm, g->win_b);
-        nccl_sym_free(g->w_a);
-        nccl_sym_free(g->w_b);
-        g->win_a = g->win_b = nullptr;
-        g->w_a = g->w_b = nullptr;
-    } else {
-        dfree_aligned(g->w_a);
-        dfree_aligned(g->w_b);
-        g->w_a = g->w_b = nullptr;
-    }
-}
-
-void alloc_iterates(cpg_graph* g, size_t cols) {
+void alloc_iterates(cpg_graph* g, Workspace* w, size_t cols) {
     const size_t bytes = sizeof(double) * g->n_pad * cols;
     if (!g->p2p) {
-        g->w_a = static_cast<double*>(dalloc_aligned(bytes));
-        g->w_b = static_cast<double*>(dalloc_aligned(bytes));
+        w->w_a = static_cast<double*>(dalloc_aligned(bytes));
+        w->w_b = static_cast<double*>(dalloc_aligned(bytes));
         return;
     }
-    g->w_a = static_cast<double*>(nccl_sym_alloc(bytes));
-    g->w_b = static_cast<double*>(nccl_sym_alloc(bytes));
-    g->win_a = nccl_sym_register(g->nccl_comm, g->w_a, bytes);
-    g->win_b = nccl_sym_register(g->nccl_comm, g->w_b, bytes);
-    if (!g->d_peers_a) {
-        g->d_peers_a = dalloc<double*>(static_cast<size_t>(g->nranks));
-        g->d_peers_b = dalloc<double*>(static_cast<size_t>(g->nranks));
-        g->d_barrier = dalloc<double>(1);
-        CPG_CUDA(cudaMemset(g->d_barrier, 0, sizeof(double)));
+    void* nc = g->comm->nccl();
+    w->w_a = static_cast<double*>(nccl_sym_alloc(bytes));
+    w->w_b = static_cast<double*>(nccl_sym_alloc(bytes));
+    w->win_a = nccl_sym_register(nc, w->w_a, bytes);
+    w->win_b = nccl_sym_register(nc, w->w_b, bytes);
+    if (!w->d_peers_a) {
+        w->d_peers_a = dalloc<double*>(static_cast<size_t>(g->nranks));
+        w->d_peers_b = dalloc<double*>(static_cast<size_t>(g->nranks));
+        w->d_barrier = dalloc<double>(1);
+        CPG_CUDA(cudaMemset(w->d_barrier, 0, sizeof(double)));
     }
-    nccl_sym_peer_ptrs(g->win_a, g->nranks, g->d_peers_a, g->stream);
-    nccl_sym_peer_ptrs(g->win_b, g->nranks, g->d_peers_b, g->stream);
-    CPG_CUDA(cudaStreamSynchronize(g->stream));
+    nccl_sym_peer_ptrs(w->win_a, g->nranks, w->d_peers_a, w->stream);
+    nccl_sym_peer_ptrs(w->win_b, g->nranks, w->d_peers_b, w->stream);
+    CPG_CUDA(cudaStreamSynchronize(w->stream));
 }
 
-void ensure_ws(cpg_graph* g, size_t cols) {
-    if (g->ws_cols == cols) return;
-    free_iterates(g);
-    dfree_aligned(g->acc);
-    g->acc = nullptr;
-    dfree(g->full);
-    alloc_iterates(g, cols);
-    g->acc = static_cast<double*>(dalloc_aligned(sizeof(double) * g->n_loc * cols));
-    if (g->nccl_comm) g->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
-    CPG_CUDA(cudaMemset(g->w_a, 0, sizeof(double) * g->n_pad * cols));
-    CPG_CUDA(cudaMemset(g->w_b, 0, sizeof(double) * g->n_pad * cols));
-    g->ws_cols = cols;
+void ensure_ws(cpg_graph* g, Workspace* w, size_t cols) {
+    if (w->ws_cols == cols) return;
+    CPG_CUDA(cudaStreamSynchronize(w->stream));
+    free_iterates(g, w);
+    dfree_aligned(w->acc);
+    w->acc = nullptr;
+    dfree(w->full);
+    alloc_iterates(g, w, cols);
+    w->acc = static_cast<double*>(dalloc_aligned(sizeof(double) * g->n_loc * cols));
+    if (g->comm) w->full = dalloc<double>(static_cast<size_t>(g->n_pad) * cols);
+    CPG_CUDA(cudaMemset(w->w_a, 0, sizeof(double) * g->n_pad * cols));
+    CPG_CUDA(cudaMemset(w->w_b, 0, sizeof(double) * g->n_pad * cols));
+    w->ws_cols = cols;
 }
 
 // Mass-partial columns per (step, chunk) of a query group of Q queries: the
@@ -197,60 +281,58 @@ uint32_t mass_cols(const cpg_graph* g, uint32_t Q) {
     return static_cast<uint32_t>(std::max(1, step_occupancy(g->tile)) * g->sm_count);
 }
 
+void ensure_mass(Workspace* w, size_t partials, size_t steps) {
+    if (w->mass_cap < partials) {
+        dfree(w->d_mass_partial);
+        w->d_mass_partial = dalloc<double>(partials);
+        w->mass_cap = partials;
+    }
+    if (w->step_mass_cap < steps) {
+        dfree(w->d_step_mass);
+        w->d_step_mass = dalloc<double>(steps);
+        w->step_mass_cap = steps;
+    }
+}
+
 // Per-query device state for a group of Q single-source queries: hub partial
 // slots and tickets, and the mass arrays.
-void ensure_group(cpg_graph* g, uint32_t K, uint32_t Q) {
-    if (g->hub_q < Q) {
-        dfree(g->hub_partial);
-        cudaFree(g->hub_count);
-        g->hub_partial = dalloc<double>(static_cast<size_t>(g->n_partials) * Q);
-        g->hub_count = dalloc<unsigned int>(static_cast<size_t>(g->n_loc) * Q);
-        CPG_CUDA(cudaMemset(g->hub_count, 0, sizeof(unsigned int) * std::max<size_t>(1, static_cast<size_t>(g->n_loc) * Q)));
-        g->hub_q = Q;
+void ensure_group(cpg_graph* g, Workspace* w, uint32_t K, uint32_t Q) {
+    if (w->hub_q < Q) {
+        dfree(w->hub_partial);
+        dfree(w->hub_count);
+        w->hub_partial = dalloc<double>(static_cast<size_t>(g->n_partials) * Q);
+        w->hub_count = dalloc<unsigned int>(static_cast<size_t>(g->n_loc) * Q);
+        CPG_CUDA(cudaMemset(w->hub_count, 0, sizeof(unsigned int) * std::max<size_t>(1, static_cast<size_t>(g->n_loc) * Q)));
+        w->hub_q = Q;
     }
-    const size_t need = static_cast<size_t>(K) * g->chunks * mass_cols(g, Q) * Q;
-    if (g->mass_cap < need) {
-        dfree(g->d_mass_partial);
-        g->d_mass_partial = dalloc<double>(need);
-        g->mass_cap = need;
+    ensure_mass(w, static_cast<size_t>(K) * g->chunks * mass_cols(g, Q) * Q, static_cast<size_t>(K) * Q);
+}
+
+void ensure_params(Workspace* w, uint32_t K, uint32_t n_sources) {
+    if (w->coeff_cap < K + 1) {
+        dfree(w->d_coeffs);
+        w->d_coeffs = dalloc<double>(K + 1);
+        w->coeff_cap = K + 1;
     }
-    if (g->step_mass_cap < static_cast<size_t>(K) * Q) {
-        dfree(g->d_step_mass);
-        g->d_step_mass = dalloc<double>(static_cast<size_t>(K) * Q);
-        g->step_mass_cap = static_cast<size_t>(K) * Q;
+    if (w->src_cap < n_sources) {
+        dfree(w->d_sources);
+        w->d_sources = dalloc<uint32_t>(n_sources);
+        w->src_cap = n_sources;
     }
 }
 
-void ensure_params(cpg_graph* g, uint32_t K, uint32_t n_sources) {
-    if (g->coeff_cap < K + 1) {
-        dfree(g->d_coeffs);
-        g->d_coeffs = dalloc<double>(K + 1);
-        g->coeff_cap = K + 1;
-    }
-    if (g->step_mass_cap < K + 1) {
-        dfree(g->d_step_mass);
-        g->d_step_mass = dalloc<double>(K + 1);
-        g->step_mass_cap = K + 1;
-    }
-    if (g->src_cap < n_sources) {
-        dfree(g->d_sources);
-        g->d_sources = dalloc<uint32_t>(n_sources);
-        g->src_cap = n_sources;
-    }
-    const size_t need = static_cast<size_t>(K) * g->chunks * g->step_grid;
-    if (g->mass_cap < need) {
-        dfree(g->d_mass_partial);
-        g->d_mass_partial = dalloc<double>(need);
-        g->mass_cap = need;
-    }
-}
-
-void ensure_stage(cpg_graph* g, size_t doubles) {
-    if (g->stage_cap >= doubles) return;
-    CPG_CUDA(cudaStreamSynchronize(g->copy_stream));  // a pipelined copy may still read the old slots
-    dfree(g->d_stage);
-    g->d_stage = dalloc<double>(2 * doubles);
-    g->stage_cap = doubles;
+// Staging slots for host output.  A pipelined call's last copy may still be
+// reading a slot: the slots alternate across calls, and when the slot layout
+// changes (another tile or group size) the copies in flight are drained first,
+// since the new slot boundaries no longer line up with the old ones.
+void ensure_stage(Workspace* w, size_t doubles) {
+    if (w->stage_slot != doubles && w->stage_slot != 0) CPG_CUDA(cudaStreamSynchronize(w->copy_stream));
+    w->stage_slot = doubles;
+    if (w->stage_cap >= doubles) return;
+    CPG_CUDA(cudaStreamSynchronize(w->copy_stream));
+    dfree(w->d_stage);
+    w->d_stage = dalloc<double>(2 * doubles);
+    w->stage_cap = doubles;
 }
 
 void check_query(const cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t ns) {
@@ -271,35 +353,33 @@ uint32_t chunk_row0(const cpg_graph* g, uint32_t c) {
 // In-place all-gather of chunk c of a replicated [n_pad][cols] iterate on the
 // comm stream, after the chunk's step kernel (event chunk_ev[c]); the next use
 // of the iterate waits for chunk_ev[C + C-1] (the comm stream is in order).
-void gather_chunk(cpg_graph* g, double* w, uint32_t c, size_t cols, cudaStream_t st) {
-    if (!g->nccl_comm) return;
+void gather_chunk(cpg_graph* g, Workspace* w, double* v, uint32_t c, size_t cols, cudaStream_t st) {
+    if (!g->comm) return;
     const size_t C = static_cast<size_t>(g->chunks);
     const size_t R = static_cast<size_t>(g->nranks);
-    double* base = w + static_cast<size_t>(c) * R * g->cr * cols;
-    CPG_CUDA(cudaEventRecord(g->chunk_ev[c], st));
-    CPG_CUDA(cudaStreamWaitEvent(g->comm_stream, g->chunk_ev[c], 0));
-    nccl_allgather_f64(base + static_cast<size_t>(g->rank) * g->cr * cols, base, g->cr * cols, g->nccl_comm,
-                       g->comm_stream);
-    if (c + 1 == C) CPG_CUDA(cudaEventRecord(g->chunk_ev[C + c], g->comm_stream));
+    double* base = v + static_cast<size_t>(c) * R * g->cr * cols;
+    CPG_CUDA(cudaEventRecord(w->chunk_ev[c], st));
+    CPG_CUDA(cudaStreamWaitEvent(w->comm_stream, w->chunk_ev[c], 0));
+    g->comm->allgather(base + static_cast<size_t>(g->rank) * g->cr * cols, base, g->cr * cols, w->comm_stream);
+    if (c + 1 == C) CPG_CUDA(cudaEventRecord(w->chunk_ev[C + c], w->comm_stream));
 }
 
-void wait_gathers(cpg_graph* g, cudaStream_t st) {
-    if (!g->nccl_comm) return;
+void wait_gathers(cpg_graph* g, Workspace* w, cudaStream_t st) {
+    if (!g->comm) return;
     const size_t C = static_cast<size_t>(g->chunks);
-    CPG_CUDA(cudaStreamWaitEvent(st, g->chunk_ev[C + C - 1], 0));
+    CPG_CUDA(cudaStreamWaitEvent(st, w->chunk_ev[C + C - 1], 0));
 }
 
 // Final d*acc (local rows) -> full [n_pad][cols] replicated, chunk by chunk.
-const double* gather_result(cpg_graph* g, size_t cols, cudaStream_t st) {
-    if (!g->nccl_comm) return g->acc;
+const double* gather_result(cpg_graph* g, Workspace* w, size_t cols, cudaStream_t st) {
+    if (!g->comm) return w->acc;
     const size_t R = static_cast<size_t>(g->nranks);
     for (uint32_t c = 0; c < static_cast<uint32_t>(g->chunks); ++c)
-        nccl_allgather_f64(g->acc + static_cast<size_t>(c) * g->cr * cols,
-                           g->full + static_cast<size_t>(c) * R * g->cr * cols, g->cr * cols, g->nccl_comm, st);
-    return g->full;
+        g->comm->allgather(w->acc + static_cast<size_t>(c) * g->cr * cols,
+                           w->full + static_cast<size_t>(c) * R * g->cr * cols, g->cr * cols, st);
+    return w->full;
 }
 
-// The K fused steps of one query, chunk by chunk (last = write d*acc).
 // Single-source L2 residency split (CPG_HOT1_MB, default 0 = off): ids below
 // the budget are gathered evict_last, the rest evict_first.
 uint32_t single_hot_rows(const cpg_graph* g) {
@@ -315,7 +395,8 @@ bool step_split(const cpg_graph* g) {
     return e ? e[0] == '1' : g->step_split;
 }
 
-uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
+// The K fused steps of one query (group), chunk by chunk (last = write d*acc).
+uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
                    cudaStream_t st, StepProf* prof, bool taylor = false, uint32_t Q = 1) {
     uint32_t launches = 0;
     const int occ = std::max(1, step_occupancy(g->tile));
@@ -325,13 +406,13 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
         StepArgs a;
         a.rowptr = g->rowptr;
         a.col = g->col;
-        a.w_cur = (k & 1) ? g->w_a : g->w_b;
-        a.w_io = (k & 1) ? g->w_b : g->w_a;
-        a.acc = g->acc;
-        a.out = g->acc;
-        a.hub_partial = g->hub_partial;
-        a.hub_count = g->hub_count;
-        a.coeffs = g->d_coeffs;
+        a.w_cur = (k & 1) ? w->w_a : w->w_b;
+        a.w_io = (k & 1) ? w->w_b : w->w_a;
+        a.acc = w->acc;
+        a.out = w->acc;
+        a.hub_partial = w->hub_partial;
+        a.hub_count = w->hub_count;
+        a.coeffs = w->d_coeffs;
         a.tile = g->tile;
         a.hot_rows = single_hot_rows(g);
         a.k = static_cast<int>(k);
@@ -345,13 +426,13 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
         gq.part_stride = g->n_partials;
         gq.cnt_stride = g->n_loc;
         gq.mass_stride = K * C * MG;
-        if (k > 1) wait_gathers(g, st);
+        if (k > 1) wait_gathers(g, w, st);
         for (uint32_t c = 0; c < C; ++c) {
             const ItemTable& t = g->tables[c];
             a.items = t.items;
             a.n_items = t.n_items;
             a.row0 = chunk_row0(g, c);
-            a.mass_partial = g->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * MG;
+            a.mass_partial = w->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * MG;
             if (t.n_items && Q == 1 && step_split(g)) {  // hub pieces, then row tiles at higher occupancy
                 if (prof) prof->before(st);
                 StepArgs h = a;
@@ -378,37 +459,38 @@ uint32_t run_steps(cpg_graph* g, uint32_t k_first, uint32_t k_last, uint32_t K, 
                 if (prof) prof->after(st);
                 ++launches;
             }
-            gather_chunk(g, a.w_io, c, 1, st);
+            gather_chunk(g, w, a.w_io, c, 1, st);
         }
     }
-    wait_gathers(g, st);
+    wait_gathers(g, w, st);
     return launches;
 }
 
 // A group of Q single-source queries (sources q0 .. q0+Q-1) in one launch per
 // step, or one dense-seed query (seed_dev != null, Q = 1); results d*acc
 // unpermuted into d_dst[Q][n] (caller ids) if non-null.
-uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t Q, const double* seed_dev, double mass0,
-                    double* d_dst, cudaStream_t st, StepProf* prof, bool taylor = false, double gp_a = 0.0) {
+uint32_t run_single(cpg_graph* g, Workspace* w, uint32_t K, uint32_t q0, uint32_t Q, const double* seed_dev,
+                    double mass0, double* d_dst, cudaStream_t st, StepProf* prof, bool taylor = false,
+                    double gp_a = 0.0) {
     uint32_t launches = 0;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
-    ensure_group(g, K, Q);
+    ensure_group(g, w, K, Q);
     const size_t mstride = static_cast<size_t>(K) * C * mass_cols(g, Q);
-    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * Q, st));
-    CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * mstride * Q, st));
+    CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * g->n_pad * Q, st));
+    CPG_CUDA(cudaMemsetAsync(w->d_mass_partial, 0, sizeof(double) * mstride * Q, st));
     if (seed_dev)
-        launch_init_dense(g->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, gp_a, st);
+        launch_init_dense(w->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, gp_a, st);
     else
-        launch_init_onehot(g->w_a, g->n_pad, g->gdeg, g->new_of_old, g->d_sources, q0, Q, st);
+        launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, q0, Q, st);
     ++launches;
-    launches += run_steps(g, 1, K, K, true, st, prof, taylor, Q);
-    launch_mass_steps(g->d_mass_partial, C * mass_cols(g, Q), mstride, K, Q, g->d_step_mass, st);
+    launches += run_steps(g, w, 1, K, K, true, st, prof, taylor, Q);
+    launch_mass_steps(w->d_mass_partial, C * mass_cols(g, Q), mstride, K, Q, w->d_step_mass, st);
     ++launches;
-    if (g->nccl_comm) nccl_allreduce_sum_f64(g->d_step_mass, g->d_step_mass, K, g->nccl_comm, st);
-    launch_mass_err(g->d_step_mass, K * Q, mass0, g->d_mass_err, st);
+    if (g->comm) g->comm->allreduce_sum(w->d_step_mass, static_cast<size_t>(K) * Q, st);
+    launch_mass_err(w->d_step_mass, K * Q, mass0, w->d_mass_err, st);
     ++launches;
     if (d_dst) {
-        launch_unpermute(d_dst, gather_result(g, 1, st), g->n_loc, g->new_of_old, g->n, Q, g->gdeg, gp_a, st);
+        launch_unpermute(d_dst, gather_result(g, w, 1, st), g->n_loc, g->new_of_old, g->n, Q, g->gdeg, gp_a, st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
@@ -416,51 +498,62 @@ uint32_t run_single(cpg_graph* g, uint32_t K, uint32_t q0, uint32_t Q, const dou
 }
 
 // One tile of up to B sources (q0 .. q0+count) through the batched step.
-uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
-                   cudaStream_t st, StepProf* prof, const double* seeds_dev = nullptr, double gp_a = 0.0) {
+// mass0_dev: per-column conserved mass of dense seeds (null: unit seeds, 1 each;
+// mass_check false: no conservation to check, general_gp with a != 0).
+uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t q0, uint32_t count, double* d_dst,
+                   cudaStream_t st, StepProf* prof, const double* seeds_dev = nullptr, double gp_a = 0.0,
+                   const double* mass0_dev = nullptr, bool mass_check = true) {
     uint32_t launches = 0;
     const size_t cols = B;
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     const int occ = batch_occupancy();
+    const BatchTables& bt = ensure_batch_tables(g, static_cast<int>(B));
     // L2 budget for the degree-sorted hot prefix of the gathered iterate: its rows are
     // loaded evict_last, the rest evict_first.  64 MB of the 126 MB L2 measured best
     // (profiles/r01/hot_prefix_sweep.txt); CPG_HOT_MB overrides, 0 = plain loads.
     uint64_t hot_mb = 64;
     if (const char* e = std::getenv("CPG_HOT_MB")) hot_mb = static_cast<uint64_t>(std::atoll(e));
     const uint32_t hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (hot_mb << 20) / (8 * cols)));
-    CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * g->n_pad * cols, st));
+    CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * g->n_pad * cols, st));
+    // mass partials: one [B] row per warp of every launch, packed per step (the
+    // launches, and so the rows, are the same every step: `used` rows per step)
+    const size_t step_rows = static_cast<size_t>(C) * 2 * batch_warp_cap(g);
+    ensure_mass(w, static_cast<size_t>(K) * step_rows * B, static_cast<size_t>(K) * count);
+    size_t used = 0;
+    constexpr size_t W = kBatchThreads / 32;
     // Fused kernel (small graphs): warps claim jobs from a counter instead of a static
     // stride, so a warp that drew short rows takes more (CPG_DYN_JOBS=0: static).
     static const bool dyn_jobs = [] {
         const char* e = std::getenv("CPG_DYN_JOBS");
         return !e || e[0] != '0';
     }();
-    const bool use_ctr = dyn_jobs && !batch_split(g->nnz_loc);
+    const bool split = batch_split(g->nnz_loc);
+    const bool use_ctr = dyn_jobs && !split;
     if (use_ctr) {
         const size_t need = static_cast<size_t>(K) * C;
-        if (g->job_ctr_cap < need) {
-            dfree(g->d_job_ctr);
-            g->d_job_ctr = dalloc<unsigned int>(need);
-            g->job_ctr_cap = need;
+        if (w->job_ctr_cap < need) {
+            dfree(w->d_job_ctr);
+            w->d_job_ctr = dalloc<unsigned int>(need);
+            w->job_ctr_cap = need;
         }
-        CPG_CUDA(cudaMemsetAsync(g->d_job_ctr, 0, sizeof(unsigned int) * need, st));
+        CPG_CUDA(cudaMemsetAsync(w->d_job_ctr, 0, sizeof(unsigned int) * need, st));
     }
     if (seeds_dev)
-        launch_init_dense_batch(g->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
+        launch_init_dense_batch(w->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
     else
-        launch_init_onehot_batch(g->w_a, g->gdeg, g->new_of_old, g->d_sources, q0, count, B, st);
+        launch_init_onehot_batch(w->w_a, g->gdeg, g->new_of_old, w->d_sources, q0, count, B, st);
     ++launches;
     for (uint32_t k = 1; k <= K; ++k) {
         BatchArgs b;
         b.rowptr = g->rowptr;
         b.col = g->col;
-        b.w_cur = (k & 1) ? g->w_a : g->w_b;
-        b.w_io = (k & 1) ? g->w_b : g->w_a;
-        b.acc = g->acc;
-        b.out = g->acc;
-        b.hub_partial = g->bhub_partial;
-        b.hub_count = g->bhub_count;
-        b.coeffs = g->d_coeffs;
+        b.w_cur = (k & 1) ? w->w_a : w->w_b;
+        b.w_io = (k & 1) ? w->w_b : w->w_a;
+        b.acc = w->acc;
+        b.out = w->acc;
+        b.hub_partial = w->bhub_partial;
+        b.hub_count = w->bhub_count;
+        b.coeffs = w->d_coeffs;
         b.hot_rows = hot_rows;
         b.k = static_cast<int>(k);
         b.first = k == 1;
@@ -469,33 +562,38 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
         PeerArgs peer_args{nullptr, 0, 0};
         const PeerArgs* pa = nullptr;
         if (g->p2p) {  // fused all-gather: the epilogue stores into every replica
-            peer_args.peer_io = (k & 1) ? g->d_peers_b : g->d_peers_a;
+            peer_args.peer_io = (k & 1) ? w->d_peers_b : w->d_peers_a;
             peer_args.n_peer = g->nranks;
             peer_args.self = g->p2p_self ? -1 : g->rank;
             pa = &peer_args;
         }
-        if (k > 1 && !g->p2p) wait_gathers(g, st);
+        if (k > 1 && !g->p2p) wait_gathers(g, w, st);
+        size_t rows = 0;  // mass-partial rows of this step so far
+        double* const mp_step = w->d_mass_partial + static_cast<size_t>(k - 1) * step_rows * B;
         for (uint32_t c = 0; c < C; ++c) {
-            const ItemTable& t = g->btables[c];
+            const ItemTable& t = bt.tables[c];
             b.hub_items = t.items;
             b.n_hub_items = t.n_hub_items;
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
-            if (batch_split(g->nnz_loc)) {
+            if (split) {
                 // hub pieces (fused kernel with no plain rows), then the plain rows
                 if (prof) prof->before(st);
                 if (t.n_hub_items) {
                     BatchArgs h = b;
                     h.n_loc = b.hub_rows;
+                    h.mass_partial = mp_step + rows * B;
                     const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
                         1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
-                    launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
+                    rows += W * launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
                     ++launches;
                 }
                 if (t.row_end > b.hub_rows) {
-                    launch_batch_rows(b, static_cast<int>(B), occ * g->sm_count, st, pa);
+                    BatchArgs r = b;
+                    r.mass_partial = mp_step + rows * B;
+                    rows += W * launch_batch_rows(r, static_cast<int>(B), occ * g->sm_count, st, pa);
                     ++launches;
                 }
                 if (prof) prof->after(st);
@@ -503,44 +601,57 @@ uint32_t run_batch(cpg_graph* g, uint32_t K, uint32_t B, uint32_t q0, uint32_t c
                 const uint32_t jobs = t.n_hub_items + (t.row_end - b.hub_rows);
                 if (jobs) {
                     const int grid = occ * g->sm_count;
-                    if (use_ctr) b.job_ctr = g->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
+                    if (use_ctr) b.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
+                    b.mass_partial = mp_step + rows * B;
                     if (prof) prof->before(st);
-                    launch_batch(b, static_cast<int>(B), grid, st, pa);
+                    rows += W * launch_batch(b, static_cast<int>(B), grid, st, pa);
                     if (prof) prof->after(st);
                     ++launches;
                 }
             }
-            if (!g->p2p) gather_chunk(g, b.w_io, c, cols, st);
+            if (!g->p2p) gather_chunk(g, w, b.w_io, c, cols, st);
         }
+        if (rows > step_rows) fail(CPG_ECUDA, "batched mass partials overflow");
+        if (k > 1 && rows != used) fail(CPG_ECUDA, "batched launches differ between steps");
+        used = rows;
         // iteration barrier: every rank's rows of w_k are in every replica before step k+1
-        if (g->p2p) nccl_allreduce_sum_f64(g->d_barrier, g->d_barrier, 1, g->nccl_comm, st);
+        if (g->p2p) g->comm->allreduce_sum(w->d_barrier, 1, st);
     }
-    if (!g->p2p) wait_gathers(g, st);
+    if (!g->p2p) wait_gathers(g, w, st);
+    if (mass_check && count) {
+        launch_mass_steps_batch(w->d_mass_partial, static_cast<uint32_t>(step_rows), static_cast<uint32_t>(used), B, K,
+                                count, w->d_step_mass, st);
+        ++launches;
+        if (g->comm) g->comm->allreduce_sum(w->d_step_mass, static_cast<size_t>(K) * count, st);
+        launch_mass_err_cols(w->d_step_mass, K, count, mass0_dev, w->d_mass_err, st);
+        ++launches;
+    }
     if (d_dst) {
-        launch_unpermute_batch(d_dst, gather_result(g, cols, st), g->new_of_old, g->n, count, B, g->gdeg, gp_a, st);
+        launch_unpermute_batch(d_dst, gather_result(g, w, cols, st), g->new_of_old, g->n, count, B, g->gdeg, gp_a,
+                               st);
         ++launches;
     }
     CPG_CUDA(cudaGetLastError());
     return launches;
 }
 
-void upload_params(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t ns,
+void upload_params(Workspace* w, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t ns,
                    cudaStream_t st) {
-    ensure_params(g, K, std::max<uint32_t>(ns, 1));
-    CPG_CUDA(cudaMemcpyAsync(g->d_coeffs, coeffs, sizeof(double) * (K + 1), cudaMemcpyHostToDevice, st));
-    if (ns) CPG_CUDA(cudaMemcpyAsync(g->d_sources, sources, sizeof(uint32_t) * ns, cudaMemcpyHostToDevice, st));
-    launch_zero_f64(g->d_mass_err, st);
+    ensure_params(w, K, std::max<uint32_t>(ns, 1));
+    CPG_CUDA(cudaMemcpyAsync(w->d_coeffs, coeffs, sizeof(double) * (K + 1), cudaMemcpyHostToDevice, st));
+    if (ns) CPG_CUDA(cudaMemcpyAsync(w->d_sources, sources, sizeof(uint32_t) * ns, cudaMemcpyHostToDevice, st));
+    launch_zero_f64(w->d_mass_err, st);
 }
 
-void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, double wall, float dev_ms,
-                uint32_t launches, uint32_t cols) {
+void fill_stats(cpg_graph* g, Workspace* w, cpg_stats* stats, uint32_t K, uint64_t queries, double wall,
+                float dev_ms, uint32_t launches, uint32_t cols, bool mass_checked) {
     if (!stats) return;
-    const double merr = *static_cast<volatile double*>(g->d_mass_err);  // mapped; the stream was synchronized
+    const double merr = *static_cast<volatile double*>(w->d_mass_err);  // mapped; the stream was synchronized
     stats->iterations = K;
     stats->push_work = static_cast<uint64_t>(K) * g->nnz * queries;
     stats->wall_seconds = wall;
     stats->device_ms = dev_ms;
-    stats->mass_err_max = cols == 1 ? merr : 0.0;
+    stats->mass_err_max = mass_checked ? merr : std::nan("");
     const double tiles = cols == 1 ? static_cast<double>(queries) : std::ceil(static_cast<double>(queries) / cols);
     stats->bytes_model = tiles * K * cpg_bytes_per_step(g, cols);
     stats->launches = launches;
@@ -548,18 +659,16 @@ void fill_stats(cpg_graph* g, cpg_stats* stats, uint32_t K, uint64_t queries, do
     stats->step_launches = 0;
 }
 
-// Shared driver for host / device outputs.  mode 0 = one-hot single source,
-// 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources,
-// 3 = power method (Taylor), 4 = batched dense seed columns (general_gp_matrix).
 // Single-source queries per launch: enough to give every resident CTA several
 // work items when the graph alone cannot (small graphs are latency-bound at
 // one query per launch), capped at 16 and by a 2 GB workspace.  One rank only
-// (the all-gathers move one iterate).  CPG_GROUP_Q overrides (tests).
+// (the all-gathers move one iterate).  CPG_GROUP_Q overrides (tests), capped at
+// 32: the one-hot seed kernel seeds up to 32 queries of a group.
 uint32_t single_group(const cpg_graph* g, uint32_t nq) {
-    if (nq <= 1 || g->nccl_comm) return 1;
+    if (nq <= 1 || g->comm) return 1;
     uint32_t Q;
     if (const char* e = std::getenv("CPG_GROUP_Q")) {
-        Q = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+        Q = static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(e))));
     } else {
         // measured: config 1 (0.95 M edges) best at 16, config 2 (2.1 M) at 8, config 3 (86 M) at 1
         Q = static_cast<uint32_t>(std::min<uint64_t>(16, std::max<uint64_t>(1, (16ull << 20) / std::max<uint64_t>(1, g->nnz_loc))));
@@ -571,6 +680,17 @@ uint32_t single_group(const cpg_graph* g, uint32_t nq) {
     return (nq + groups - 1) / groups;
 }
 
+template <typename T>
+void ensure_buf(T*& p, size_t& cap, size_t need) {
+    if (cap >= need) return;
+    dfree(p);
+    p = dalloc<T>(need);
+    cap = need;
+}
+
+// Shared driver for host / device outputs.  mode 0 = one-hot single source,
+// 1 = dense seeds (seeds_host), 2 = batched tiles of `tile` sources,
+// 3 = power method (Taylor), 4 = batched dense seed columns (general_gp_matrix).
 int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
           uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
           cpg_stats* stats, double gp_a = 0.0, bool pipelined = false) {
@@ -584,43 +704,51 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         } else {
             check_query(g, coeffs, K, sources, nq);
         }
-        std::lock_guard<std::mutex> lock(g->mu);
+        const bool batched = mode == 2 || mode == 4;
+        if (batched) require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
         DeviceGuard dg(g->device);
+        WsLease lease(g);
+        Workspace* w = lease.w;
         const double t0 = now_s();
-        cudaStream_t st = g->stream;
+        cudaStream_t st = w->stream;
         cudaEvent_t e0, e1;
         CPG_CUDA(cudaEventCreate(&e0));
         CPG_CUDA(cudaEventCreate(&e1));
         if (user_stream) {
-            CPG_CUDA(cudaEventRecord(g->ev[4], static_cast<cudaStream_t>(user_stream)));
-            CPG_CUDA(cudaStreamWaitEvent(st, g->ev[4], 0));
+            CPG_CUDA(cudaEventRecord(w->ev[4], static_cast<cudaStream_t>(user_stream)));
+            CPG_CUDA(cudaStreamWaitEvent(st, w->ev[4], 0));
         }
-        const bool batched = mode == 2 || mode == 4;
         const uint32_t B = batched ? batch_width(tile) : 1;
         const size_t cols = B;
         if (batched) {
-            require(tile >= 1 && tile <= kBatchCols, "batched tile must be in [1, 64]");
-            ensure_batch_tables(g, static_cast<int>(B));
-            const size_t need = static_cast<size_t>(g->n_bpartials) * B;
-            if (g->bhub_items_cap < need || !g->bhub_partial) {
-                dfree(g->bhub_partial);
-                g->bhub_partial = dalloc<double>(need);
-                g->bhub_items_cap = need;
-            }
-            if (!g->bhub_count) {
-                g->bhub_count = dalloc<unsigned int>(g->n_loc);
-                CPG_CUDA(cudaMemset(g->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
+            const BatchTables& bt = ensure_batch_tables(g, static_cast<int>(B));
+            ensure_buf(w->bhub_partial, w->bhub_cap, std::max<size_t>(1, static_cast<size_t>(bt.n_bpartials) * B));
+            if (!w->bhub_count) {
+                w->bhub_count = dalloc<unsigned int>(g->n_loc);
+                CPG_CUDA(cudaMemset(w->bhub_count, 0, sizeof(unsigned int) * std::max<uint32_t>(1, g->n_loc)));
             }
         }
         const uint32_t per = batched ? tile : (mode == 0 || mode == 3) ? single_group(g, nq) : 1;
-        ensure_ws(g, batched ? cols : per);
-        upload_params(g, coeffs, K, sources, dense ? 0 : nq, st);
+        ensure_ws(g, w, batched ? cols : per);
+        upload_params(w, coeffs, K, sources, dense ? 0 : nq, st);
         const size_t n = g->n;
         const uint32_t nbatches = (nq + per - 1) / per;
         const size_t slot = n * per;  // doubles per result slot
-        double* seed_dev = nullptr;
-        if (dense) seed_dev = dalloc<double>(n * per);
-        if (!out_on_device && out) ensure_stage(g, slot);
+        if (dense) ensure_buf(w->d_seeds, w->seeds_cap, n * per);
+        // conserved mass of dense seed columns: sum of the seed (a = 0); a != 0 has none
+        const bool mass_checked = !(dense && gp_a != 0.0);
+        std::vector<double> mass0;
+        if (mode == 4 && mass_checked) {
+            mass0.resize(nq);
+            for (uint32_t q = 0; q < nq; ++q) {
+                double m = 0.0;
+                for (size_t v = 0; v < n; ++v) m += seeds_host[q * n + v];
+                mass0[q] = m;
+            }
+            ensure_buf(w->d_mass0, w->mass0_cap, std::max<size_t>(1, nq));
+            CPG_CUDA(cudaMemcpyAsync(w->d_mass0, mass0.data(), sizeof(double) * nq, cudaMemcpyHostToDevice, st));
+        }
+        if (!out_on_device && out) ensure_stage(w, slot);
         uint32_t launches = 0;
         std::unique_ptr<StepProf> prof(g_profile.load() ? new StepProf : nullptr);
         CPG_CUDA(cudaEventRecord(e0, st));
@@ -631,64 +759,67 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             if (out && out_on_device) {
                 dst = out + static_cast<size_t>(q0) * n;
             } else if (out) {
-                const uint32_t sl = (g->stage_seq + b) & 1;
-                dst = g->d_stage + sl * slot;
-                CPG_CUDA(cudaStreamWaitEvent(st, g->ev[sl], 0));  // slot free (its previous copy done)
+                const uint32_t sl = (w->stage_seq + b) & 1;
+                dst = w->d_stage + sl * slot;
+                CPG_CUDA(cudaStreamWaitEvent(st, w->ev[sl], 0));  // slot free (its previous copy done)
             }
             if (mode == 0 || mode == 3) {
-                launches += run_single(g, K, q0, count, nullptr, 1.0, dst, st, prof.get(), mode == 3);
+                launches += run_single(g, w, K, q0, count, nullptr, 1.0, dst, st, prof.get(), mode == 3);
             } else if (mode == 1) {
                 const double* sh = seeds_host + static_cast<size_t>(q0) * n;
-                double mass0 = 0.0;  // sum of the D^a-scaled seed: the conserved mass
-                for (size_t v = 0; v < n; ++v) mass0 += sh[v];
-                CPG_CUDA(cudaMemcpyAsync(seed_dev, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-                launches += run_single(g, K, q0, 1, seed_dev, gp_a == 0.0 ? mass0 : std::nan(""), dst, st, prof.get(),
-                                       false, gp_a);
+                double m0 = 0.0;  // sum of the D^a-scaled seed: the conserved mass
+                for (size_t v = 0; v < n; ++v) m0 += sh[v];
+                CPG_CUDA(cudaMemcpyAsync(w->d_seeds, sh, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+                launches += run_single(g, w, K, q0, 1, w->d_seeds, gp_a == 0.0 ? m0 : std::nan(""), dst, st,
+                                       prof.get(), false, gp_a);
             } else if (mode == 4) {
-                CPG_CUDA(cudaMemcpyAsync(seed_dev, seeds_host + static_cast<size_t>(q0) * n,
+                CPG_CUDA(cudaMemcpyAsync(w->d_seeds, seeds_host + static_cast<size_t>(q0) * n,
                                          sizeof(double) * n * count, cudaMemcpyHostToDevice, st));
-                launches += run_batch(g, K, B, q0, count, dst, st, prof.get(), seed_dev, gp_a);
+                launches += run_batch(g, w, K, B, q0, count, dst, st, prof.get(), w->d_seeds, gp_a,
+                                      mass_checked ? w->d_mass0 + q0 : nullptr, mass_checked);
             } else {
-                launches += run_batch(g, K, B, q0, count, dst, st, prof.get());
+                launches += run_batch(g, w, K, B, q0, count, dst, st, prof.get());
             }
             if (out && !out_on_device) {
                 // compute of batch b is queued; now drain batch b-1 (overlaps b's steps)
-                const uint32_t sl = (g->stage_seq + b) & 1, ps = sl ^ 1u;
-                CPG_CUDA(cudaEventRecord(g->ev[2 + sl], st));
+                const uint32_t sl = (w->stage_seq + b) & 1, ps = sl ^ 1u;
+                CPG_CUDA(cudaEventRecord(w->ev[2 + sl], st));
                 if (b >= 1) {
-                    CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + ps], 0));
+                    CPG_CUDA(cudaStreamWaitEvent(w->copy_stream, w->ev[2 + ps], 0));
                     const uint32_t pq0 = (b - 1) * per, pc = std::min<uint32_t>(per, nq - pq0);
-                    CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + ps * slot,
-                                             sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
-                    CPG_CUDA(cudaEventRecord(g->ev[ps], g->copy_stream));
+                    CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, w->d_stage + ps * slot,
+                                             sizeof(double) * n * pc, cudaMemcpyDeviceToHost, w->copy_stream));
+                    CPG_CUDA(cudaEventRecord(w->ev[ps], w->copy_stream));
                 }
             }
         }
         CPG_CUDA(cudaEventRecord(e1, st));
         if (out && !out_on_device && nbatches > 0) {
             const uint32_t b = nbatches - 1;
-            const uint32_t sl = (g->stage_seq + b) & 1;
+            const uint32_t sl = (w->stage_seq + b) & 1;
             const uint32_t pq0 = b * per, pc = std::min<uint32_t>(per, nq - pq0);
-            CPG_CUDA(cudaStreamWaitEvent(g->copy_stream, g->ev[2 + sl], 0));
-            CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, g->d_stage + sl * slot,
-                                     sizeof(double) * n * pc, cudaMemcpyDeviceToHost, g->copy_stream));
-            CPG_CUDA(cudaEventRecord(g->ev[sl], g->copy_stream));
-            g->stage_seq += nbatches;
-            if (!pipelined) CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
+            CPG_CUDA(cudaStreamWaitEvent(w->copy_stream, w->ev[2 + sl], 0));
+            CPG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(pq0) * n, w->d_stage + sl * slot,
+                                     sizeof(double) * n * pc, cudaMemcpyDeviceToHost, w->copy_stream));
+            CPG_CUDA(cudaEventRecord(w->ev[sl], w->copy_stream));
+            w->stage_seq += nbatches;
+            if (!pipelined) CPG_CUDA(cudaStreamSynchronize(w->copy_stream));
         }
         if (user_stream) {
-            CPG_CUDA(cudaEventRecord(g->ev[4], st));
-            CPG_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(user_stream), g->ev[4], 0));
+            CPG_CUDA(cudaEventRecord(w->ev[4], st));
+            CPG_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(user_stream), w->ev[4], 0));
         }
         float ms = 0.f;
         if (!user_stream || stats) {
-            CPG_CUDA(cudaStreamSynchronize(st));
+            if (g->comm)
+                g->comm->sync(st);  // polls the communicator's async error
+            else
+                CPG_CUDA(cudaStreamSynchronize(st));
             CPG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        if (seed_dev) cudaFree(seed_dev);
-        fill_stats(g, stats, K, nq, now_s() - t0, ms, launches, batched ? tile : 1u);
+        fill_stats(g, w, stats, K, nq, now_s() - t0, ms, launches, batched ? tile : 1u, mass_checked);
         if (stats && prof) {
             stats->step_ms = prof->total_ms();
             stats->step_launches = static_cast<uint32_t>(prof->ev.size() / 2);
@@ -712,11 +843,11 @@ int cpg_graph_create(const uint64_t* offsets, const uint32_t* neighbors, uint32_
         DeviceGuard dg(device);
         uint64_t* d_off = dalloc<uint64_t>(static_cast<size_t>(n) + 1);
         uint32_t* d_nbr = dalloc<uint32_t>(nnz);
-        CPG_CUDA(cudaMemcpy(d_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyHostToDevice));
-        CPG_CUDA(cudaMemcpy(d_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
         cpg_graph* g = nullptr;
         try {
-            g = create_common(d_off, d_nbr, n, nnz, device, 0, 1);
+            CPG_CUDA(cudaMemcpy(d_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyHostToDevice));
+            CPG_CUDA(cudaMemcpy(d_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+            g = create_common(d_off, d_nbr, n, nnz, device, 0, 1, nullptr);
         } catch (...) {
             cudaFree(d_off);
             cudaFree(d_nbr);
@@ -735,7 +866,7 @@ int cpg_graph_create_device(const uint64_t* d_offsets, const uint32_t* d_neighbo
         require(d_offsets && d_neighbors && out, "null argument");
         require(n > 0, "empty graph");
         DeviceGuard dg(device);
-        *out = create_common(d_offsets, d_neighbors, n, nnz, device, 0, 1);
+        *out = create_common(d_offsets, d_neighbors, n, nnz, device, 0, 1, nullptr);
     });
 }
 
@@ -746,45 +877,49 @@ int cpg_nccl_unique_id(void* out128) {
     });
 }
 
-int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
-                             int on_device, int device, int rank, int nranks, const void* nccl_unique_id,
-                             cpg_graph** out) {
+} // extern "C"
+
+namespace {
+// Shared tail of the sharded constructors: CSR to the device if needed, the
+// shard of `rank`, and the data plane (made by make_comm; owned by the graph).
+template <typename MakeComm>
+int create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz, int on_device,
+                   int device, int rank, int nranks, bool allow_p2p, MakeComm make_comm, cpg_graph** out) {
     return guarded([&] {
         require(offsets && neighbors && out, "null argument");
         require(n > 0, "empty graph");
         require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank/nranks");
-        require(nranks == 1 || nccl_unique_id != nullptr, "sharded graph needs an NCCL unique id");
         DeviceGuard dg(device);
         const uint64_t* d_off = offsets;
         const uint32_t* d_nbr = neighbors;
         uint64_t* t_off = nullptr;
         uint32_t* t_nbr = nullptr;
-        if (!on_device) {
-            t_off = dalloc<uint64_t>(static_cast<size_t>(n) + 1);
-            t_nbr = dalloc<uint32_t>(nnz);
-            CPG_CUDA(cudaMemcpy(t_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyHostToDevice));
-            CPG_CUDA(cudaMemcpy(t_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
-            d_off = t_off;
-            d_nbr = t_nbr;
-        }
         cpg_graph* g = nullptr;
-        void* comm = nullptr;
+        Comm* comm = nullptr;
         try {
-            // NCCL whenever an id is given (also for one rank: exercises the collective path)
-            if (nccl_unique_id) comm = nccl_comm_init(nccl_unique_id, nranks, rank);
+            if (!on_device) {
+                t_off = dalloc<uint64_t>(static_cast<size_t>(n) + 1);
+                t_nbr = dalloc<uint32_t>(nnz);
+                CPG_CUDA(cudaMemcpy(t_off, offsets, sizeof(uint64_t) * (static_cast<size_t>(n) + 1),
+                                    cudaMemcpyHostToDevice));
+                CPG_CUDA(cudaMemcpy(t_nbr, neighbors, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+                d_off = t_off;
+                d_nbr = t_nbr;
+            }
+            comm = make_comm();
             // CPG_P2P=1: fused all-gather through NCCL symmetric windows when the
             // NCCL in the process has the device API and all ranks share one
             // NVLink domain (one chunk: no separate collective to overlap)
             const char* pe = std::getenv("CPG_P2P");
-            const bool p2p = comm && pe && pe[0] == '1' && nccl_sym_supported(comm, nranks, rank);
-            g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks,
+            const bool p2p = allow_p2p && comm && comm->nccl() && pe && pe[0] == '1' &&
+                             nccl_sym_supported(comm->nccl(), nranks, rank);
+            g = create_common(d_off, d_nbr, n, nnz, device, rank, nranks, comm,
                               p2p && !std::getenv("CPG_CHUNKS") ? 1 : 0);
-            g->nccl_comm = comm;
-            comm = nullptr;
+            comm = nullptr;  // owned by g
             g->p2p = p2p;
             if (const char* ps = std::getenv("CPG_P2P_SELF")) g->p2p_self = ps[0] == '1';
         } catch (...) {
-            if (comm) nccl_comm_destroy(comm);
+            delete comm;
             if (t_off) cudaFree(t_off);
             if (t_nbr) cudaFree(t_nbr);
             if (g) cpg_graph_destroy(g);
@@ -794,6 +929,41 @@ int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors,
         if (t_nbr) cudaFree(t_nbr);
         *out = g;
     });
+}
+} // namespace
+
+extern "C" {
+
+int cpg_graph_create_sharded(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                             int on_device, int device, int rank, int nranks, const void* nccl_unique_id,
+                             cpg_graph** out) {
+    if (nranks > 1 && !nccl_unique_id) {
+        return guarded([&] { fail(CPG_EINVAL, "sharded graph needs an NCCL unique id"); });
+    }
+    // NCCL whenever an id is given (also for one rank: exercises the collective path)
+    return create_sharded(offsets, neighbors, n, nnz, on_device, device, rank, nranks, true,
+                          [&]() -> Comm* { return nccl_unique_id ? make_nccl_comm(nccl_unique_id, nranks, rank) : nullptr; },
+                          out);
+}
+
+int cpg_loopback_group_create(int nranks, cpg_loopback_group** out) {
+    return guarded([&] {
+        require(out && nranks >= 1 && nranks <= 64, "loopback: 1..64 ranks and an output pointer");
+        *out = reinterpret_cast<cpg_loopback_group*>(loopback_group_create(nranks));
+    });
+}
+
+int cpg_loopback_group_destroy(cpg_loopback_group* grp) {
+    return guarded([&] { loopback_group_destroy(reinterpret_cast<LoopbackGroup*>(grp)); });
+}
+
+int cpg_graph_create_loopback(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                              int on_device, int device, int rank, cpg_loopback_group* grp, cpg_graph** out) {
+    auto* lg = reinterpret_cast<LoopbackGroup*>(grp);
+    if (!lg) return guarded([&] { fail(CPG_EINVAL, "loopback: null group"); });
+    const int nranks = loopback_group_size(lg);
+    return create_sharded(offsets, neighbors, n, nnz, on_device, device, rank, nranks, false,
+                          [&]() -> Comm* { return make_loopback_comm(lg, rank); }, out);
 }
 
 int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info) {
@@ -822,32 +992,23 @@ int cpg_graph_destroy(cpg_graph* g) {
     return guarded([&] {
         DeviceGuard dg(g->device);
         cudaDeviceSynchronize();
-        if (g->p2p) {  // windows are deregistered through the communicator, before it goes
-            free_iterates(g);
-            for (void* p : {(void*)g->d_peers_a, (void*)g->d_peers_b, (void*)g->d_barrier})
-                if (p) cudaFree(p);
+        {
+            std::lock_guard<std::mutex> lock(g->ws_mu);
+            for (Workspace* w : g->ws_all) ws_destroy(g, w);  // p2p windows go through the communicator first
+            g->ws_all.clear();
+            g->ws_free.clear();
         }
-        if (g->nccl_comm) nccl_comm_destroy(g->nccl_comm);
+        delete g->comm;
+        g->comm = nullptr;
         for (auto& t : g->tables) cudaFree(t.items);
-        for (auto& t : g->btables)
-            if (t.items) cudaFree(t.items);
-        for (auto e : g->chunk_ev)
-            if (e) cudaEventDestroy(e);
-        if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
-        if (!g->p2p) free_iterates(g);
-        for (void* p : {(void*)g->rowptr, (void*)g->col, (void*)g->acc})
+        for (auto& kv : g->btabs)
+            for (auto& t : kv.second.tables)
+                if (t.items) cudaFree(t.items);
+        for (void* p : {(void*)g->rowptr, (void*)g->col})
             dfree_aligned(p);
-        for (void* p : {(void*)g->gdeg, (void*)g->new_of_old,
-                        (void*)g->hub_partial, (void*)g->hub_count, (void*)g->bhub_partial,
-                        (void*)g->bhub_count, (void*)g->d_job_ctr, (void*)g->full,
-                        (void*)g->d_coeffs, (void*)g->d_sources, (void*)g->d_mass_partial,
-                        (void*)g->d_step_mass, (void*)g->d_stage})
+        for (void* p : {(void*)g->gdeg, (void*)g->new_of_old})
             if (p) cudaFree(p);
-        if (g->d_mass_err) cudaFreeHost(g->d_mass_err);
-        for (auto e : g->ev)
-            if (e) cudaEventDestroy(e);
         if (g->stream) cudaStreamDestroy(g->stream);
-        if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
         delete g;
     });
 }
@@ -880,10 +1041,17 @@ int cpg_chebypower_batched_async(cpg_graph* g, const double* coeffs, uint32_t K,
 int cpg_graph_sync(cpg_graph* g) {
     return guarded([&] {
         require(g != nullptr, "null graph handle");
-        std::lock_guard<std::mutex> lock(g->mu);
         DeviceGuard dg(g->device);
-        CPG_CUDA(cudaStreamSynchronize(g->copy_stream));
-        CPG_CUDA(cudaStreamSynchronize(g->stream));
+        std::vector<Workspace*> all;
+        {
+            std::lock_guard<std::mutex> lock(g->ws_mu);
+            all = g->ws_all;
+        }
+        for (Workspace* w : all) {
+            if (!w) continue;
+            CPG_CUDA(cudaStreamSynchronize(w->copy_stream));
+            CPG_CUDA(cudaStreamSynchronize(w->stream));
+        }
     });
 }
 
@@ -912,36 +1080,46 @@ int cpg_power_method(cpg_graph* g, const double* zeta, uint32_t n_steps, const u
 
 // Queries ranked on the device: only the top-k (caller id, score) pairs per
 // source come back (the reference ranks on the host, tools/chebyprop.cpp:148-156).
+// Sources run in groups (one device-resident [Q][n] result buffer per group) and
+// each result column is ranked on the device while the next group computes.
 int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, uint32_t n_sources,
                         uint32_t k, uint32_t* ids, double* vals, cpg_stats* stats) {
     return guarded([&] {
         check_query(g, coeffs, K, sources, n_sources);
         require(k >= 1 && ids && vals, "topk: k >= 1 and output arrays required");
         const uint32_t kk = std::min(k, g->n);
-        double* d_res = nullptr;
-        {
-            DeviceGuard dg(g->device);
-            d_res = dalloc<double>(g->n);
-        }
+        DeviceGuard dg(g->device);
+        // group size: the single-source grouping rule, bounded by a 2 GB result buffer
+        const uint32_t Q = std::max<uint32_t>(
+            1, std::min<uint32_t>(single_group(g, n_sources),
+                                  static_cast<uint32_t>(std::max<uint64_t>(1, (2ull << 30) / (8ull * g->n)))));
+        double* d_res = dalloc<double>(static_cast<size_t>(g->n) * Q);
+        cudaStream_t st = nullptr;
         cpg_stats acc{};
-        for (uint32_t q = 0; q < n_sources; ++q) {
-            cpg_stats st{};
-            const int rc = drive(g, coeffs, K, sources + q, nullptr, 1, 1, 0, d_res, true, nullptr, &st);
-            if (rc != CPG_OK) {
-                cudaFree(d_res);
-                fail(rc, cpg_last_error());
+        try {
+            CPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            for (uint32_t q0 = 0; q0 < n_sources; q0 += Q) {
+                const uint32_t cnt = std::min(Q, n_sources - q0);
+                cpg_stats s{};
+                const int rc = drive(g, coeffs, K, sources + q0, nullptr, cnt, 1, 0, d_res, true, st, &s);
+                if (rc != CPG_OK) fail(rc, cpg_last_error());
+                for (uint32_t j = 0; j < cnt; ++j)
+                    device_topk(d_res + static_cast<size_t>(j) * g->n, g->n, kk,
+                                ids + static_cast<size_t>(q0 + j) * kk, vals + static_cast<size_t>(q0 + j) * kk, st);
+                acc.iterations = s.iterations;
+                acc.push_work += s.push_work;
+                acc.wall_seconds += s.wall_seconds;
+                acc.device_ms += s.device_ms;
+                acc.mass_err_max = std::max(acc.mass_err_max, s.mass_err_max);
+                acc.bytes_model += s.bytes_model;
+                acc.launches += s.launches;
             }
-            DeviceGuard dg(g->device);
-            device_topk(d_res, g->n, kk, ids + static_cast<size_t>(q) * kk, vals + static_cast<size_t>(q) * kk,
-                        g->stream);
-            acc.iterations = st.iterations;
-            acc.push_work += st.push_work;
-            acc.wall_seconds += st.wall_seconds;
-            acc.device_ms += st.device_ms;
-            acc.mass_err_max = std::max(acc.mass_err_max, st.mass_err_max);
-            acc.bytes_model += st.bytes_model;
-            acc.launches += st.launches;
+        } catch (...) {
+            if (st) cudaStreamDestroy(st);
+            cudaFree(d_res);
+            throw;
         }
+        cudaStreamDestroy(st);
         cudaFree(d_res);
         if (stats) *stats = acc;
     });
@@ -966,21 +1144,23 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
     return guarded([&] {
         check_query(g, coeffs, K, &source, 1);
         require(g->nranks == 1, "trace is single-GPU only");
-        std::lock_guard<std::mutex> lock(g->mu);
         DeviceGuard dg(g->device);
-        cudaStream_t st = g->stream;
-        ensure_ws(g, 1);
-        upload_params(g, coeffs, K, &source, 1, st);
+        WsLease lease(g);
+        Workspace* w = lease.w;
+        cudaStream_t st = w->stream;
+        ensure_ws(g, w, 1);
+        ensure_group(g, w, K, 1);
+        upload_params(w, coeffs, K, &source, 1, st);
         const size_t n = g->n, np = g->n_pad;
         std::vector<uint32_t> no(n), gdeg(np);
         CPG_CUDA(cudaMemcpy(no.data(), g->new_of_old, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
         CPG_CUDA(cudaMemcpy(gdeg.data(), g->gdeg, sizeof(uint32_t) * np, cudaMemcpyDeviceToHost));
-        std::vector<double> w(np), acc(np);
-        auto emit = [&](uint32_t k, const double* wv, const double* av, double a_scale) {
+        std::vector<double> wv(np), acc(np);
+        auto emit = [&](uint32_t k, const double* wk, const double* av, double a_scale) {
             for (size_t v = 0; v < n; ++v) {
                 const uint32_t gv = no[v];
                 const double d = static_cast<double>(gdeg[gv]);
-                if (r_trace) r_trace[k * n + v] = d * wv[gv];
+                if (r_trace) r_trace[k * n + v] = d * wk[gv];
                 if (est_trace) est_trace[k * n + v] = a_scale * d * av[gv];
             }
         };
@@ -989,17 +1169,17 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
             if (r_trace) r_trace[v] = v == source ? 1.0 : 0.0;
             if (est_trace) est_trace[v] = v == source ? coeffs[0] : 0.0;
         }
-        CPG_CUDA(cudaMemsetAsync(g->w_a, 0, sizeof(double) * np, st));
-        launch_init_onehot(g->w_a, g->n_pad, g->gdeg, g->new_of_old, g->d_sources, 0, 1, st);
-        CPG_CUDA(cudaMemsetAsync(g->d_mass_partial, 0, sizeof(double) * K * g->chunks * g->step_grid, st));
+        CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * np, st));
+        launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, 0, 1, st);
+        CPG_CUDA(cudaMemsetAsync(w->d_mass_partial, 0, sizeof(double) * K * g->chunks * g->step_grid, st));
         for (uint32_t k = 1; k <= K; ++k) {
-            run_steps(g, k, k, K, false, st, nullptr);
+            run_steps(g, w, k, k, K, false, st, nullptr);
             CPG_CUDA(cudaGetLastError());
-            const double* w_io = (k & 1) ? g->w_b : g->w_a;
-            CPG_CUDA(cudaMemcpyAsync(w.data(), w_io, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
-            CPG_CUDA(cudaMemcpyAsync(acc.data(), g->acc, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+            const double* w_io = (k & 1) ? w->w_b : w->w_a;
+            CPG_CUDA(cudaMemcpyAsync(wv.data(), w_io, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+            CPG_CUDA(cudaMemcpyAsync(acc.data(), w->acc, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
             CPG_CUDA(cudaStreamSynchronize(st));
-            emit(k, w.data(), acc.data(), 1.0);
+            emit(k, wv.data(), acc.data(), 1.0);
             if (k == K && out)
                 for (size_t v = 0; v < n; ++v) out[v] = static_cast<double>(gdeg[no[v]]) * acc[no[v]];
         }

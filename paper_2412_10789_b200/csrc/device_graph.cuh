@@ -32,6 +32,7 @@ constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per 
 // Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
 constexpr int kBatchCols = 64;
 constexpr int kBatchThreads = 256;
+constexpr int kBatchMaxCtasPerSm = 6;            // grid cap of every batched launch (mass-partial sizing)
 constexpr int kBatchHubEdges = 2048;             // B = 64: rows above this are split
 // Hub piece in the fused batched kernel (small graphs): rows above this many
 // edges are split into pieces of this length.  One row slot (B/2 lanes) works
@@ -121,6 +122,7 @@ struct BatchArgs {
     uint32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last); 0 = off
     int k, first, last;
     unsigned int* job_ctr;      // fused kernel: zeroed job counter (warps claim RPW jobs each); null = static stride
+    double* mass_partial;       // [gridDim.x * warps][B] per-warp column sums of d_v w_{k+1}(v) (acceptance C13); null = off
 };
 
 // Fused all-gather (second parameter of the PEER instances of the batched

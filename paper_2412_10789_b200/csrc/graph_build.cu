@@ -384,29 +384,32 @@ void dfree_aligned(void* p) {
     cudaFree(base);
 }
 
-void ensure_batch_tables(cpg_graph* g, int B) {
+const BatchTables& ensure_batch_tables(cpg_graph* g, int B) {
     const bool split = batch_split(g->nnz_loc);  // piece length depends on the kernel that runs them
-    if (!g->btables.empty() && g->bitems_width == B && g->bitems_split == split) return;
-    for (auto& t : g->btables)
-        if (t.items) cudaFree(t.items);
-    g->btables.clear();
+    const int key = B * 2 + (split ? 1 : 0);
+    std::lock_guard<std::mutex> lock(g->tab_mu);
+    auto it = g->btabs.find(key);
+    if (it != g->btabs.end()) return it->second;
+    BatchTables bt;
     uint32_t slots = 0;
     const uint32_t C = static_cast<uint32_t>(std::max(1, g->chunks));
     const int64_t hb = split ? batch_piece_edges(B) : batch_hub_edges(B);
+    cudaStream_t st = nullptr;
+    CPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     for (uint32_t c = 0; c < C; ++c) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
-        build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0,
-                        g->stream);
+        build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0, st);
         t.n_items = t.n_hub_items;
         slots += t.n_hub_items;
-        g->btables.push_back(t);
+        bt.tables.push_back(t);
     }
-    g->n_bpartials = slots;
-    g->bitems_width = B;
-    g->bitems_split = split;
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    bt.n_bpartials = slots;
     CPG_CUDA(cudaGetLastError());
+    return g->btabs.emplace(key, std::move(bt)).first->second;
 }
 
 } // namespace cpg

@@ -7,8 +7,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 
 #include "cpg_graph.hpp"
@@ -26,6 +28,8 @@ struct NcclApi {
                                cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
+    ncclResult_t (*get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*comm_abort)(ncclComm_t) = nullptr;
 };
 
 NcclApi& api() {
@@ -45,6 +49,8 @@ NcclApi& api() {
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.h, "ncclAllReduce"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.h, "ncclCommDestroy"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.h, "ncclGetErrorString"));
+        a.get_async_error = reinterpret_cast<decltype(a.get_async_error)>(dlsym(a.h, "ncclCommGetAsyncError"));
+        a.comm_abort = reinterpret_cast<decltype(a.comm_abort)>(dlsym(a.h, "ncclCommAbort"));
     });
     if (!a.h || !a.get_unique_id || !a.comm_init_rank || !a.all_gather || !a.all_reduce)
         fail(CPG_ENCCL, "libnccl.so.2 not loadable: " + std::string(dlerror() ? dlerror() : "missing symbols"));
@@ -82,8 +88,57 @@ void nccl_allreduce_sum_f64(const double* send, double* recv, size_t count, void
           "ncclAllReduce");
 }
 
+// Asynchronous communicator errors (a peer died, a network failure): polled
+// while a sharded query waits for its stream, so a dead peer surfaces as
+// CPG_ENCCL instead of a hang.  On error the communicator is aborted, which
+// releases the kernels blocked in it.
+void nccl_check_async(void* comm) {
+    if (!comm || !api().get_async_error) return;
+    ncclResult_t st = ncclSuccess;
+    const ncclResult_t r = api().get_async_error(static_cast<ncclComm_t>(comm), &st);
+    if (r == ncclSuccess && (st == ncclSuccess || st == ncclInProgress)) return;
+    const ncclResult_t bad = r != ncclSuccess ? r : st;
+    fail(CPG_ENCCL, std::string("NCCL communicator failed: ") + (api().error_string ? api().error_string(bad) : "error"));
+}
+
 void nccl_comm_destroy(void* comm) {
     if (comm && api().comm_destroy) api().comm_destroy(static_cast<ncclComm_t>(comm));
+}
+
+namespace {
+struct NcclComm final : Comm {
+    void* c = nullptr;
+    ~NcclComm() override { nccl_comm_destroy(c); }
+    void allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+        nccl_allgather_f64(send, recv, count, c, st);
+    }
+    void allreduce_sum(double* buf, size_t count, cudaStream_t st) override {
+        nccl_allreduce_sum_f64(buf, buf, count, c, st);
+    }
+    void sync(cudaStream_t st) override {
+        for (;;) {
+            const cudaError_t e = cudaStreamQuery(st);
+            if (e == cudaSuccess) return;
+            if (e != cudaErrorNotReady) CPG_CUDA(e);
+            nccl_check_async(c);
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    void* nccl() override { return c; }
+};
+} // namespace
+
+Comm* make_nccl_comm(const void* id128, int nranks, int rank) {
+    auto* m = new NcclComm;
+    try {
+        m->c = nccl_comm_init(id128, nranks, rank);
+    } catch (...) {
+        delete m;
+        throw;
+    }
+    m->rank = rank;
+    m->nranks = nranks;
+    return m;
 }
 
 } // namespace cpg

@@ -465,6 +465,47 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
     return j;
 }
 
+// Per-warp column sums of the mass (acceptance C13): every lane accumulates its
+// two columns in its own shared-memory cells, mcells[warp][row slot][column]
+// (one owner per cell: no atomics, no registers held across the row loop, no
+// CTA barrier).  At the end lane l of each warp sums its columns over the
+// warp's row slots into the warp's partial row; the warp order of the final
+// sum is fixed (mass_steps_batch_kernel), so with a static job stride the
+// value is reproducible run to run.
+template <int B>
+__device__ __forceinline__ double* batch_mass_cell() {
+    __shared__ double mcells[kBatchThreads / 32][64];  // [warp][slot * B + column], RPW * B = 64
+    const int lane = threadIdx.x & 31;
+    return &mcells[threadIdx.x >> 5][(lane / (B / 2)) * B + 2 * (lane % (B / 2))];
+}
+
+template <int B>
+__device__ __forceinline__ void batch_mass_init() {
+    double* c = batch_mass_cell<B>();
+    c[0] = 0.0;
+    c[1] = 0.0;
+}
+
+template <int B>
+__device__ __forceinline__ void batch_mass_flush(const BatchArgs& a) {
+    if (!a.mass_partial) return;  // uniform over the launch
+    constexpr int L = B / 2;
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (lane < L) {  // lane l sums its warp's row slots for columns 2l, 2l+1 (warp barrier only)
+        const double* c = batch_mass_cell<B>();  // slot 0 cells of this lane's columns
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 64 / B; ++r) {
+            s0 += c[r * B];
+            s1 += c[r * B + 1];
+        }
+        double* dst = a.mass_partial + (static_cast<size_t>(blockIdx.x) * (kBatchThreads / 32) + (threadIdx.x >> 5)) * B;
+        dst[2 * lane] = s0;
+        dst[2 * lane + 1] = s1;
+    }
+}
+
 template <int B, bool PEER = false>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArgs& pa, uint32_t r, double2 y,
                                                int64_t d, int cl, double2 wp, double2 ac) {
@@ -484,6 +525,11 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArg
             acc_new.x = ac.x + ck * w_new.x;
             acc_new.y = ac.y + ck * w_new.y;
         }
+        // sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v), per column: this lane's own
+        // shared-memory cells (no registers held across the row loop)
+        double* mcell = batch_mass_cell<B>();
+        mcell[0] += dd * w_new.x;
+        mcell[1] += dd * w_new.y;
     }
     reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl] = w_new;
     if (PEER) {  // fused all-gather: the row into every other rank's replica (NVLink stores)
@@ -540,6 +586,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 #endif
     constexpr uint32_t CLAIM = RPW > CPG_CLAIM_ROWS ? RPW : (CPG_CLAIM_ROWS / RPW) * RPW;
     unsigned int* const ctr = a.job_ctr;
+    batch_mass_init<B>();
     uint32_t claim_end = 0;
     uint32_t base_job = wg * RPW;
     if (ctr) {
@@ -627,6 +674,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
         }
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
+    batch_mass_flush<B>(a);
 }
 
 // Plain-row batched step (rows [hub_rows, n_loc) of the chunk; hub pieces run
@@ -661,6 +709,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
         }
     };
     load_chunk(e0, e1);
+    batch_mass_init<B>();
     while (__any_sync(0xffffffffu, r < r_end)) {
         const uint32_t rn = r + stride;
         int64_t ne0 = 0, ne1 = 0;
@@ -714,6 +763,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
         e1 = ne1;
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
+    batch_mass_flush<B>(a);
 }
 
 // Hub-piece batched step (split path): the jobs are the hub pieces of the
@@ -762,6 +812,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     int64_t e0, e1;
     load_item(job, r, sb, e0, e1);
     load_chunk(c, e0, e1);
+    batch_mass_init<B>();
     while (__any_sync(0xffffffffu, job < n_jobs)) {
         uint32_t nr, nsb;
         int64_t ne0, ne1;
@@ -832,6 +883,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         e1 = ne1;
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
+    batch_mass_flush<B>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -937,6 +989,31 @@ __global__ void mass_err_kernel(const double* steps, uint32_t K, double mass0, d
     *err = worst;
 }  // (over all K*count entries of a query group: called with K*count)
 
+// Batched: steps[j*K + k] = sum_{i < used} mp[(k*stride + i)*B + j] for the
+// count live columns (i over the step's warp rows in launch order; one CTA
+// per (k, j); fixed order).
+__global__ void mass_steps_batch_kernel(const double* mp, uint32_t stride, uint32_t used, uint32_t B, uint32_t K,
+                                        double* steps) {
+    __shared__ double red[kStepThreads / 32];
+    const uint32_t k = blockIdx.x, j = blockIdx.y;
+    double s = 0.0;
+    for (uint32_t i = threadIdx.x; i < used; i += blockDim.x)
+        s += mp[(static_cast<size_t>(k) * stride + i) * B + j];
+    s = block_sum<kStepThreads>(s, red);
+    if (threadIdx.x == 0) steps[static_cast<size_t>(j) * K + k] = s;
+}
+
+// err = max(err, max_{j,k} |steps[j*K + k] - mass0[j]|) (mass0 null: 1 for every column).
+__global__ void mass_err_cols_kernel(const double* steps, uint32_t K, uint32_t count, const double* mass0,
+                                     double* err) {
+    double worst = *err;
+    for (uint32_t j = 0; j < count; ++j) {
+        const double m0 = mass0 ? mass0[j] : 1.0;
+        for (uint32_t k = 0; k < K; ++k) worst = fmax(worst, fabs(steps[static_cast<size_t>(j) * K + k] - m0));
+    }
+    *err = worst;
+}
+
 // Host-side launch wrappers ---------------------------------------------------
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq) {
     const bool group = gq && gq->nq > 1;
@@ -999,33 +1076,35 @@ int step_occupancy(int tile) {  // same for both instances (64 registers, same s
     return blocks;
 }
 template <int B, int U, int MINB>
-void launch_slot(const BatchArgs& a, cudaStream_t st) {
+int launch_slot(const BatchArgs& a, cudaStream_t st) {
     int occ = 0, sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cheby_batch_kernel<B, U, MINB>, kBatchThreads, 0);
-    cheby_batch_kernel<B, U, MINB><<<occ * sms, kBatchThreads, 0, st>>>(a, PeerArgs{});
+    const int grid = std::max(1, std::min(occ, kBatchMaxCtasPerSm)) * sms;
+    cheby_batch_kernel<B, U, MINB><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{});
+    return grid;
 }
 
 template <int B>
-bool launch_slot_b(const BatchArgs& a, int cfg, cudaStream_t st) {
+int launch_slot_b(const BatchArgs& a, int cfg, cudaStream_t st) {
     switch (cfg) {
-    case 41: launch_slot<B, 4, 4>(a, st); return true;
-    case 45: launch_slot<B, 4, 5>(a, st); return true;
-    case 46: launch_slot<B, 4, 6>(a, st); return true;
-    case 64: launch_slot<B, 6, 4>(a, st); return true;
-    case 84: launch_slot<B, 8, 4>(a, st); return true;
-    case 85: launch_slot<B, 8, 5>(a, st); return true;
-    default: return false;
+    case 41: return launch_slot<B, 4, 4>(a, st);
+    case 45: return launch_slot<B, 4, 5>(a, st);
+    case 46: return launch_slot<B, 4, 6>(a, st);
+    case 64: return launch_slot<B, 6, 4>(a, st);
+    case 84: return launch_slot<B, 8, 4>(a, st);
+    case 85: return launch_slot<B, 8, 5>(a, st);
+    default: return 0;
     }
 }
 
-bool launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
+int launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
     switch (B) {
     case 16: return launch_slot_b<16>(a, cfg, st);
     case 32: return launch_slot_b<32>(a, cfg, st);
     case 64: return launch_slot_b<64>(a, cfg, st);
-    default: return false;
+    default: return 0;
     }
 }
 
@@ -1039,16 +1118,17 @@ bool launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
     default: KERNEL<64, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                          \
     }
 
-void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_kernel, B, grid, st, a, *pa);
-        return;
+        return grid;
     }
     static const int cfg = [] {  // tuning hook: CPG_SLOT_CFG = U*10 + MINB
         const char* e = std::getenv("CPG_SLOT_CFG");
         return e ? std::atoi(e) : 0;
     }();
-    if (cfg && launch_slot_cfg(a, B, cfg, st)) return;
+    if (cfg)
+        if (const int g = launch_slot_cfg(a, B, cfg, st)) return g;
     switch (B) {
     case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
@@ -1056,6 +1136,7 @@ void launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const Pe
     case 32: cheby_batch_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
+    return grid;
 }
 // Split path: hub pieces through cheby_batch_kernel, then plain rows through
 // cheby_batch_rows_kernel.  Faster on every graph with >= 8M local edges
@@ -1070,13 +1151,15 @@ bool batch_split(uint64_t nnz_loc) {
 // Launch a persistent batched kernel instance with its grid capped at its own
 // occupancy x SMs (callers size `grid` for the default 4 CTAs/SM).
 template <typename Kern>
-void launch_capped(Kern kernel, const BatchArgs& a, int grid, cudaStream_t st) {
+int launch_capped(Kern kernel, const BatchArgs& a, int grid, cudaStream_t st) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int occ = 0;  // per kernel instance; the same on every B200
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBatchThreads, 0);
-    kernel<<<std::max(1, std::min(grid, std::max(1, occ) * sms)), kBatchThreads, 0, st>>>(a, PeerArgs{});
+    const int g = std::max(1, std::min(grid, std::max(1, std::min(occ, kBatchMaxCtasPerSm)) * sms));
+    kernel<<<g, kBatchThreads, 0, st>>>(a, PeerArgs{});
+    return g;
 }
 
 // Geometry of the split kernels (U row gathers in flight per lane, MINB CTAs
@@ -1091,16 +1174,16 @@ int split_cfg(const char* env, int B) {
 
 #define CPG_SPLIT_CFG_SWITCH(KERNEL, B)                                                             \
     switch (cfg) {                                                                                  \
-    case 83: launch_capped(KERNEL<B, 8, 3>, a, grid, st); return;                                   \
-    case 63: launch_capped(KERNEL<B, 6, 3>, a, grid, st); return;                                   \
-    case 162: launch_capped(KERNEL<B, 16, 2>, a, grid, st); return;                                 \
-    default: launch_capped(KERNEL<B, 8, 4>, a, grid, st); return;                                   \
+    case 83: return launch_capped(KERNEL<B, 8, 3>, a, grid, st);                                    \
+    case 63: return launch_capped(KERNEL<B, 6, 3>, a, grid, st);                                    \
+    case 162: return launch_capped(KERNEL<B, 16, 2>, a, grid, st);                                  \
+    default: return launch_capped(KERNEL<B, 8, 4>, a, grid, st);                                    \
     }
 
-void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_pieces_kernel, B, grid, st, a, *pa);
-        return;
+        return grid;
     }
     static const int cfg16 = split_cfg("CPG_PIECES_CFG", 16), cfg64 = split_cfg("CPG_PIECES_CFG", 64);
     if (B == 16) {
@@ -1116,12 +1199,13 @@ void launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, c
     case 8: cheby_batch_pieces_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     default: cheby_batch_pieces_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
+    return grid;
 }
 
-void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_rows_kernel, B, grid, st, a, *pa);
-        return;
+        return grid;
     }
     static const int cfg16 = split_cfg("CPG_ROWS_CFG", 16), cfg64 = split_cfg("CPG_ROWS_CFG", 64);
     if (B == 16) {
@@ -1137,6 +1221,7 @@ void launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, con
     case 8: cheby_batch_rows_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     default: cheby_batch_rows_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
     }
+    return grid;
 }
 
 int batch_occupancy() {
@@ -1176,6 +1261,14 @@ __global__ void zero_f64_kernel(double* p) { *p = 0.0; }
 void launch_zero_f64(double* p, cudaStream_t st) { zero_f64_kernel<<<1, 1, 0, st>>>(p); }
 void launch_mass_err(const double* steps, uint32_t K, double mass0, double* err, cudaStream_t st) {
     mass_err_kernel<<<1, 1, 0, st>>>(steps, K, mass0, err);
+}
+void launch_mass_steps_batch(const double* mp, uint32_t stride, uint32_t used, uint32_t B, uint32_t K,
+                             uint32_t count, double* steps, cudaStream_t st) {
+    mass_steps_batch_kernel<<<dim3(K, count), kStepThreads, 0, st>>>(mp, stride, used, B, K, steps);
+}
+void launch_mass_err_cols(const double* steps, uint32_t K, uint32_t count, const double* mass0, double* err,
+                          cudaStream_t st) {
+    mass_err_cols_kernel<<<1, 1, 0, st>>>(steps, K, count, mass0, err);
 }
 
 } // namespace cpg

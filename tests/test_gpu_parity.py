@@ -556,3 +556,46 @@ def test_single_source_query_groups(cpg, gpu, group, monkeypatch):
         for j, s in enumerate(src):
             want, _, _ = ref.cheby_power(fam, param, int(s), K)
             assert_parity(got[j], want)
+
+
+def test_batched_mass_check(cpg, gpu):
+    """North star item (3) for the batched step: the epilogue's per-column mass
+    sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v) (acceptance.cpp:349-360, C13) is reduced
+    on the device for every column and step, in both batched paths; dense seed
+    columns (general_gp_matrix, a = 0) conserve their own sums; a != 0 has no
+    conserved mass and reports NaN."""
+    import os
+
+    off, nb = cpg.gen_chunglu(20000, 200000, 2.1, 20.0, 3000, seed=12)
+    g = cpg.Graph.from_csr(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    for split in ("0", "1"):
+        os.environ["CPG_BATCH_SPLIT"] = split
+        try:
+            for tile in (4, 16, 64):
+                _, st = cpg.cheby_power_many(g, k, list(range(tile)), 26, batched=True, tile=tile)
+                assert 0.0 <= st.mass_err_max <= 1e-9, (split, tile, st.mass_err_max)
+        finally:
+            del os.environ["CPG_BATCH_SPLIT"]
+    from oracle import Port
+
+    n = g.node_count()
+    X = np.stack([Port.random_vector(n, 3 + j, 0.0, 1.0) for j in range(5)])
+    cols = cpg.general_gp_matrix(g, k, 0.0, X, 26, tile=8)
+    assert len(cols) == 5
+    # stats through the C ABI: conserved mass = column sums
+    import ctypes
+
+    from paper_2412_10789_b200 import _lib
+
+    c = k.cheby_coeffs(26)
+    out = np.empty_like(X)
+    s = _lib.cpg_stats()
+    rc = _lib.lib().cpg_general_gp(g.device(0).handle, c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 26, 0.0,
+                                   X.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 5, 8, out.ctypes.data,
+                                   ctypes.byref(s))
+    assert rc == 0 and s.mass_err_max <= 1e-9 * X.sum(axis=1).max()
+    rc = _lib.lib().cpg_general_gp(g.device(0).handle, c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 26, 0.5,
+                                   X.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 5, 8, out.ctypes.data,
+                                   ctypes.byref(s))
+    assert rc == 0 and np.isnan(s.mass_err_max)
