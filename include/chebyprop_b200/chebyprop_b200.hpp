@@ -78,12 +78,14 @@ namespace cuda {
 template <typename Estimate, typename Graph, typename Kernel, typename ParameterErrorT, typename Observer>
 Estimate cheby_power_t(const Graph& g, const Kernel& kernel, uint32_t source, std::size_t cheby_steps,
                        const Observer& observer, int device = 0) {
-    const auto start = std::chrono::steady_clock::now();
     if (cheby_steps < 1) throw ParameterErrorT("cheby_power: cheby_steps must be >= 1");
     if (source >= g.node_count())
         throw ParameterErrorT("source node " + std::to_string(source) + " out of range");
-    const std::vector<double> c = kernel.cheby_coeffs(cheby_steps);
+    // the first call's upload is graph loading, which the reference's wall_seconds
+    // excludes (README.md:93-95): the clock starts once the device graph exists
     cpg_graph* dg = chebyprop_b200::device_graph<Graph, ParameterErrorT>(g, device);
+    const auto start = std::chrono::steady_clock::now();
+    const std::vector<double> c = kernel.cheby_coeffs(cheby_steps);
     const std::size_t n = g.node_count();
     Estimate est;
     est.values.assign(n, 0.0);
@@ -110,20 +112,35 @@ Estimate cheby_power_t(const Graph& g, const Kernel& kernel, uint32_t source, st
     return est;
 }
 
-// cheby_power_vec (solvers.cpp:197-234) on the GPU.
-template <typename Estimate, typename Graph, typename Kernel, typename ParameterErrorT>
+// cheby_power_vec (solvers.cpp:197-234) on the GPU.  A non-empty observer takes
+// the trace slow path (solvers.cpp:215, 219, 226), as cheby_power_t does.
+template <typename Estimate, typename Graph, typename Kernel, typename ParameterErrorT, typename Observer>
 Estimate cheby_power_vec_t(const Graph& g, const Kernel& kernel, const std::vector<double>& seed,
-                           std::size_t cheby_steps, int device = 0) {
-    const auto start = std::chrono::steady_clock::now();
+                           std::size_t cheby_steps, const Observer& observer, int device = 0) {
     if (seed.size() != g.node_count()) throw ParameterErrorT("seed vector length mismatch");
     if (cheby_steps < 1) throw ParameterErrorT("cheby_power: cheby_steps must be >= 1");
-    const std::vector<double> c = kernel.cheby_coeffs(cheby_steps);
     cpg_graph* dg = chebyprop_b200::device_graph<Graph, ParameterErrorT>(g, device);
+    const auto start = std::chrono::steady_clock::now();
+    const std::vector<double> c = kernel.cheby_coeffs(cheby_steps);
+    const std::size_t n = g.node_count();
     Estimate est;
-    est.values.assign(g.node_count(), 0.0);
+    est.values.assign(n, 0.0);
     const uint32_t K = static_cast<uint32_t>(cheby_steps);
-    cpg_stats st{};
-    chebyprop_b200::check<ParameterErrorT>(cpg_chebypower_vec(dg, c.data(), K, seed.data(), 1, est.values.data(), &st));
+    if (observer) {
+        std::vector<double> rt((K + 1) * n), et((K + 1) * n);
+        chebyprop_b200::check<ParameterErrorT>(
+            cpg_chebypower_vec_trace(dg, c.data(), K, seed.data(), est.values.data(), rt.data(), et.data()));
+        std::vector<double> r(n), e(n);
+        for (uint32_t k = 0; k <= K; ++k) {
+            r.assign(rt.begin() + k * n, rt.begin() + (k + 1) * n);
+            e.assign(et.begin() + k * n, et.begin() + (k + 1) * n);
+            observer(k, r, e);
+        }
+    } else {
+        cpg_stats st{};
+        chebyprop_b200::check<ParameterErrorT>(
+            cpg_chebypower_vec(dg, c.data(), K, seed.data(), 1, est.values.data(), &st));
+    }
     est.stats.iterations = K;
     est.stats.push_work = static_cast<std::uint64_t>(K) * g.volume();
     est.stats.algorithm = "chebypower";
@@ -139,6 +156,8 @@ Estimate cheby_power_vec_t(const Graph& g, const Kernel& kernel, const std::vect
 // before including this file to get the exact reference signatures:
 //   chebyprop::cuda::cheby_power(const Graph&, const Kernel&, NodeId, std::size_t,
 //                                const StepObserver& = {})
+//   chebyprop::cuda::cheby_power_vec(const Graph&, const Kernel&, const NodeVector&,
+//                                    std::size_t, const StepObserver& = {})
 #ifdef CHEBYPROP_B200_REFERENCE_TYPES
 #include "chebyprop/error.hpp"
 #include "chebyprop/solvers.hpp"
@@ -149,8 +168,8 @@ inline Estimate cheby_power(const Graph& g, const Kernel& kernel, NodeId source,
     return cheby_power_t<Estimate, Graph, Kernel, ParameterError>(g, kernel, source, cheby_steps, observer);
 }
 inline Estimate cheby_power_vec(const Graph& g, const Kernel& kernel, const NodeVector& seed,
-                                std::size_t cheby_steps) {
-    return cheby_power_vec_t<Estimate, Graph, Kernel, ParameterError>(g, kernel, seed, cheby_steps);
+                                std::size_t cheby_steps, const StepObserver& observer = {}) {
+    return cheby_power_vec_t<Estimate, Graph, Kernel, ParameterError>(g, kernel, seed, cheby_steps, observer);
 }
 } // namespace cuda
 } // namespace chebyprop

@@ -18,7 +18,9 @@
  * a status code; cpg_last_error() gives the calling thread's message for the
  * last failure.  Status mapping to the reference's exceptions (error.hpp):
  *   CPG_EINVAL  -> ParameterError   (bad source, K < 1, bad alpha/t/eps, length)
- *   CPG_ESTRUCT -> StructuralError  (invalid CSR)
+ *   CPG_ESTRUCT -> StructuralError  (invalid CSR, empty graph after cleaning)
+ *   CPG_EPARSE  -> ParseError       (edge-list text, CPGR / CPGT headers)
+ *   CPG_EIO     -> IoError          (cannot open / write a file)
  *   CPG_ECUDA / CPG_ENOMEM / CPG_ENCCL -> runtime failures (no CPU fallback).
  *
  * Node ids, offsets and the CSR layout are the reference's own
@@ -41,7 +43,9 @@ enum {
     CPG_ECUDA = 2,
     CPG_ENCCL = 3,
     CPG_ENOMEM = 4,
-    CPG_ESTRUCT = 5
+    CPG_ESTRUCT = 5,
+    CPG_EPARSE = 6,   /* ParseError: malformed text / binary cache (error.hpp:8-10) */
+    CPG_EIO = 7       /* IoError: cannot open / read / write (error.hpp:28-30)      */
 };
 
 enum { CPG_PPR = 0, CPG_HKPR = 1 };
@@ -221,6 +225,12 @@ int cpg_general_gp(cpg_graph* g, const double* coeffs, uint32_t K, double a, con
  * solvers.cpp:215,219,226.  Either trace pointer may be NULL. */
 int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source,
                          double* out, double* r_trace, double* est_trace);
+/* The same observer slow path for a dense seed vector x (length n, caller ids):
+ * cheby_power_vec with a non-empty StepObserver (solvers.hpp:62-64,
+ * solvers.cpp:197-234).  r_trace[k*n..] = T_k(P) x, est_trace[k*n..] = the
+ * partial estimate after step k (est_0 = c_0 x, solvers.cpp:209). */
+int cpg_chebypower_vec_trace(cpg_graph* g, const double* coeffs, uint32_t K, const double* seed,
+                             double* out, double* r_trace, double* est_trace);
 
 /* PwMethod (solvers.cpp:87-121), the reference's ground-truth engine
  * (eval.cpp:52-59): out = sum_{k<n_steps} zeta_k P^k e_s, n_steps - 1 fused
@@ -257,6 +267,60 @@ int cpg_ingest_edges(const int64_t* pairs, uint64_t m, int device, uint64_t** of
 /* Copy a device-resident CSR (e.g. from the generator) into caller host arrays. */
 int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint32_t n, uint64_t nnz,
                     int device, uint64_t* offsets, uint32_t* neighbors);
+
+/* ---- the formats and metrics either side of the path ---- */
+
+/* ErrorReport (eval.hpp:15-20). */
+typedef struct {
+    double l1;
+    double l2;
+    double deg_norm_inf;
+    uint32_t argmax_node;
+} cpg_error_report;
+
+/* measure(truth, estimate, g) (eval.cpp:18-37) for n_cols column pairs
+ * ([n_cols][n] each, caller ids) on the graph's device.  on_device != 0: both
+ * pointers are device memory; else host memory (uploaded).  l1/l2 are
+ * compensated sums (within the reference's own rounding of its sequential
+ * sum), deg_norm_inf and argmax_node are exact (ties keep the smaller id). */
+int cpg_measure(cpg_graph* g, const double* truth, const double* estimate, uint32_t n_cols, int on_device,
+                cpg_error_report* reports);
+/* n_sources ChebyPower queries measured against truths[n_sources][n] on the
+ * device (the eval harness's run_query: estimate + measure, eval.cpp:18-37,
+ * tools/chebyprop.cpp:140-160) -- no n-vector crosses PCIe.  truths_on_device
+ * != 0: truths is device memory (e.g. from cpg_power_method's device output). */
+int cpg_chebypower_measure(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                           uint32_t n_sources, const double* truths, int truths_on_device,
+                           cpg_error_report* reports, cpg_stats* stats);
+
+/* Edge-list text with the reference loader's line rules (graph.cpp:126-151):
+ * blank lines and lines whose first non-blank char is `comment` are skipped;
+ * every other line must start with two integers (istream >> int64 rules),
+ * optionally followed by ONE token that parses fully as a number (a weight).
+ * Errors: CPG_EPARSE with the reference's message ("line N: expected two
+ * integers, got \"...\"" / "line N: trailing garbage \"...\"") for the
+ * first bad line.  pairs == NULL counts only; else cap_pairs >= the count.
+ * Self-loops are kept here (cpg_ingest_edges drops them, graph.cpp:149). */
+int cpg_parse_edge_text(const char* text, uint64_t len, char comment, int64_t* pairs, uint64_t cap_pairs,
+                        uint64_t* n_pairs, int n_threads);
+/* CPGR binary CSR cache (graph.hpp:87-90, graph.cpp:217-255): "CPGR", u32 1,
+ * u64 n, u64 m, u64 offsets[n+1], u32 neighbors[2m].  info reads the header
+ * (CPG_EPARSE bad magic / version / short header, CPG_ESTRUCT n out of
+ * range); read fills caller arrays (CPG_EPARSE "truncated CSR cache").
+ * Validation is Graph::from_csr's (cpg_validate_csr). */
+int cpg_csr_cache_write(const char* path, const uint64_t* offsets, const uint32_t* neighbors, uint64_t n,
+                        uint64_t nnz);
+int cpg_csr_cache_info(const char* path, uint64_t* n, uint64_t* m);
+int cpg_csr_cache_read(const char* path, uint64_t* offsets, uint32_t* neighbors, uint64_t n, uint64_t m);
+/* CPGT ground-truth cache (eval.cpp:92-145): "CPGT", u32 1, u32 len,
+ * descriptor, u64 source, u64 n, f64 values[n]; and truth_cache_filename
+ * (eval.cpp:147-156). */
+int cpg_truth_cache_write(const char* path, const char* kernel_descriptor, uint64_t source, const double* values,
+                          uint64_t n);
+int cpg_truth_cache_info(const char* path, char* desc, uint64_t desc_cap, uint64_t* source, uint64_t* n);
+int cpg_truth_cache_read(const char* path, double* values, uint64_t n);
+int cpg_truth_cache_filename(uint64_t structure_hash, const char* kernel_descriptor, uint64_t source, char* out,
+                             uint64_t cap);
 
 #ifdef __cplusplus
 }

@@ -55,7 +55,10 @@ def _csr(offsets, nbrs):
 
 
 class OracleError(RuntimeError):
-    pass
+    def __init__(self, msg, status=0, detail=""):
+        super().__init__(msg)
+        self.status = status  # Ref: the reference exception's code (Ref.PARSE, ...)
+        self.detail = detail  # Ref: the reference exception's what()
 
 
 class _Plan:
@@ -360,13 +363,47 @@ class Ref:
             L.ref_select_sources_uniform.argtypes = [c_void_p, c_uint64, c_uint64, _u32p]
             L.ref_cheby_power_pool.argtypes = [c_void_p, c_int, c_double, _u32p, c_uint64,
                                                c_uint64, c_int, _f64p, _f64p]
+            L.ref_measure.argtypes = [c_void_p, _f64p, _f64p, _f64p, _u32p]
+            L.ref_write_csr_cache.argtypes = [c_void_p, c_void_p, c_uint64, _u64p]
+            L.ref_read_csr_cache.argtypes = [c_void_p, c_uint64, POINTER(c_void_p)]
+            L.ref_write_truth_cache.argtypes = [c_char_p, c_uint64, _f64p, c_uint64, c_void_p, c_uint64, _u64p]
+            L.ref_read_truth_cache.argtypes = [c_void_p, c_uint64, c_char_p, c_uint64, _u64p, _f64p, c_uint64,
+                                               _u64p]
+            L.ref_truth_cache_filename.argtypes = [c_void_p, c_int, c_double, c_uint32, c_char_p, c_uint64]
             cls._lib = L
         return cls._lib
 
     @classmethod
     def _check(cls, rc, what):
         if rc != 0:
-            raise OracleError(f"{what}: status {rc}: {cls.lib().ref_last_error().decode()}")
+            raise OracleError(f"{what}: status {rc}: {cls.lib().ref_last_error().decode()}", rc,
+                              cls.lib().ref_last_error().decode())
+
+    # status codes of ref_shim.cpp's guarded(): the reference's exception types
+    PARAMETER, STRUCTURAL, OTHER, PARSE, IO = 1, 5, 6, 7, 8
+
+    @classmethod
+    def write_truth_cache(cls, desc, source, values):
+        """write_truth_cache (eval.cpp:113-124) -> bytes."""
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        n = np.zeros(1, dtype=np.uint64)
+        cls._check(cls.lib().ref_write_truth_cache(desc.encode(), source, _p(values, _f64p), len(values), None, 0,
+                                                   _p(n, _u64p)), "write_truth_cache")
+        buf = ctypes.create_string_buffer(int(n[0]))
+        cls._check(cls.lib().ref_write_truth_cache(desc.encode(), source, _p(values, _f64p), len(values), buf,
+                                                   int(n[0]), _p(n, _u64p)), "write_truth_cache")
+        return buf.raw
+
+    @classmethod
+    def read_truth_cache(cls, data):
+        """read_truth_cache (eval.cpp:126-145) of bytes -> (descriptor, source, values)."""
+        desc = ctypes.create_string_buffer(4096)
+        src = np.zeros(1, dtype=np.uint64)
+        n = np.zeros(1, dtype=np.uint64)
+        vals = np.empty(max(1, len(data) // 8))
+        cls._check(cls.lib().ref_read_truth_cache(data, len(data), desc, len(desc), _p(src, _u64p), _p(vals, _f64p),
+                                                  len(vals), _p(n, _u64p)), "read_truth_cache")
+        return desc.value.decode(), int(src[0]), vals[: int(n[0])].copy()
 
     @classmethod
     def ppr_cheby_coeffs(cls, alpha, max_index):
@@ -460,6 +497,37 @@ class RefGraph:
         nb = np.empty(self.nnz, dtype=np.uint32)
         Ref.lib().ref_graph_csr(self.h, _p(off, _u64p), _p(nb, _u32p))
         return off, nb
+
+    def measure(self, truth, est):
+        """measure (eval.cpp:18-37) -> (l1, l2, deg_norm_inf, argmax_node)."""
+        truth = np.ascontiguousarray(truth, dtype=np.float64)
+        est = np.ascontiguousarray(est, dtype=np.float64)
+        out = np.empty(3)
+        arg = np.zeros(1, dtype=np.uint32)
+        Ref._check(Ref.lib().ref_measure(self.h, _p(truth, _f64p), _p(est, _f64p), _p(out, _f64p), _p(arg, _u32p)),
+                   "measure")
+        return float(out[0]), float(out[1]), float(out[2]), int(arg[0])
+
+    def csr_cache_bytes(self):
+        """write_csr_cache (graph.cpp:217-232) -> bytes."""
+        n = np.zeros(1, dtype=np.uint64)
+        Ref._check(Ref.lib().ref_write_csr_cache(self.h, None, 0, _p(n, _u64p)), "write_csr_cache")
+        buf = ctypes.create_string_buffer(int(n[0]))
+        Ref._check(Ref.lib().ref_write_csr_cache(self.h, buf, int(n[0]), _p(n, _u64p)), "write_csr_cache")
+        return buf.raw
+
+    @classmethod
+    def from_csr_cache_bytes(cls, data):
+        """read_csr_cache (graph.cpp:234-255) of bytes."""
+        h = c_void_p()
+        Ref._check(Ref.lib().ref_read_csr_cache(data, len(data), ctypes.byref(h)), "read_csr_cache")
+        return cls(h)
+
+    def truth_cache_filename(self, family, param, source):
+        out = ctypes.create_string_buffer(4096)
+        Ref._check(Ref.lib().ref_truth_cache_filename(self.h, family, param, source, out, len(out)),
+                   "truth_cache_filename")
+        return out.value.decode()
 
     def original_ids(self):
         k = int(Ref.lib().ref_graph_original_ids(self.h, None))

@@ -9,7 +9,7 @@
 //
 // Every entry calls the reference's public C++ API (include/chebyprop/*.hpp)
 // and converts its exceptions to status codes:
-//   0 ok, 1 ParameterError, 5 StructuralError/ParseError, 6 other.
+//   0 ok, 1 ParameterError, 5 StructuralError, 7 ParseError, 8 IoError, 6 other.
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -44,7 +44,10 @@ int guarded(F&& f) {
         return 5;
     } catch (const ParseError& e) {
         g_err = e.what();
-        return 5;
+        return 7;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 8;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 6;
@@ -229,6 +232,84 @@ int ref_graph_from_edge_text(const char* text, void** out) {
     return guarded([&] {
         std::istringstream in{std::string(text)};
         *out = new Graph(load_edge_list(in));
+    });
+}
+
+// measure (eval.cpp:18-37): out = {l1, l2, deg_norm_inf}, *argmax = argmax_node.
+int ref_measure(void* gp, const double* truth, const double* est, double* out, uint32_t* argmax) {
+    return guarded([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const NodeVector t(truth, truth + g.node_count()), e(est, est + g.node_count());
+        const ErrorReport r = measure(t, e, g);
+        out[0] = r.l1;
+        out[1] = r.l2;
+        out[2] = r.deg_norm_inf;
+        *argmax = r.argmax_node;
+    });
+}
+
+// write_csr_cache (graph.cpp:217-232) into a caller buffer (buf NULL: size only).
+int ref_write_csr_cache(void* gp, char* buf, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        std::ostringstream out(std::ios::binary);
+        write_csr_cache(*static_cast<Graph*>(gp), out);
+        const std::string b = out.str();
+        *len = b.size();
+        if (buf) {
+            if (cap < b.size()) throw ParameterError("ref_write_csr_cache: buffer too small");
+            std::memcpy(buf, b.data(), b.size());
+        }
+    });
+}
+
+// read_csr_cache (graph.cpp:234-255) from bytes.
+int ref_read_csr_cache(const char* buf, uint64_t len, void** out) {
+    return guarded([&] {
+        std::istringstream in(std::string(buf, len), std::ios::binary);
+        *out = new Graph(read_csr_cache(in));
+    });
+}
+
+// write_truth_cache (eval.cpp:113-124) into a caller buffer (buf NULL: size only).
+int ref_write_truth_cache(const char* desc, uint64_t source, const double* values, uint64_t n, char* buf,
+                          uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        GroundTruth t;
+        t.kernel_descriptor = desc;
+        t.source = static_cast<NodeId>(source);
+        t.values.assign(values, values + n);
+        std::ostringstream out(std::ios::binary);
+        write_truth_cache(t, out);
+        const std::string b = out.str();
+        *len = b.size();
+        if (buf) {
+            if (cap < b.size()) throw ParameterError("ref_write_truth_cache: buffer too small");
+            std::memcpy(buf, b.data(), b.size());
+        }
+    });
+}
+
+// read_truth_cache (eval.cpp:126-145) from bytes: descriptor, source, values (cap n_cap).
+int ref_read_truth_cache(const char* buf, uint64_t len, char* desc, uint64_t desc_cap, uint64_t* source,
+                         double* values, uint64_t n_cap, uint64_t* n) {
+    return guarded([&] {
+        std::istringstream in(std::string(buf, len), std::ios::binary);
+        const GroundTruth t = read_truth_cache(in);
+        if (t.kernel_descriptor.size() >= desc_cap || t.values.size() > n_cap)
+            throw ParameterError("ref_read_truth_cache: buffer too small");
+        std::memcpy(desc, t.kernel_descriptor.c_str(), t.kernel_descriptor.size() + 1);
+        *source = t.source;
+        *n = t.values.size();
+        std::memcpy(values, t.values.data(), t.values.size() * sizeof(double));
+    });
+}
+
+// truth_cache_filename (eval.cpp:147-156).
+int ref_truth_cache_filename(void* gp, int family, double param, uint32_t source, char* out, uint64_t cap) {
+    return guarded([&] {
+        const std::string s = truth_cache_filename(*static_cast<Graph*>(gp), make_kernel(family, param), source);
+        if (s.size() >= cap) throw ParameterError("ref_truth_cache_filename: buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
     });
 }
 

@@ -44,6 +44,9 @@ __all__ = [
     "general_gp_vector", "general_gp_matrix", "gen_rmat", "gen_chunglu", "DeviceCSR", "power_method",
     "ground_truth", "ground_truth_steps", "select_sources_uniform", "shard_plan", "cheby_power_topk",
     "ingest_edges", "load_edge_list_file", "cheby_power_many_pipelined", "sync", "LoopbackGroup",
+    "ParseError", "IoError", "parse_edge_text", "load_edge_list", "write_csr_cache", "read_csr_cache",
+    "ErrorReport", "measure", "cheby_power_measure", "GroundTruth", "write_truth_cache", "read_truth_cache",
+    "truth_cache_filename", "load_or_compute_truth",
 ]
 
 
@@ -60,6 +63,14 @@ class DeviceError(RuntimeError):
     pass
 
 
+class ParseError(RuntimeError):
+    """Malformed edge-list text or binary cache header (error.hpp:8-10)."""
+
+
+class IoError(RuntimeError):
+    """Cannot open / read / write a file (error.hpp:28-30)."""
+
+
 def _check(rc: int, what: str = "") -> None:
     if rc == L.CPG_OK:
         return
@@ -70,6 +81,10 @@ def _check(rc: int, what: str = "") -> None:
         raise ParameterError(msg)
     if rc == L.CPG_ESTRUCT:
         raise StructuralError(msg)
+    if rc == L.CPG_EPARSE:
+        raise ParseError(msg)
+    if rc == L.CPG_EIO:
+        raise IoError(msg)
     raise DeviceError(f"[status {rc}] {msg}")
 
 
@@ -394,11 +409,14 @@ def _steps(cheby_steps) -> int:
 
 def cheby_power(g, kernel: Kernel, source: int, cheby_steps: int, observer: Optional[StepObserver] = None,
                 device: int = 0) -> Estimate:
-    """yhat = sum_{k=0..K} c_k T_k(P) e_source (solvers.cpp:236-239) on the GPU."""
-    t0 = time.perf_counter()
+    """yhat = sum_{k=0..K} c_k T_k(P) e_source (solvers.cpp:236-239) on the GPU.
+
+    wall_seconds covers coefficients + iterations, not the first call's graph
+    upload (the reference times queries on a loaded graph, README.md:93-95)."""
     K = _steps(cheby_steps)
-    c = kernel.cheby_coeffs(K)  # coefficients inside the call, like solvers.cpp:205
     dg = _dev(g, device)
+    t0 = time.perf_counter()
+    c = kernel.cheby_coeffs(K)  # coefficients inside the call, like solvers.cpp:205
     if source < 0 or source >= dg.n:
         raise ParameterError(f"source node {source} out of range")
     n = dg.n
@@ -420,17 +438,35 @@ def cheby_power(g, kernel: Kernel, source: int, cheby_steps: int, observer: Opti
     return Estimate(out, st)
 
 
-def cheby_power_vec(g, kernel: Kernel, seed, cheby_steps: int, device: int = 0) -> Estimate:
-    """cheby_power_vec (solvers.cpp:197-234) for a dense seed vector (or an (s, n) stack)."""
-    t0 = time.perf_counter()
+def cheby_power_vec(g, kernel: Kernel, seed, cheby_steps: int, observer: Optional[StepObserver] = None,
+                    device: int = 0) -> Estimate:
+    """cheby_power_vec (solvers.cpp:197-234) for a dense seed vector (or an (s, n) stack).
+
+    A non-None observer (one seed vector only) takes the trace slow path and is
+    called with (k, T_k(P) x, partial estimate) for k = 0..K (solvers.cpp:215, 219, 226)."""
     K = _steps(cheby_steps)
     dg = _dev(g, device)
+    t0 = time.perf_counter()
     seeds = np.ascontiguousarray(seed, dtype=np.float64)
     single = seeds.ndim == 1
     seeds = seeds.reshape(-1, seeds.shape[-1])
     if seeds.shape[1] != dg.n:
         raise ParameterError("seed vector length mismatch")  # solvers.cpp:36-37
     c = kernel.cheby_coeffs(K)
+    if observer is not None:
+        if not single:
+            raise ParameterError("observer takes one seed vector")
+        n = dg.n
+        out = np.empty(n)
+        rt = np.empty((K + 1, n))
+        et = np.empty((K + 1, n))
+        _check(L.lib().cpg_chebypower_vec_trace(dg.handle, _f64p(c), K, _f64p(seeds), out.ctypes.data,
+                                                rt.ctypes.data, et.ctypes.data))
+        for k in range(K + 1):
+            observer(k, rt[k], et[k])
+        st = SolveStats(iterations=K, push_work=K * int(dg.info.nnz), params=f"K={K}")
+        st.wall_seconds = time.perf_counter() - t0
+        return Estimate(out, st)
     out = np.empty_like(seeds)
     s = cpg_stats()
     _check(L.lib().cpg_chebypower_vec(dg.handle, _f64p(c), K, _f64p(seeds), seeds.shape[0], out.ctypes.data,
@@ -624,22 +660,170 @@ def ingest_edges(pairs, device: int = 0):
     return DeviceCSR(off.value, nbr.value, n.value, nnz.value, device), labels[: n.value].copy()
 
 
-def load_edge_list_file(path: str, device: int = 0, comment: str = "#") -> Graph:
-    """graph.cpp:173-177 + :113-171: parse "u v" lines on the host, build the CSR on the GPU."""
-    import numpy as _np
+def parse_edge_text(text, comment: str = "#", n_threads: int = 0) -> np.ndarray:
+    """Edge-list text -> (m, 2) int64 label pairs with the reference loader's line rules
+    (graph.cpp:126-151): natively parsed, multi-threaded; ParseError names the first bad line."""
+    buf = text.encode() if isinstance(text, str) else bytes(text)
+    cap = buf.count(b"\n") + 1
+    pairs = np.empty((cap, 2), dtype=np.int64)
+    got = ctypes.c_uint64()
+    _check(L.lib().cpg_parse_edge_text(buf, len(buf), comment.encode()[:1] or b"#", pairs.ctypes.data, cap,
+                                       ctypes.byref(got), int(n_threads)))
+    return pairs[: got.value]
 
-    try:
-        data = _np.loadtxt(path, dtype=_np.int64, comments=comment, usecols=(0, 1), ndmin=2)
-    except OSError as e:
-        raise DeviceError(f"cannot open graph file: {path}") from e
-    except ValueError as e:
-        raise ParameterError(f"malformed edge list {path}: {e}") from e
-    csr, labels = ingest_edges(data, device)
+
+def load_edge_list(text, comment: str = "#", device: int = 0) -> Graph:
+    """load_edge_list (graph.cpp:113-171): parse the text natively, intern / symmetrise /
+    dedup on the GPU.  The graph carries ``original_ids`` (graph.hpp:45)."""
+    pairs = parse_edge_text(text, comment)
+    csr, labels = ingest_edges(pairs, device)
     off, nb = csr.to_host()
     csr.close()
     g = Graph(off, nb)
     g.original_ids = labels
     return g
+
+
+def load_edge_list_file(path: str, device: int = 0, comment: str = "#") -> Graph:
+    """load_edge_list_file (graph.cpp:173-177)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError as e:
+        raise IoError(f"cannot open graph file: {path}") from e
+    return load_edge_list(data, comment, device)
+
+
+def write_csr_cache(g: Graph, path: str) -> None:
+    """write_csr_cache (graph.cpp:217-232): "CPGR", u32 1, n, m, offsets, neighbors."""
+    off, nb = g.offsets(), g.neighbor_array()
+    _check(L.lib().cpg_csr_cache_write(str(path).encode(), _u64p(off), _u32p(nb), len(off) - 1, len(nb)))
+
+
+def read_csr_cache(path: str, validate: bool = True) -> Graph:
+    """read_csr_cache (graph.cpp:234-255): header checks, then Graph::from_csr's validation."""
+    p = str(path).encode()
+    n, m = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(L.lib().cpg_csr_cache_info(p, ctypes.byref(n), ctypes.byref(m)))
+    off = np.empty(n.value + 1, dtype=np.uint64)
+    nb = np.empty(2 * m.value, dtype=np.uint32)
+    _check(L.lib().cpg_csr_cache_read(p, _u64p(off), _u32p(nb), n.value, m.value))
+    return Graph.from_csr(off, nb, validate=validate)
+
+
+@dataclass
+class ErrorReport:  # eval.hpp:15-20
+    l1: float = 0.0
+    l2: float = 0.0
+    deg_norm_inf: float = 0.0
+    argmax_node: int = 0
+
+
+def _reports(arr) -> list:
+    return [ErrorReport(r.l1, r.l2, r.deg_norm_inf, int(r.argmax_node)) for r in arr]
+
+
+def measure(truth, estimate, g, device: int = 0) -> ErrorReport:
+    """measure (eval.cpp:18-37) on the GPU; (s, n) stacks give a list of reports."""
+    dg = _dev(g, device)
+    t = np.ascontiguousarray(truth, dtype=np.float64)
+    e = np.ascontiguousarray(estimate, dtype=np.float64)
+    if t.shape != e.shape or t.shape[-1] != dg.n:
+        raise ParameterError("measure: vector length mismatch")  # eval.cpp:21-22
+    cols = 1 if t.ndim == 1 else t.shape[0]
+    reps = (L.cpg_error_report * cols)()
+    _check(L.lib().cpg_measure(dg.handle, t.ctypes.data, e.ctypes.data, cols, 0, reps))
+    out = _reports(reps)
+    return out[0] if t.ndim == 1 else out
+
+
+def cheby_power_measure(g, kernel: Kernel, sources: Sequence[int], cheby_steps: int, truths, device: int = 0):
+    """ChebyPower for every source, measured against truths[i] on the device (the eval
+    harness's estimate + measure, tools/chebyprop.cpp:140-160); only the reports return."""
+    K = _steps(cheby_steps)
+    dg = _dev(g, device)
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    tr = np.ascontiguousarray(truths, dtype=np.float64).reshape(len(src), -1)
+    if tr.shape[1] != dg.n:
+        raise ParameterError("measure: vector length mismatch")
+    c = kernel.cheby_coeffs(K)
+    reps = (L.cpg_error_report * max(1, len(src)))()
+    s = cpg_stats()
+    _check(L.lib().cpg_chebypower_measure(dg.handle, _f64p(c), K, _u32p(src), len(src), tr.ctypes.data, 0, reps,
+                                          ctypes.byref(s)))
+    return _reports(reps)[: len(src)], _to_stats(s, K)
+
+
+@dataclass
+class GroundTruth:  # eval.hpp:25-30
+    values: np.ndarray
+    kernel_descriptor: str = ""
+    source: int = 0
+    truncation: int = 0
+
+
+def write_truth_cache(truth: GroundTruth, path: str) -> None:
+    """write_truth_cache (eval.cpp:113-124)."""
+    v = np.ascontiguousarray(truth.values, dtype=np.float64)
+    _check(L.lib().cpg_truth_cache_write(str(path).encode(), truth.kernel_descriptor.encode(), int(truth.source),
+                                         _f64p(v), len(v)))
+
+
+def read_truth_cache(path: str) -> GroundTruth:
+    """read_truth_cache (eval.cpp:126-145)."""
+    p = str(path).encode()
+    desc = ctypes.create_string_buffer(4096)
+    src, n = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(L.lib().cpg_truth_cache_info(p, desc, len(desc), ctypes.byref(src), ctypes.byref(n)))
+    v = np.empty(n.value)
+    _check(L.lib().cpg_truth_cache_read(p, _f64p(v), n.value))
+    return GroundTruth(v, desc.value.decode(), int(src.value), 0)
+
+
+def _hash_of(g) -> int:
+    if isinstance(g, Graph):
+        if not g.structure_hash():
+            g._hash = Graph.from_csr(g.offsets(), g.neighbor_array()).structure_hash()
+        return g.structure_hash()
+    return int(g.info.structure_hash)
+
+
+def truth_cache_filename(g, kernel: Kernel, source: int) -> str:
+    """truth_cache_filename (eval.cpp:147-156)."""
+    out = ctypes.create_string_buffer(4096)
+    _check(L.lib().cpg_truth_cache_filename(_hash_of(g), kernel.descriptor().encode(), int(source), out, len(out)))
+    return out.value.decode()
+
+
+def load_or_compute_truth(g, kernel: Kernel, source: int, cache_dir: str = "", device: int = 0):
+    """load_or_compute_truth (eval.cpp:158-192): (GroundTruth, was_cached).  A cached file is
+    used when its descriptor, source and length match; corrupt or stale entries (ParseError)
+    are recomputed -- on the GPU (PwMethod, eval.cpp:52-59) -- and rewritten."""
+    import os as _os
+
+    dg = _dev(g, device)
+    if source < 0 or source >= dg.n:
+        raise ParameterError("load_or_compute_truth: source out of range")
+    path = ""
+    if cache_dir:
+        path = _os.path.join(cache_dir, truth_cache_filename(g, kernel, source))
+        if _os.path.exists(path):
+            try:
+                t = read_truth_cache(path)
+                if t.kernel_descriptor == kernel.descriptor() and t.source == source and len(t.values) == dg.n:
+                    t.truncation = ground_truth_steps(kernel)
+                    return t, True
+            except (ParseError, IoError):
+                pass
+    t = GroundTruth(ground_truth(g, kernel, source, device), kernel.descriptor(), int(source),
+                    ground_truth_steps(kernel))
+    if cache_dir:
+        _os.makedirs(cache_dir, exist_ok=True)
+        try:
+            write_truth_cache(t, path)
+        except IoError:
+            pass  # eval.cpp:186-189: a cache that cannot be written is skipped
+    return t, False
 
 
 def gen_rmat(scale: int, n_samples: int, a=0.57, b=0.19, c=0.19, seed: int = 1, device: int = -1):

@@ -12,7 +12,7 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_uint32, c_uint64, c_voi
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CPG_LIB_PATH") or os.path.join(PKG, "libcpg.so")  # override: A/B builds
 
-CPG_OK, CPG_EINVAL, CPG_ECUDA, CPG_ENCCL, CPG_ENOMEM, CPG_ESTRUCT = 0, 1, 2, 3, 4, 5
+CPG_OK, CPG_EINVAL, CPG_ECUDA, CPG_ENCCL, CPG_ENOMEM, CPG_ESTRUCT, CPG_EPARSE, CPG_EIO = 0, 1, 2, 3, 4, 5, 6, 7
 
 
 class cpg_stats(ctypes.Structure):
@@ -31,6 +31,10 @@ class cpg_graph_info(ctypes.Structure):
                 ("row_begin", c_uint32), ("n_padded", c_uint32), ("n_hubs", c_uint32),
                 ("n_items", c_uint32), ("max_degree", c_uint32), ("rank", c_int), ("nranks", c_int),
                 ("device", c_int), ("structure_hash", c_uint64), ("chunks", c_int), ("fused_allgather", c_int)]
+
+
+class cpg_error_report(ctypes.Structure):  # ErrorReport, eval.hpp:15-20
+    _fields_ = [("l1", c_double), ("l2", c_double), ("deg_norm_inf", c_double), ("argmax_node", c_uint32)]
 
 
 _u64p = POINTER(c_uint64)
@@ -76,6 +80,7 @@ SIGNATURES = {
                                              POINTER(cpg_stats)]),
     "cpg_graph_sync": (c_int, [_G]),
     "cpg_chebypower_trace": (c_int, [_G, _f64p, c_uint32, c_uint32, c_void_p, c_void_p, c_void_p]),
+    "cpg_chebypower_vec_trace": (c_int, [_G, _f64p, c_uint32, _f64p, c_void_p, c_void_p, c_void_p]),
     "cpg_apply_walk": (c_int, [_G, _f64p, _f64p]),
     "cpg_chebypower_topk": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_uint32, _u32p, _f64p,
                                     POINTER(cpg_stats)]),
@@ -90,6 +95,17 @@ SIGNATURES = {
     "cpg_ingest_edges": (c_int, [POINTER(ctypes.c_int64), c_uint64, c_int, POINTER(c_void_p), POINTER(c_void_p),
                                  _u32p, _u64p, POINTER(ctypes.c_int64), c_uint64]),
     "cpg_csr_to_host": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, _u64p, _u32p]),
+    "cpg_measure": (c_int, [_G, c_void_p, c_void_p, c_uint32, c_int, POINTER(cpg_error_report)]),
+    "cpg_chebypower_measure": (c_int, [_G, _f64p, c_uint32, _u32p, c_uint32, c_void_p, c_int,
+                                       POINTER(cpg_error_report), POINTER(cpg_stats)]),
+    "cpg_parse_edge_text": (c_int, [c_void_p, c_uint64, ctypes.c_char, c_void_p, c_uint64, _u64p, c_int]),
+    "cpg_csr_cache_write": (c_int, [c_char_p, _u64p, _u32p, c_uint64, c_uint64]),
+    "cpg_csr_cache_info": (c_int, [c_char_p, _u64p, _u64p]),
+    "cpg_csr_cache_read": (c_int, [c_char_p, _u64p, _u32p, c_uint64, c_uint64]),
+    "cpg_truth_cache_write": (c_int, [c_char_p, c_char_p, c_uint64, _f64p, c_uint64]),
+    "cpg_truth_cache_info": (c_int, [c_char_p, c_char_p, c_uint64, _u64p, _u64p]),
+    "cpg_truth_cache_read": (c_int, [c_char_p, _f64p, c_uint64]),
+    "cpg_truth_cache_filename": (c_int, [c_uint64, c_char_p, c_uint64, c_char_p, c_uint64]),
 }
 
 _lib = None

@@ -1125,6 +1125,98 @@ int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const ui
     });
 }
 
+// measure (eval.cpp:18-37) on the device: n_cols (truth, estimate) column pairs.
+int cpg_measure(cpg_graph* g, const double* truth, const double* estimate, uint32_t n_cols, int on_device,
+                cpg_error_report* reports) {
+    return guarded([&] {
+        require(g && truth && estimate && (reports || n_cols == 0), "null argument");
+        if (!n_cols) return;
+        DeviceGuard dg(g->device);
+        WsLease lease(g);
+        Workspace* w = lease.w;
+        cudaStream_t st = w->stream;
+        const size_t n = g->n, cols = n_cols;
+        const double* dt = truth;
+        const double* de = estimate;
+        double* tmp = nullptr;
+        if (!on_device) {
+            tmp = dalloc<double>(2 * n * cols);
+            CPG_CUDA(cudaMemcpyAsync(tmp, truth, sizeof(double) * n * cols, cudaMemcpyHostToDevice, st));
+            CPG_CUDA(cudaMemcpyAsync(tmp + n * cols, estimate, sizeof(double) * n * cols, cudaMemcpyHostToDevice, st));
+            dt = tmp;
+            de = tmp + n * cols;
+        }
+        char* scratch = dalloc<char>(measure_scratch_bytes(g, n_cols) + sizeof(cpg_error_report) * cols);
+        cpg_error_report* d_rep =
+            reinterpret_cast<cpg_error_report*>(scratch + measure_scratch_bytes(g, n_cols));
+        launch_measure(g, dt, de, n_cols, scratch, d_rep, st);
+        CPG_CUDA(cudaMemcpyAsync(reports, d_rep, sizeof(cpg_error_report) * cols, cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaStreamSynchronize(st));
+        dfree(scratch);
+        if (tmp) dfree(tmp);
+    });
+}
+
+// The eval harness's query (tools/chebyprop.cpp:140-160: estimate, then
+// measure against the truth) with both steps on the device: per group of
+// queries the estimates stay in a device [Q][n] buffer and only the reports
+// come back.
+int cpg_chebypower_measure(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources,
+                           uint32_t n_sources, const double* truths, int truths_on_device,
+                           cpg_error_report* reports, cpg_stats* stats) {
+    return guarded([&] {
+        check_query(g, coeffs, K, sources, n_sources);
+        require(truths && reports, "null argument");
+        DeviceGuard dg(g->device);
+        const size_t n = g->n;
+        const uint32_t Q = std::max<uint32_t>(
+            1, std::min<uint32_t>(single_group(g, n_sources),
+                                  static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << 30) / (8ull * n)))));
+        double* d_res = dalloc<double>(n * Q);
+        double* d_truth = truths_on_device ? nullptr : dalloc<double>(n * Q);
+        char* scratch = dalloc<char>(measure_scratch_bytes(g, Q) + sizeof(cpg_error_report) * n_sources);
+        cpg_error_report* d_rep = reinterpret_cast<cpg_error_report*>(scratch + measure_scratch_bytes(g, Q));
+        cudaStream_t st = nullptr;
+        cpg_stats acc{};
+        auto cleanup = [&] {
+            if (st) cudaStreamDestroy(st);
+            cudaFree(d_res);
+            if (d_truth) cudaFree(d_truth);
+            cudaFree(scratch);
+        };
+        try {
+            CPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            for (uint32_t q0 = 0; q0 < n_sources; q0 += Q) {
+                const uint32_t cnt = std::min(Q, n_sources - q0);
+                const double* t = truths + static_cast<size_t>(q0) * n;
+                if (!truths_on_device) {
+                    CPG_CUDA(cudaMemcpyAsync(d_truth, t, sizeof(double) * n * cnt, cudaMemcpyHostToDevice, st));
+                    t = d_truth;
+                }
+                cpg_stats s{};
+                const int rc = drive(g, coeffs, K, sources + q0, nullptr, cnt, 1, 0, d_res, true, st, &s);
+                if (rc != CPG_OK) fail(rc, cpg_last_error());
+                launch_measure(g, t, d_res, cnt, scratch, d_rep + q0, st);
+                acc.iterations = s.iterations;
+                acc.push_work += s.push_work;
+                acc.wall_seconds += s.wall_seconds;
+                acc.device_ms += s.device_ms;
+                acc.mass_err_max = std::max(acc.mass_err_max, s.mass_err_max);
+                acc.bytes_model += s.bytes_model;
+                acc.launches += s.launches + 2;
+            }
+            CPG_CUDA(cudaMemcpyAsync(reports, d_rep, sizeof(cpg_error_report) * n_sources, cudaMemcpyDeviceToHost,
+                                     st));
+            CPG_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+        if (stats) *stats = acc;
+    });
+}
+
 // general_gp_vector / general_gp_matrix with ChebyPower (solvers.cpp:390-414):
 // z_j = D^-a f(P) D^a x_j for n_cols dense columns, in tiles of `tile` columns
 // through the batched step (tile 1: single-column path).
@@ -1139,10 +1231,22 @@ int cpg_apply_walk(cpg_graph* g, const double* x, double* y) {
     return cpg_chebypower_vec(g, c, 1, x, 1, y, nullptr);
 }
 
-int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source, double* out,
-                         double* r_trace, double* est_trace) {
+}  // extern "C"
+
+namespace {
+// Observer slow path for one source (seed == null) or one dense seed vector
+// (cheby_power_vec, solvers.cpp:197-234): T_k(P)x and the partial estimate
+// after every step come back to the host (solvers.cpp:215, 219, 226).
+int trace_impl(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source, const double* seed, double* out,
+               double* r_trace, double* est_trace) {
     return guarded([&] {
-        check_query(g, coeffs, K, &source, 1);
+        if (seed) {
+            require(g != nullptr, "null graph handle");
+            require(K >= 1, "cheby_power: cheby_steps must be >= 1");  // solvers.cpp:201
+            require(coeffs != nullptr, "null argument");
+        } else {
+            check_query(g, coeffs, K, &source, 1);
+        }
         require(g->nranks == 1, "trace is single-GPU only");
         DeviceGuard dg(g->device);
         WsLease lease(g);
@@ -1164,13 +1268,20 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
                 if (est_trace) est_trace[k * n + v] = a_scale * d * av[gv];
             }
         };
-        // k = 0: T_0 = e_s, est = c0 e_s (solvers.cpp:209, 215)
+        // k = 0: T_0 = x, est = c0 x (solvers.cpp:209, 215); x = e_s or the seed
         for (size_t v = 0; v < n; ++v) {
-            if (r_trace) r_trace[v] = v == source ? 1.0 : 0.0;
-            if (est_trace) est_trace[v] = v == source ? coeffs[0] : 0.0;
+            const double x = seed ? seed[v] : (v == source ? 1.0 : 0.0);
+            if (r_trace) r_trace[v] = x;
+            if (est_trace) est_trace[v] = coeffs[0] * x;
         }
         CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * np, st));
-        launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, 0, 1, st);
+        if (seed) {
+            ensure_buf(w->d_seeds, w->seeds_cap, n);
+            CPG_CUDA(cudaMemcpyAsync(w->d_seeds, seed, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+            launch_init_dense(w->w_a, g->gdeg, g->new_of_old, w->d_seeds, g->n, 0.0, st);
+        } else {
+            launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, 0, 1, st);
+        }
         CPG_CUDA(cudaMemsetAsync(w->d_mass_partial, 0, sizeof(double) * K * g->chunks * g->step_grid, st));
         for (uint32_t k = 1; k <= K; ++k) {
             run_steps(g, w, k, k, K, false, st, nullptr);
@@ -1184,6 +1295,20 @@ int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_
                 for (size_t v = 0; v < n; ++v) out[v] = static_cast<double>(gdeg[no[v]]) * acc[no[v]];
         }
     });
+}
+}  // namespace
+
+extern "C" {
+
+int cpg_chebypower_trace(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source, double* out,
+                         double* r_trace, double* est_trace) {
+    return trace_impl(g, coeffs, K, source, nullptr, out, r_trace, est_trace);
+}
+
+int cpg_chebypower_vec_trace(cpg_graph* g, const double* coeffs, uint32_t K, const double* seed, double* out,
+                             double* r_trace, double* est_trace) {
+    if (!seed) return guarded([] { require(false, "null argument"); });
+    return trace_impl(g, coeffs, K, 0, seed, out, r_trace, est_trace);
 }
 
 double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile) {

@@ -196,6 +196,10 @@ void launch_mass_err_cols(const double* steps, uint32_t K, uint32_t count, const
 
 // topk.cu
 void device_topk(const double* d_vals, uint32_t n, uint32_t k, uint32_t* ids, double* vals, cudaStream_t st);
+// measure (eval.cpp:18-37) of [cols][n] device column pairs into d_reports[cols] (measure.cu)
+size_t measure_scratch_bytes(const cpg_graph* g, uint32_t cols);
+void launch_measure(const cpg_graph* g, const double* d_truth, const double* d_est, uint32_t cols, void* scratch,
+                    cpg_error_report* d_reports, cudaStream_t st);
 
 // nccl_dl.cpp
 void nccl_get_unique_id(void* out128);

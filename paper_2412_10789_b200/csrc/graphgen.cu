@@ -328,7 +328,7 @@ void ingest_device(const int64_t* d_pairs, uint64_t m, uint64_t** off_out, uint3
     uint64_t mk = 0;
     CPG_CUDA(cudaMemcpy(&mk, d_cnt, sizeof(mk), cudaMemcpyDeviceToHost));
     cudaFree(keep);
-    require(mk > 0, "empty graph after cleaning");  // graph.cpp:156
+    if (mk == 0) fail(CPG_ESTRUCT, "empty graph after cleaning");  // graph.cpp:156 (StructuralError)
     const uint64_t cnt = 2 * mk;
     uint64_t *key = dm<uint64_t>(cnt), *pos = dm<uint64_t>(cnt), *key_s = dm<uint64_t>(cnt), *pos_s = dm<uint64_t>(cnt);
     k_endpoints<<<grid_for(mk), 256, 0, st>>>(d_pairs, kept, mk, key, pos);
@@ -461,7 +461,7 @@ int cpg_csr_to_host(const uint64_t* d_offsets, const uint32_t* d_neighbors, uint
 int cpg_ingest_edges(const int64_t* pairs, uint64_t m, int device, uint64_t** offsets, uint32_t** neighbors,
                      uint32_t* n, uint64_t* nnz, int64_t* original_ids_host, uint64_t original_ids_cap) {
     return guarded([&] {
-        require(pairs && offsets && neighbors && n && nnz, "null argument");
+        require((pairs || m == 0) && offsets && neighbors && n && nnz, "null argument");
         require(device >= 0, "ingest runs on a device");
         CPG_CUDA(cudaSetDevice(device));
         int64_t* d_pairs = nullptr;
@@ -469,7 +469,7 @@ int cpg_ingest_edges(const int64_t* pairs, uint64_t m, int device, uint64_t** of
         CPG_CUDA(cudaMemcpy(d_pairs, pairs, 2 * m * sizeof(int64_t), cudaMemcpyHostToDevice));
         int64_t* labels = nullptr;
         try {
-            require(m > 0, "empty graph after cleaning");
+            if (m == 0) fail(CPG_ESTRUCT, "empty graph after cleaning");  // graph.cpp:156
             ingest_device(d_pairs, m, offsets, neighbors, n, nnz, &labels);
         } catch (...) {
             cudaFree(d_pairs);

@@ -121,6 +121,24 @@ int main() {
         const auto gpu = cuda::cheby_power_vec(g, Kernel::hkpr(5.0), x, 25);
         const auto cpu = chebyprop::cheby_power_vec(g, Kernel::hkpr(5.0), x, 25);
         CHECK(linf(gpu.values, cpu.values) <= 1e-12);
+        // observer on cheby_power_vec (solvers.hpp:62-64): the same (k, r_k, yhat_k) sequence
+        std::vector<NodeVector> gr, ge, cr, ce;
+        const auto gpu_o = cuda::cheby_power_vec(g, Kernel::hkpr(5.0), x, 25,
+                                                 [&](std::size_t, const NodeVector& r, const NodeVector& e) {
+                                                     gr.push_back(r);
+                                                     ge.push_back(e);
+                                                 });
+        chebyprop::cheby_power_vec(g, Kernel::hkpr(5.0), x, 25,
+                                   [&](std::size_t, const NodeVector& r, const NodeVector& e) {
+                                       cr.push_back(r);
+                                       ce.push_back(e);
+                                   });
+        CHECK(gr.size() == cr.size() && gr.size() == 26);
+        double worst = 0;
+        for (std::size_t k = 0; k < std::min(gr.size(), cr.size()); ++k)
+            worst = std::max({worst, linf(gr[k], cr[k]), linf(ge[k], ce[k])});
+        CHECK(worst <= 1e-12);
+        CHECK(linf(gpu_o.values, cpu.values) <= 1e-12);
     }
     {  // error behaviour (solvers.cpp:28-29, :201)
         bool threw = false;

@@ -104,6 +104,28 @@ def test_observer_trace_matches_reference(graphs, cpg):
     assert_parity(est.values, want)
 
 
+def test_vec_observer_trace_matches_oracle(graphs, cpg):
+    """cheby_power_vec with an observer (solvers.hpp:62-64): the per-step T_k x and
+    partial estimates equal the pinned C restatement's trace."""
+    from oracle import Port
+
+    off, nb = graphs["ring_chord_200"]
+    g = cpg.Graph.from_csr(off, nb)
+    x = Port.random_vector(g.node_count(), 5, -1.0, 1.0)
+    K = 11
+    k5 = cpg.Kernel.hkpr(5.0)
+    rs, es = [], []
+    est = cpg.cheby_power_vec(g, k5, x, K, observer=lambda k, r, e: (rs.append(r.copy()), es.append(e.copy())))
+    want, _, rt, et = Port.cheby_power_vec(off, nb, k5.cheby_coeffs(K), K, x, trace=True)
+    assert len(rs) == K + 1
+    for k in range(K + 1):
+        assert np.abs(rs[k] - rt[k]).max() <= 1e-12
+        assert np.abs(es[k] - et[k]).max() <= 1e-12
+    assert np.abs(est.values - want).max() <= 1e-12
+    with pytest.raises(cpg.ParameterError):
+        cpg.cheby_power_vec(g, k5, np.stack([x, x]), K, observer=lambda *a: None)
+
+
 def test_mass_conservation_every_step(graphs, cpg):
     """test_solvers.cpp:122-128 / acceptance C13: |sum r_k - 1| <= 1e-9."""
     from oracle import Port
