@@ -121,6 +121,8 @@ def lib():
                 "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("CPG_LIB_PATH") and not hasattr(L, name):
+                continue  # A/B against an older build: its missing entries stay unbound
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -402,6 +402,10 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
     const int occ = std::max(1, step_occupancy(g->tile));
     const uint32_t C = static_cast<uint32_t>(g->chunks);
     const uint32_t MG = mass_cols(g, Q);
+    // programmatic dependent launch between consecutive step kernels: only when
+    // nothing else sits between them in the stream (one chunk, no data plane, no
+    // profiling events)
+    const bool pdl = !g->comm && C == 1 && !prof;
     for (uint32_t k = k_first; k <= k_last; ++k) {
         StepArgs a;
         a.rowptr = g->rowptr;
@@ -439,7 +443,7 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
                 h.n_items = t.n_hub_items;
                 const int gh = t.n_hub_items ? table_grid(g, t.n_hub_items, std::max(1, step_hubs_occupancy())) : 0;
                 if (gh) {
-                    launch_step_hubs(h, gh, st);
+                    launch_step_hubs(h, gh, st, pdl);
                     ++launches;
                 }
                 StepArgs r = a;
@@ -448,14 +452,14 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
                 r.mass_partial = a.mass_partial + gh;
                 if (r.n_items) {
                     launch_step_tiles(r, g->tile, table_grid(g, r.n_items, std::max(1, step_tiles_occupancy(g->tile))),
-                                      st);
+                                      st, pdl);
                     ++launches;
                 }
                 if (prof) prof->after(st);
             } else if (t.n_items) {
                 const int grid = table_grid(g, t.n_items * Q, occ);
                 if (prof) prof->before(st);
-                launch_step(a, grid, st, &gq);
+                launch_step(a, grid, st, &gq, pdl);
                 if (prof) prof->after(st);
                 ++launches;
             }
@@ -529,6 +533,8 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
     }();
     const bool split = batch_split(g->nnz_loc);
     const bool use_ctr = dyn_jobs && !split;
+    // PDL between the fused step kernels (see run_steps): one chunk, no data plane, no profiling
+    const bool pdl = !g->comm && C == 1 && !prof;
     if (use_ctr) {
         const size_t need = static_cast<size_t>(K) * C;
         if (w->job_ctr_cap < need) {
@@ -604,7 +610,7 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                     if (use_ctr) b.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
                     b.mass_partial = mp_step + rows * B;
                     if (prof) prof->before(st);
-                    rows += W * launch_batch(b, static_cast<int>(B), grid, st, pa);
+                    rows += W * launch_batch(b, static_cast<int>(B), grid, st, pa, pdl && !pa);
                     if (prof) prof->after(st);
                     ++launches;
                 }

@@ -160,14 +160,15 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
                            int64_t piece, uint32_t slot_off, cudaStream_t st);
 
 // step_kernels.cu
-void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr);
+void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr, bool pdl = false);
 int step_occupancy(int tile);
-void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st);
-void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st);
+void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st, bool pdl = false);
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st, bool pdl = false);
 int step_tiles_occupancy(int tile);
 int step_hubs_occupancy();
 // batched launches return the grid they used (mass partial rows = grid * warps)
-int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
+int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr,
+                 bool pdl = false);
 int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
 int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);

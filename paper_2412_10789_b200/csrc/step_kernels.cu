@@ -116,6 +116,30 @@ __device__ __forceinline__ double2 ld_gather2_hot(const double* p, bool hot, uin
     return v;
 }
 
+// Programmatic dependent launch (sm_90+): the step kernels are launched with
+// programmatic stream serialization, so step k+1's CTAs can become resident as
+// step k's retire and run their prologue (work-item decode, row offsets, the
+// first index chunk: static graph data) before griddepcontrol.wait returns,
+// which is when step k has completed and its stores are visible.  Everything a
+// previous step wrote (iterates, acc, hub tickets/partials) is read after the
+// wait.  launch_dependents lets the next step's grid be scheduled at once.
+// The L1 is not coherent and is invalidated only at a kernel launch; under PDL
+// that launch precedes the end of the previous step, whose CTAs on the same SM
+// keep caching lines of the buffers it overwrites (its w_{k-1} rows, read
+// before they are rewritten) -- the gathers would hit them stale (measured:
+// config 3 lost parity).  So the wait is followed by a gpu-scope fence, which
+// invalidates the SM's L1 (CCTL.IVALL in the SASS).
+#ifndef CPG_PDL_FENCE
+#define CPG_PDL_FENCE 1  // A/B hook only: 0 is wrong under PDL (stale L1 lines)
+#endif
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#if CPG_PDL_FENCE
+    __threadfence();
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Deterministic CTA sum: xor butterfly per warp, warp partials summed in warp
 // order by thread 0.  Result valid in thread 0 only.
 template <int THREADS>
@@ -183,9 +207,9 @@ struct TileSmem {
 // stream, the epilogue operands of the rows this thread finalises), then the
 // gathers; one barrier; lane-group row sums from shared memory; one barrier;
 // the fused epilogue with thread t owning rows t and t + 256.
-template <int THREADS, int TILE>
+template <int THREADS, int TILE, bool PDL>
 __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, TileSmem<TILE>& sm,
-                                             double& mass) {
+                                             double& mass, bool& wait_pending) {
     constexpr int PER = TILE / THREADS;
     constexpr int RPT = kTileMaxRows / THREADS;
     const uint32_t rb = it.a;
@@ -202,6 +226,10 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
         idx[i] = j < cnt ? ld_index(colp + j) : 0u;
     }
     for (int j = threadIdx.x; j <= nrows; j += THREADS) sm.rp[j] = static_cast<int>(a.rowptr[rb + j] - e0);
+    if (PDL && wait_pending) {  // first item of this CTA: the previous step's iterate from here on
+        pdl_wait();
+        wait_pending = false;
+    }
     double w_prev[RPT], acc_old[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
@@ -249,9 +277,9 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
     __syncthreads();  // shared memory is reused by the next item
 }
 
-template <int THREADS>
+template <int THREADS, bool PDL>
 __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it, double* red,
-                                            int* flag, double& mass) {
+                                            int* flag, double& mass, bool& wait_pending) {
     constexpr int PER = kHubPieceEdges / THREADS;
     const uint32_t r = it.a, slot_base = it.b, hub = it.a;
     const int64_t p0 = code_e0(it.c);
@@ -266,6 +294,10 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
     for (int i = 0; i < PER; ++i) {
         const int64_t e = p0 + i * THREADS + threadIdx.x;
         idx[i] = e < p1 ? ld_index(a.col + e) : 0u;
+    }
+    if (PDL && wait_pending) {
+        pdl_wait();
+        wait_pending = false;
     }
     double vals[PER];
 #pragma unroll
@@ -315,6 +347,8 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
     __shared__ double red[THREADS / 32];
     __shared__ int flag;
     double mass = 0.0;
+    bool wait_pending = true;
+    pdl_launch_dependents();
     for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
         WorkItem it;
         const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
@@ -322,9 +356,9 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
         if (it.c & kHubBit)
-            process_hub<THREADS>(a, it, red, &flag, mass);
+            process_hub<THREADS, true>(a, it, red, &flag, mass, wait_pending);
         else
-            process_tile<THREADS, TILE>(a, it, sm, mass);
+            process_tile<THREADS, TILE, true>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
@@ -340,13 +374,14 @@ __global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs
     __shared__ double red[THREADS / 32];
     __shared__ int flag;
     double mass = 0.0;
+    bool wait_pending = true;
     for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
         WorkItem it;
         const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
         it.a = raw.x;
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        process_hub<THREADS>(a, it, red, &flag, mass);
+        process_hub<THREADS, false>(a, it, red, &flag, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
@@ -357,13 +392,14 @@ __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const S
     __shared__ TileSmem<TILE> sm;
     __shared__ double red[THREADS / 32];
     double mass = 0.0;
+    bool wait_pending = true;
     for (uint32_t i = blockIdx.x; i < a.n_items; i += gridDim.x) {
         WorkItem it;
         const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
         it.a = raw.x;
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        process_tile<THREADS, TILE>(a, it, sm, mass);
+        process_tile<THREADS, TILE, false>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
@@ -380,6 +416,7 @@ __global__ void __launch_bounds__(THREADS) cheby_step_group_kernel(const StepArg
     __shared__ double red[THREADS / 32];
     __shared__ int flag;
     double mass = 0.0;
+    bool wait_pending = false;  // launched plainly (PDL measured slower for query groups)
     const uint32_t total = a.n_items * gq.nq;
     uint32_t q_cur = 0u;
     for (uint32_t x = blockIdx.x; x < total; x += gridDim.x) {
@@ -405,9 +442,9 @@ __global__ void __launch_bounds__(THREADS) cheby_step_group_kernel(const StepArg
             aq.hub_partial = a.hub_partial + static_cast<size_t>(q_cur) * gq.part_stride;
             aq.hub_count = a.hub_count + static_cast<size_t>(q_cur) * gq.cnt_stride;
             if (it.c & kHubBit)
-                process_hub<THREADS>(aq, it, red, &flag, mass);
+                process_hub<THREADS, false>(aq, it, red, &flag, mass, wait_pending);
             else
-                process_tile<THREADS, TILE>(aq, it, sm, mass);
+                process_tile<THREADS, TILE, false>(aq, it, sm, mass, wait_pending);
         }
     }
     mass = block_sum<THREADS>(mass, red);
@@ -465,50 +502,95 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
     return j;
 }
 
-// Per-warp column sums of the mass (acceptance C13): every lane accumulates its
-// two columns in its own shared-memory cells, mcells[warp][row slot][column]
-// (one owner per cell: no atomics, no registers held across the row loop, no
-// CTA barrier).  At the end lane l of each warp sums its columns over the
-// warp's row slots into the warp's partial row; the warp order of the final
-// sum is fixed (mass_steps_batch_kernel), so with a static job stride the
+// Per-warp column sums of the mass (acceptance C13), two ways (MODE):
+//   1 = each lane keeps its two columns' sums in registers across its rows and
+//       the warp folds its row slots with an xor-shuffle tree at the end (no
+//       shared memory: the L1 carve-out stays whole for the gathers);
+//   0 = per-lane shared-memory cells mcells[warp][slot][column] (no registers
+//       held across the row loop).
+// The fused kernel uses 1 for B <= 16 and 0 for wider rows, whose instances
+// already spill; the split kernels use 0 (profiles/r02/ab_mass.txt).
+// CPG_MASS_MODE (compile-time A/B hook) forces 0, 1, or 2 = no mass (timing
+// only; batched mass_err then reads 1).  Every order is fixed (the warps are
+// summed in order by mass_steps_batch_kernel), so with a static job stride the
 // value is reproducible run to run.
+#ifndef CPG_MASS_MODE
+#define CPG_MASS_MODE -1
+#endif
+template <int PREF>
+constexpr int mass_mode() {
+    return CPG_MASS_MODE >= 0 ? CPG_MASS_MODE : PREF;
+}
+
 template <int B>
 __device__ __forceinline__ double* batch_mass_cell() {
-    __shared__ double mcells[kBatchThreads / 32][64];  // [warp][slot * B + column], RPW * B = 64
+    __shared__ __align__(16) double mcells[kBatchThreads / 32][64];  // [warp][slot * B + column], RPW * B = 64
     const int lane = threadIdx.x & 31;
     return &mcells[threadIdx.x >> 5][(lane / (B / 2)) * B + 2 * (lane % (B / 2))];
 }
 
-template <int B>
-__device__ __forceinline__ void batch_mass_init() {
-    double* c = batch_mass_cell<B>();
-    c[0] = 0.0;
-    c[1] = 0.0;
+template <int B, int MODE>
+__device__ __forceinline__ void batch_mass_init(double2& msum) {
+    msum = make_double2(0.0, 0.0);
+    if (MODE == 0) {
+        double* c = batch_mass_cell<B>();
+        c[0] = 0.0;
+        c[1] = 0.0;
+    }
 }
 
-template <int B>
-__device__ __forceinline__ void batch_mass_flush(const BatchArgs& a) {
+template <int B, int MODE>
+__device__ __forceinline__ void batch_mass_add(double2& msum, double m0, double m1) {
+    if (MODE == 0) {  // one 16-B shared load and store (the cell pair is 16-B aligned)
+        double2* mcell = reinterpret_cast<double2*>(batch_mass_cell<B>());
+        double2 c = *mcell;
+        c.x += m0;
+        c.y += m1;
+        *mcell = c;
+    } else if (MODE == 1) {
+        msum.x += m0;
+        msum.y += m1;
+    }
+}
+
+template <int B, int MODE>
+__device__ __forceinline__ void batch_mass_flush(const BatchArgs& a, double2 msum) {
     if (!a.mass_partial) return;  // uniform over the launch
     constexpr int L = B / 2;
     const int lane = threadIdx.x & 31;
+    double* dst = a.mass_partial + (static_cast<size_t>(blockIdx.x) * (kBatchThreads / 32) + (threadIdx.x >> 5)) * B;
+    if (MODE == 1) {
+        // lane = slot * L + cl: fold the row slots (lane bits >= log2 L) into slot 0
+#pragma unroll
+        for (int o = 16; o >= L; o >>= 1) {
+            msum.x += __shfl_xor_sync(0xffffffffu, msum.x, o);
+            msum.y += __shfl_xor_sync(0xffffffffu, msum.y, o);
+        }
+        if (lane < L) {
+            dst[2 * lane] = msum.x;
+            dst[2 * lane + 1] = msum.y;
+        }
+        return;
+    }
     __syncwarp();
     if (lane < L) {  // lane l sums its warp's row slots for columns 2l, 2l+1 (warp barrier only)
-        const double* c = batch_mass_cell<B>();  // slot 0 cells of this lane's columns
         double s0 = 0.0, s1 = 0.0;
+        if (MODE == 0) {
+            const double* c = batch_mass_cell<B>();  // slot 0 cells of this lane's columns
 #pragma unroll
-        for (int r = 0; r < 64 / B; ++r) {
-            s0 += c[r * B];
-            s1 += c[r * B + 1];
+            for (int r = 0; r < 64 / B; ++r) {
+                s0 += c[r * B];
+                s1 += c[r * B + 1];
+            }
         }
-        double* dst = a.mass_partial + (static_cast<size_t>(blockIdx.x) * (kBatchThreads / 32) + (threadIdx.x >> 5)) * B;
         dst[2 * lane] = s0;
         dst[2 * lane + 1] = s1;
     }
 }
 
-template <int B, bool PEER = false>
+template <int B, bool PEER, int MM>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArgs& pa, uint32_t r, double2 y,
-                                               int64_t d, int cl, double2 wp, double2 ac) {
+                                               int64_t d, int cl, double2 wp, double2 ac, double2& msum) {
     const uint32_t gr = a.row0 + r;
     double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
     if (d > 0) {
@@ -525,11 +607,8 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArg
             acc_new.x = ac.x + ck * w_new.x;
             acc_new.y = ac.y + ck * w_new.y;
         }
-        // sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v), per column: this lane's own
-        // shared-memory cells (no registers held across the row loop)
-        double* mcell = batch_mass_cell<B>();
-        mcell[0] += dd * w_new.x;
-        mcell[1] += dd * w_new.y;
+        // sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v), per column
+        batch_mass_add<B, MM>(msum, dd * w_new.x, dd * w_new.y);
     }
     reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl] = w_new;
     if (PEER) {  // fused all-gather: the row into every other rank's replica (NVLink stores)
@@ -586,17 +665,20 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 #endif
     constexpr uint32_t CLAIM = RPW > CPG_CLAIM_ROWS ? RPW : (CPG_CLAIM_ROWS / RPW) * RPW;
     unsigned int* const ctr = a.job_ctr;
-    batch_mass_init<B>();
+    pdl_launch_dependents();
+    // registers where they are free: B <= 16, or instances with fewer gathers in flight / CTAs
+    constexpr int MM = mass_mode<(B <= 16 || U <= 6 || MINB <= 3) ? 1 : 0>();
+    double2 msum;
+    batch_mass_init<B, MM>(msum);
     uint32_t claim_end = 0;
     uint32_t base_job = wg * RPW;
     if (ctr) {
         base_job = claim_jobs(ctr, lane, CLAIM);
         claim_end = base_job + CLAIM;
     }
+    bool wait_pending = true;
     for (; base_job < n_jobs;) {
         const BatchJob<B> j = batch_job<B>(a, base_job + slot, n_jobs);
-        double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
-        if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
         double2 s = {0.0, 0.0};
         uint32_t c[V], cn[V];
         {
@@ -607,6 +689,12 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
                 cn[v] = t < m0 ? ld_index(a.col + j.e0 + t) : 0u;
             }
         }
+        if (wait_pending) {  // the previous step's iterate, acc and hub tickets from here on
+            pdl_wait();
+            wait_pending = false;
+        }
+        double2 wp = {0.0, 0.0}, ac = {0.0, 0.0};
+        if (j.valid && !j.hub) batch_prefetch<B>(a, j.r, cl, wp, ac);
         for (int64_t e = j.e0; __any_sync(0xffffffffu, e < j.e1); e += 32) {
             const int m = static_cast<int>(e < j.e1 ? (j.e1 - e < 32 ? j.e1 - e : 32) : 0);
             // current chunk <- prefetched one; prefetch the next chunk (in flight during the gathers)
@@ -663,7 +751,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             }
         }
         (void)smask;
-        if (do_epi) batch_epilogue<B, PEER>(a, pa, j.r, y, j.d, cl, wp, ac);
+        if (do_epi) batch_epilogue<B, PEER, MM>(a, pa, j.r, y, j.d, cl, wp, ac, msum);
         if (!ctr) {
             base_job += nw * RPW;
         } else if (base_job + RPW < claim_end) {
@@ -674,7 +762,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
         }
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
-    batch_mass_flush<B>(a);
+    batch_mass_flush<B, MM>(a, msum);
 }
 
 // Plain-row batched step (rows [hub_rows, n_loc) of the chunk; hub pieces run
@@ -709,7 +797,9 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
         }
     };
     load_chunk(e0, e1);
-    batch_mass_init<B>();
+    constexpr int MM = mass_mode<0>();
+    double2 msum;
+    batch_mass_init<B, MM>(msum);
     while (__any_sync(0xffffffffu, r < r_end)) {
         const uint32_t rn = r + stride;
         int64_t ne0 = 0, ne1 = 0;
@@ -757,13 +847,13 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
             }
         }
         load_chunk(ne0, ne1);  // next row's first chunk, overlapping this epilogue
-        if (r < r_end) batch_epilogue<B, PEER>(a, pa, r, s, e1 - e0, cl, wp, ac);
+        if (r < r_end) batch_epilogue<B, PEER, MM>(a, pa, r, s, e1 - e0, cl, wp, ac, msum);
         r = rn;
         e0 = ne0;
         e1 = ne1;
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
-    batch_mass_flush<B>(a);
+    batch_mass_flush<B, MM>(a, msum);
 }
 
 // Hub-piece batched step (split path): the jobs are the hub pieces of the
@@ -812,7 +902,9 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     int64_t e0, e1;
     load_item(job, r, sb, e0, e1);
     load_chunk(c, e0, e1);
-    batch_mass_init<B>();
+    constexpr int MM = mass_mode<0>();
+    double2 msum;
+    batch_mass_init<B, MM>(msum);
     while (__any_sync(0xffffffffu, job < n_jobs)) {
         uint32_t nr, nsb;
         int64_t ne0, ne1;
@@ -873,7 +965,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             if (cl == 0) a.hub_count[r] = 0u;
             double2 wp, ac;
             batch_prefetch<B>(a, r, cl, wp, ac);
-            batch_epilogue<B, PEER>(a, pa, r, y, d, cl, wp, ac);
+            batch_epilogue<B, PEER, MM>(a, pa, r, y, d, cl, wp, ac, msum);
         }
         (void)smask;
         job += stride;
@@ -883,7 +975,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         e1 = ne1;
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
-    batch_mass_flush<B>(a);
+    batch_mass_flush<B, MM>(a, msum);
 }
 
 // ---------------------------------------------------------------------------
@@ -1015,23 +1107,52 @@ __global__ void mass_err_cols_kernel(const double* steps, uint32_t K, uint32_t c
 }
 
 // Host-side launch wrappers ---------------------------------------------------
-void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq) {
+// Step kernels go out with programmatic stream serialization (PDL, see
+// pdl_wait); CPG_PDL=0 launches them plainly (A/B hook; same results).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CPG_PDL");
+        return !e || e[0] != '0';
+    }();
+    return on;
+}
+
+// pdl: the caller's promise that the previous operation in `st` is the previous
+// step's kernel (no event record / wait or collective in between: those are not
+// ordered by griddepcontrol.wait, and a sharded run with them lost parity).
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(block));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq, bool pdl) {
     const bool group = gq && gq->nq > 1;
+    // query groups launch plainly: PDL measured 3% slower on config 1 (profiles/r02/pdl_ab.txt)
     if (a.tile == kTileMid) {
         if (group)
-            cheby_step_group_kernel<kStepThreads, kTileMid><<<grid, kStepThreads, 0, st>>>(a, *gq);
+            launch_pdl(false, cheby_step_group_kernel<kStepThreads, kTileMid>, grid, kStepThreads, st, a, *gq);
         else
-            cheby_step_kernel<kStepThreads, kTileMid><<<grid, kStepThreads, 0, st>>>(a);
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileMid>, grid, kStepThreads, st, a);
     } else if (a.tile == kTileLarge) {
         if (group)
-            cheby_step_group_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a, *gq);
+            launch_pdl(false, cheby_step_group_kernel<kStepThreads, kTileLarge>, grid, kStepThreads, st, a, *gq);
         else
-            cheby_step_kernel<kStepThreads, kTileLarge><<<grid, kStepThreads, 0, st>>>(a);
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileLarge>, grid, kStepThreads, st, a);
     } else {
         if (group)
-            cheby_step_group_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a, *gq);
+            launch_pdl(false, cheby_step_group_kernel<kStepThreads, kTileSmall>, grid, kStepThreads, st, a, *gq);
         else
-            cheby_step_kernel<kStepThreads, kTileSmall><<<grid, kStepThreads, 0, st>>>(a);
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileSmall>, grid, kStepThreads, st, a);
     }
 }
 // Split step: tile kernel instance for a tile width (MINB CTAs per SM).
@@ -1041,11 +1162,13 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* 
     case kTileMid: X(kTileMid, 6); break;                    \
     default: X(kTileLarge, 5); break;                        \
     }
-void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st) {
-    cheby_step_hubs_kernel<kStepThreads><<<grid, kStepThreads, 0, st>>>(a);
+void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st, bool) {
+    // the split step launches plainly: no PDL gain at its 20 ms steps, and the
+    // post-wait L1 invalidation cost 3% (profiles/r02/ab_fence.txt)
+    launch_pdl(false, cheby_step_hubs_kernel<kStepThreads>, grid, kStepThreads, st, a);
 }
-void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st) {
-#define CPG_L(T, M) cheby_step_tiles_kernel<kStepThreads, T, M><<<grid, kStepThreads, 0, st>>>(a)
+void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st, bool) {
+#define CPG_L(T, M) launch_pdl(false, cheby_step_tiles_kernel<kStepThreads, T, M>, grid, kStepThreads, st, a)
     CPG_TILES_SWITCH(CPG_L)
 #undef CPG_L
 }
@@ -1093,6 +1216,9 @@ int launch_slot_b(const BatchArgs& a, int cfg, cudaStream_t st) {
     case 45: return launch_slot<B, 4, 5>(a, st);
     case 46: return launch_slot<B, 4, 6>(a, st);
     case 64: return launch_slot<B, 6, 4>(a, st);
+    case 44: return launch_slot<B, 4, 4>(a, st);
+    case 83: return launch_slot<B, 8, 3>(a, st);
+    case 63: return launch_slot<B, 6, 3>(a, st);
     case 84: return launch_slot<B, 8, 4>(a, st);
     case 85: return launch_slot<B, 8, 5>(a, st);
     default: return 0;
@@ -1118,7 +1244,7 @@ int launch_slot_cfg(const BatchArgs& a, int B, int cfg, cudaStream_t st) {
     default: KERNEL<64, 8, 4, true><<<grid, kBatchThreads, 0, st>>>(a, pa); break;                          \
     }
 
-int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa, bool pdl) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_kernel, B, grid, st, a, *pa);
         return grid;
@@ -1130,11 +1256,13 @@ int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const Pee
     if (cfg)
         if (const int g = launch_slot_cfg(a, B, cfg, st)) return g;
     switch (B) {
-    case 4: cheby_batch_kernel<4><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 8: cheby_batch_kernel<8><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 16: cheby_batch_kernel<16><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    case 32: cheby_batch_kernel<32><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
-    default: cheby_batch_kernel<64><<<grid, kBatchThreads, 0, st>>>(a, PeerArgs{}); break;
+    case 4: launch_pdl(pdl, cheby_batch_kernel<4>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+    case 8: launch_pdl(pdl, cheby_batch_kernel<8>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+    case 16: launch_pdl(pdl, cheby_batch_kernel<16>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+    // B >= 32: 4 row gathers in flight per lane (the rows are 256-512 B; with the mass
+    // check in registers this beat U = 8 by 6% on config 2, profiles/r02/ab_slot64.txt)
+    case 32: launch_pdl(pdl, cheby_batch_kernel<32, 4>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+    default: launch_pdl(pdl, cheby_batch_kernel<64, 4>, grid, kBatchThreads, st, a, PeerArgs{}); break;
     }
     return grid;
 }

@@ -482,7 +482,7 @@ def test_gpu_ingest_matches_reference_loader(cpg, gpu, tmp_path):
     roff, rnb = ref.csr()
     assert np.array_equal(g.offsets(), roff) and np.array_equal(g.neighbor_array(), rnb)
     assert list(g.original_ids) == [1, 2, 3, 4]
-    with pytest.raises(cpg.ParameterError):
+    with pytest.raises(cpg.StructuralError):  # graph.cpp:156: StructuralError, like the reference
         cpg.ingest_edges([[5, 5]], 0)  # empty after cleaning
 
 
