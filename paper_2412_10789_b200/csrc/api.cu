@@ -423,6 +423,13 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
         a.first = k == 1;
         a.taylor = taylor;
         a.last = last_writes_out && k == K;
+#if CPG_CHECKED
+        a.chk_nnz = g->nnz_loc;
+        a.chk_npad = g->n_pad;
+        a.chk_nloc = g->n_loc;
+        a.chk_parts = g->n_partials;
+        a.chk_mass = MG;
+#endif
         StepGroup gq;
         gq.nq = Q;
         gq.vec_stride = g->n_pad;
@@ -450,6 +457,9 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
                 r.items = t.items + t.n_hub_items;
                 r.n_items = t.n_items - t.n_hub_items;
                 r.mass_partial = a.mass_partial + gh;
+#if CPG_CHECKED
+                r.chk_mass = MG - static_cast<uint32_t>(gh);
+#endif
                 if (r.n_items) {
                     launch_step_tiles(r, g->tile, table_grid(g, r.n_items, std::max(1, step_tiles_occupancy(g->tile))),
                                       st, pdl);
@@ -565,6 +575,12 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         b.first = k == 1;
         b.last = k == K;
         b.job_ctr = nullptr;
+#if CPG_CHECKED
+        b.chk_nnz = g->nnz_loc;
+        b.chk_npad = g->n_pad;
+        b.chk_nloc = g->n_loc;
+        b.chk_parts = bt.n_bpartials;
+#endif
         PeerArgs peer_args{nullptr, 0, 0};
         const PeerArgs* pa = nullptr;
         if (g->p2p) {  // fused all-gather: the epilogue stores into every replica
@@ -590,6 +606,9 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                     BatchArgs h = b;
                     h.n_loc = b.hub_rows;
                     h.mass_partial = mp_step + rows * B;
+#if CPG_CHECKED
+                    h.chk_mass = step_rows - rows;
+#endif
                     const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
                         1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
@@ -599,6 +618,9 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                 if (t.row_end > b.hub_rows) {
                     BatchArgs r = b;
                     r.mass_partial = mp_step + rows * B;
+#if CPG_CHECKED
+                    r.chk_mass = step_rows - rows;
+#endif
                     rows += W * launch_batch_rows(r, static_cast<int>(B), occ * g->sm_count, st, pa);
                     ++launches;
                 }
@@ -609,6 +631,9 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                     const int grid = occ * g->sm_count;
                     if (use_ctr) b.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
                     b.mass_partial = mp_step + rows * B;
+#if CPG_CHECKED
+                    b.chk_mass = step_rows - rows;
+#endif
                     if (prof) prof->before(st);
                     rows += W * launch_batch(b, static_cast<int>(B), grid, st, pa, pdl && !pa);
                     if (prof) prof->after(st);
@@ -1109,9 +1134,8 @@ int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const ui
                 cpg_stats s{};
                 const int rc = drive(g, coeffs, K, sources + q0, nullptr, cnt, 1, 0, d_res, true, st, &s);
                 if (rc != CPG_OK) fail(rc, cpg_last_error());
-                for (uint32_t j = 0; j < cnt; ++j)
-                    device_topk(d_res + static_cast<size_t>(j) * g->n, g->n, kk,
-                                ids + static_cast<size_t>(q0 + j) * kk, vals + static_cast<size_t>(q0 + j) * kk, st);
+                device_topk_batch(d_res, g->n, cnt, kk, ids + static_cast<size_t>(q0) * kk,
+                                  vals + static_cast<size_t>(q0) * kk, st);
                 acc.iterations = s.iterations;
                 acc.push_work += s.push_work;
                 acc.wall_seconds += s.wall_seconds;

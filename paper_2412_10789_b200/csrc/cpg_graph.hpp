@@ -196,7 +196,8 @@ void launch_mass_err_cols(const double* steps, uint32_t K, uint32_t count, const
                           cudaStream_t st);
 
 // topk.cu
-void device_topk(const double* d_vals, uint32_t n, uint32_t k, uint32_t* ids, double* vals, cudaStream_t st);
+void device_topk_batch(const double* d_vals, uint32_t n, uint32_t Q, uint32_t k, uint32_t* ids, double* vals,
+                       cudaStream_t st);
 // measure (eval.cpp:18-37) of [cols][n] device column pairs into d_reports[cols] (measure.cu)
 size_t measure_scratch_bytes(const cpg_graph* g, uint32_t cols);
 void launch_measure(const cpg_graph* g, const double* d_truth, const double* d_est, uint32_t cols, void* scratch,

@@ -16,8 +16,35 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace cpg {
+
+// Bounds-checked build (tools/build_variant.sh checked -DCPG_CHECKED=1): every
+// index into the CSR, the iterates, acc, the hub partials and the mass partials
+// is checked against the buffer sizes the host passes in the chk_* fields, and a
+// violation traps with the kernel, the index and the bound.  The default build
+// compiles the checks and the fields out.  (The pool's compute-sanitizer is
+// closed; this is the substitute, profiles/r02/checked/.)
+#ifndef CPG_CHECKED
+#define CPG_CHECKED 0
+#endif
+#if CPG_CHECKED
+#define CPG_CHECK(cond, what, idx, bound)                                                              \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("CPG_CHECK failed: %s index %llu bound %llu (block %d thread %d)\n", what,           \
+                   (unsigned long long)(idx), (unsigned long long)(bound), (int)blockIdx.x, (int)threadIdx.x); \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#define CPG_CHK_FIELDS uint64_t chk_nnz, chk_npad, chk_nloc, chk_parts, chk_mass;
+#else
+#define CPG_CHECK(cond, what, idx, bound) \
+    do {                                  \
+    } while (0)
+#define CPG_CHK_FIELDS
+#endif
 
 // Tile geometry of the single-source step (cheby_step_kernel).  The tile
 // width is chosen per graph at upload: kTileLarge when there are enough edges
@@ -90,6 +117,7 @@ struct StepArgs {
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
     int taylor;            // power method (PwMethod, solvers.cpp:87-116): w_k = D^-1 A w_{k-1}
     int last;              // write out = d * acc instead of acc
+    CPG_CHK_FIELDS         // CPG_CHECKED builds only: nnz_loc, n_pad, n_loc, hub partial slots, mass slots
 };
 
 // Query group (cheby_step_group_kernel): nq single-source queries in one
@@ -123,6 +151,7 @@ struct BatchArgs {
     int k, first, last;
     unsigned int* job_ctr;      // fused kernel: zeroed job counter (warps claim RPW jobs each); null = static stride
     double* mass_partial;       // [gridDim.x * warps][B] per-warp column sums of d_v w_{k+1}(v) (acceptance C13); null = off
+    CPG_CHK_FIELDS              // CPG_CHECKED builds only (partial / mass bounds in rows of B doubles)
 };
 
 // Fused all-gather (second parameter of the PEER instances of the batched

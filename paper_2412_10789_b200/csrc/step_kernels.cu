@@ -178,6 +178,7 @@ __device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, dou
         }
         mass += dd * w_new;
     }
+    CPG_CHECK(gr < a.chk_npad && r < a.chk_nloc, "step epilogue row", gr, a.chk_npad);
     a.w_io[gr] = w_new;
     if (a.last)
         a.out[r] = static_cast<double>(d) * acc_new;
@@ -218,6 +219,8 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
     const int cnt = static_cast<int>((it.c >> 40) & 0x3fff);
     const int lg = static_cast<int>((it.c >> 54) & 7);
     const uint32_t* colp = a.col + e0;
+    CPG_CHECK(static_cast<uint64_t>(e0) + cnt <= a.chk_nnz && nrows <= kTileMaxRows && cnt <= TILE, "tile edges",
+              e0 + cnt, a.chk_nnz);
 
     uint32_t idx[PER];
 #pragma unroll
@@ -247,6 +250,7 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int j = i * THREADS + threadIdx.x;
+            CPG_CHECK(j >= cnt || idx[i] < a.chk_npad, "tile gather", idx[i], a.chk_npad);
             if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[i]);
         }
     }
@@ -303,6 +307,8 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int64_t e = p0 + i * THREADS + threadIdx.x;
+        CPG_CHECK(e >= p1 || (idx[i] < a.chk_npad && static_cast<uint64_t>(e) < a.chk_nnz), "hub gather", idx[i],
+                  a.chk_npad);
         vals[i] = e < p1 ? ld_gather(a.w_cur + idx[i]) : 0.0;
     }
     double s = 0.0;
@@ -319,6 +325,7 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
         return;
     }
     if (threadIdx.x == 0) {
+        CPG_CHECK(slot_base + P <= a.chk_parts, "hub partial slot", slot_base + P, a.chk_parts);
         a.hub_partial[slot_base + piece] = s;
         __threadfence();
         const unsigned prev = atomicAdd(&a.hub_count[hub], 1u);
@@ -361,6 +368,7 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
             process_tile<THREADS, TILE, true>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
+    CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
@@ -384,6 +392,7 @@ __global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs
         process_hub<THREADS, false>(a, it, red, &flag, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
+    CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const S
         process_tile<THREADS, TILE, false>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
+    CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
@@ -559,6 +569,8 @@ __device__ __forceinline__ void batch_mass_flush(const BatchArgs& a, double2 msu
     constexpr int L = B / 2;
     const int lane = threadIdx.x & 31;
     double* dst = a.mass_partial + (static_cast<size_t>(blockIdx.x) * (kBatchThreads / 32) + (threadIdx.x >> 5)) * B;
+    CPG_CHECK(static_cast<uint64_t>(blockIdx.x + 1) * (kBatchThreads / 32) <= a.chk_mass, "batch mass row",
+              (blockIdx.x + 1) * (kBatchThreads / 32), a.chk_mass);
     if (MODE == 1) {
         // lane = slot * L + cl: fold the row slots (lane bits >= log2 L) into slot 0
 #pragma unroll
@@ -592,6 +604,7 @@ template <int B, bool PEER, int MM>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArgs& pa, uint32_t r, double2 y,
                                                int64_t d, int cl, double2 wp, double2 ac, double2& msum) {
     const uint32_t gr = a.row0 + r;
+    CPG_CHECK(gr < a.chk_npad && r < a.chk_nloc, "batch epilogue row", gr, a.chk_npad);
     double2 w_new = {0.0, 0.0}, acc_new = {0.0, 0.0};
     if (d > 0) {
         const double dd = static_cast<double>(d);
@@ -714,6 +727,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
                     val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
                                                                   u < a.hot_rows, pol_last, pol_first)
                                                  : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
@@ -730,7 +744,10 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
         double2 y = s;
         if (__any_sync(0xffffffffu, j.hub)) {
             if (j.hub)
+            {
+                CPG_CHECK(!j.hub || j.slot + j.P <= a.chk_parts, "batch hub slot", j.slot + j.P, a.chk_parts);
                 reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(j.slot + j.piece) * B)[cl] = s;
+            }
             __threadfence();
             __syncwarp();
             unsigned prev = 0;
@@ -834,6 +851,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
                     val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
                                                                   u < a.hot_rows, pol_last, pol_first)
                                                  : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
@@ -930,6 +948,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
                 for (int q = 0; q < U; ++q) {
                     const int t = t0 + q;
                     const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
                     val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
                                                                   u < a.hot_rows, pol_last, pol_first)
                                                  : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
@@ -947,6 +966,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         const int64_t d = re - rs;
         const uint32_t P = live ? static_cast<uint32_t>((d + HB - 1) / HB) : 0u;
         const uint32_t piece = live ? static_cast<uint32_t>((e0 - rs) / HB) : 0u;
+        CPG_CHECK(!live || sb + piece < a.chk_parts, "piece hub slot", sb + piece, a.chk_parts);
         if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[cl] = s;
         __threadfence();
         __syncwarp();

@@ -10,12 +10,14 @@
 //      order (deterministic), and a stable descending radix sort of the
 //      candidates by value gives (value desc, id asc), the reference's order.
 // If the threshold bin holds too many elements (massive ties), a stable sort
-// of the whole vector is used instead.
+// of the whole vector is used instead.  All columns of a query group share one
+// histogram pass, one host synchronisation and one scratch allocation.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "cpg_graph.hpp"
 
@@ -66,54 +68,76 @@ T* dmalloc(size_t count) {
 
 } // namespace
 
-// Top-k of d_vals[0..n) by (value desc, id asc) into host arrays.
-void device_topk(const double* d_vals, uint32_t n, uint32_t k, uint32_t* ids, double* vals, cudaStream_t st) {
+// Top-k of Q columns d_vals[q*n .. q*n + n) by (value desc, id asc) into host
+// arrays ids/vals [Q][k].  One histogram launch and one threshold launch for
+// all columns, ONE host synchronisation to learn the candidate counts, then per
+// column a select + stable sort (device scratch allocated once per call and
+// grown to the largest candidate set), one D2H of every column's result and a
+// final synchronisation.
+void device_topk_batch(const double* d_vals, uint32_t n, uint32_t Q, uint32_t k, uint32_t* ids, double* vals,
+                       cudaStream_t st) {
     k = std::min(k, n);
-    if (k == 0) return;
-    unsigned int* hist = dmalloc<unsigned int>(1 << 16);
-    unsigned int* meta = dmalloc<unsigned int>(3);
-    CPG_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) << 16, st));
-    k_hist16<<<1184, 256, 0, st>>>(d_vals, n, hist);
-    k_threshold<<<1, 32, 0, st>>>(hist, k, meta, meta + 1);
-    unsigned int bin_count[2] = {0, 0};
-    CPG_CUDA(cudaMemcpyAsync(bin_count, meta, sizeof(bin_count), cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    const uint32_t cand = bin_count[1];
-    const bool full = cand > (1u << 24);  // pathological ties: stable sort of everything
-    const uint32_t m = full ? n : cand;
-    uint32_t* c_ids = dmalloc<uint32_t>(m);
-    double* c_vals = dmalloc<double>(m);
-    uint32_t* s_ids = dmalloc<uint32_t>(m);
-    double* s_vals = dmalloc<double>(m);
-    void* tmp = nullptr;
-    size_t bytes = 0;
-    cub::CountingInputIterator<uint32_t> iota(0);
-    if (full) {
-        CPG_CUDA(cudaMemcpyAsync(c_vals, d_vals, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        bytes = 0;
-        cub::DeviceSelect::If(nullptr, bytes, iota, c_ids, meta + 2, n, AtLeastBin{d_vals, 0u}, st);
-        CPG_CUDA(cudaMalloc(&tmp, bytes));
-        CPG_CUDA(cub::DeviceSelect::If(tmp, bytes, iota, c_ids, meta + 2, n, AtLeastBin{d_vals, 0u}, st));
-        cudaFree(tmp);
-    } else {
-        bytes = 0;
-        cub::DeviceSelect::If(nullptr, bytes, iota, c_ids, meta + 2, n, AtLeastBin{d_vals, bin_count[0]}, st);
-        CPG_CUDA(cudaMalloc(&tmp, bytes));
-        CPG_CUDA(cub::DeviceSelect::If(tmp, bytes, iota, c_ids, meta + 2, n, AtLeastBin{d_vals, bin_count[0]}, st));
-        cudaFree(tmp);
-        k_gather_vals<<<std::max<uint32_t>(1, std::min<uint32_t>((m + 255) / 256, 1184)), 256, 0, st>>>(d_vals, c_ids,
-                                                                                                          m, c_vals);
+    if (k == 0 || Q == 0) return;
+    unsigned int* hist = dmalloc<unsigned int>(static_cast<size_t>(Q) << 16);
+    unsigned int* meta = dmalloc<unsigned int>(4 * static_cast<size_t>(Q));
+    std::vector<void*> owned{hist, meta};
+    auto release = [&] {
+        for (void* p : owned) cudaFree(p);
+    };
+    try {
+        CPG_CUDA(cudaMemsetAsync(hist, 0, (sizeof(unsigned int) << 16) * Q, st));
+        for (uint32_t q = 0; q < Q; ++q) {
+            k_hist16<<<1184, 256, 0, st>>>(d_vals + static_cast<size_t>(q) * n, n, hist + (static_cast<size_t>(q) << 16));
+            k_threshold<<<1, 32, 0, st>>>(hist + (static_cast<size_t>(q) << 16), k, meta + 2 * q, meta + 2 * q + 1);
+        }
+        std::vector<unsigned int> bc(2 * static_cast<size_t>(Q));
+        CPG_CUDA(cudaMemcpyAsync(bc.data(), meta, sizeof(unsigned int) * 2 * Q, cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaStreamSynchronize(st));
+        uint32_t mmax = 0;
+        for (uint32_t q = 0; q < Q; ++q) {
+            const bool full = bc[2 * q + 1] > (1u << 24);  // pathological ties: stable sort of everything
+            mmax = std::max(mmax, full ? n : bc[2 * q + 1]);
+        }
+        uint32_t* c_ids = dmalloc<uint32_t>(mmax);
+        double* c_vals = dmalloc<double>(mmax);
+        uint32_t* s_ids = dmalloc<uint32_t>(mmax);
+        double* s_vals = dmalloc<double>(mmax);
+        uint32_t* r_ids = dmalloc<uint32_t>(static_cast<size_t>(Q) * k);
+        double* r_vals = dmalloc<double>(static_cast<size_t>(Q) * k);
+        owned.insert(owned.end(), {c_ids, c_vals, s_ids, s_vals, r_ids, r_vals});
+        cub::CountingInputIterator<uint32_t> iota(0);
+        size_t b_sel = 0, b_sort = 0;
+        cub::DeviceSelect::If(nullptr, b_sel, iota, c_ids, meta + 2 * Q, n, AtLeastBin{d_vals, 0u}, st);
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, b_sort, c_vals, s_vals, c_ids, s_ids, mmax, 0, 64, st);
+        const size_t bytes = std::max(b_sel, b_sort);
+        void* tmp = dmalloc<char>(bytes);
+        owned.push_back(tmp);
+        for (uint32_t q = 0; q < Q; ++q) {
+            const double* v = d_vals + static_cast<size_t>(q) * n;
+            const bool full = bc[2 * q + 1] > (1u << 24);
+            const uint32_t m = full ? n : bc[2 * q + 1];
+            const unsigned bin = full ? 0u : bc[2 * q];
+            size_t b = bytes;
+            CPG_CUDA(cub::DeviceSelect::If(tmp, b, iota, c_ids, meta + 2 * Q + q, n, AtLeastBin{v, bin}, st));
+            k_gather_vals<<<std::max<uint32_t>(1, std::min<uint32_t>((m + 255) / 256, 1184)), 256, 0, st>>>(v, c_ids, m,
+                                                                                                          c_vals);
+            // stable descending sort by value: ties keep ascending id order (candidates are in id order)
+            b = bytes;
+            CPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, b, c_vals, s_vals, c_ids, s_ids, m, 0, 64, st));
+            CPG_CUDA(cudaMemcpyAsync(r_ids + static_cast<size_t>(q) * k, s_ids, sizeof(uint32_t) * k,
+                                     cudaMemcpyDeviceToDevice, st));
+            CPG_CUDA(cudaMemcpyAsync(r_vals + static_cast<size_t>(q) * k, s_vals, sizeof(double) * k,
+                                     cudaMemcpyDeviceToDevice, st));
+        }
+        CPG_CUDA(cudaMemcpyAsync(ids, r_ids, sizeof(uint32_t) * k * Q, cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaMemcpyAsync(vals, r_vals, sizeof(double) * k * Q, cudaMemcpyDeviceToHost, st));
+        CPG_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        cudaStreamSynchronize(st);
+        release();
+        throw;
     }
-    // stable descending sort by value: ties keep ascending id order (candidates are in id order)
-    bytes = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, c_vals, s_vals, c_ids, s_ids, m, 0, 64, st);
-    CPG_CUDA(cudaMalloc(&tmp, bytes));
-    CPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, c_vals, s_vals, c_ids, s_ids, m, 0, 64, st));
-    cudaFree(tmp);
-    CPG_CUDA(cudaMemcpyAsync(ids, s_ids, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaMemcpyAsync(vals, s_vals, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    CPG_CUDA(cudaStreamSynchronize(st));
-    for (void* p : {(void*)hist, (void*)meta, (void*)c_ids, (void*)c_vals, (void*)s_ids, (void*)s_vals}) cudaFree(p);
+    release();
 }
 
 } // namespace cpg
