@@ -137,6 +137,16 @@ def load_traffic(cfg_index, mode, tile):
         return None
 
 
+def load_gather_ceiling():
+    """Measured rate of random 8-B gathers from an L2-resident table (tools/gather_l2.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "gather", "gather_l2_c3.json")) as f:
+            rows = [json.loads(x) for x in f if x.startswith("{")]
+        return max(r["G_gathers_per_s"] for r in rows if r["variant"].startswith("ldg_U")) * 1e9
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -352,13 +362,33 @@ def run_reference(args, cfg):
             "setup_s": {"generate": t_gen, "samples": t_samples},
             # the reference arm maps only oracle/ libraries (checked, not assumed)
             "product_library_loaded": "paper_2412_10789_b200" in sys.modules}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 METRIC = "ChebyPower GTEPS (K*nnz*sources/s) on the config graph; queries/s and % HBM roofline alongside"
 
 
+# The JSON line is the only thing on stdout: native libraries print to fd 1 on their own
+# (NCCL's "NCCL version ..." banner at communicator init), so fd 1 is pointed at stderr for
+# the whole run and the line goes to a saved copy of the original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -525,15 +555,16 @@ def run_ours(args, cfg):
     outs = [torch.empty((len(sources), n) if host_out else (1, 1), dtype=torch.float64, pin_memory=True).numpy()
             for _ in range(2 if batched else 1)]
 
-    def step_host(i, pipelined):
+    def step_host(i, pipelined, last=True):
         st = P._lib.cpg_stats()
         out_np = outs[i % len(outs)]
         if not host_out:  # same steps and result all-gather (a collective), device output
             step_device()
             return st
-        if batched and pipelined:  # the result copy overlaps the next step (cpg_graph_sync at the end)
+        if batched and pipelined:  # the result copy overlaps the next step (cpg_graph_sync at the end);
+            # without stats the call returns once queued, so the next query is enqueued while this one runs
             P._check(L.cpg_chebypower_batched_async(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np),
-                                                    tile, out_np.ctypes.data, ctypes.byref(st)))
+                                                    tile, out_np.ctypes.data, ctypes.byref(st) if last else None))
         elif batched:
             P._check(L.cpg_chebypower_batched(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), tile,
                                               out_np.ctypes.data, ctypes.byref(st)))
@@ -550,7 +581,7 @@ def run_ours(args, cfg):
     e2.record(stream)
     t = time.perf_counter()
     for i in range(args.steps):
-        st = step_host(i, not args.sync_e2e)
+        st = step_host(i, not args.sync_e2e, last=i == args.steps - 1)
     P._check(L.cpg_graph_sync(dg.handle))  # the last step's result has landed in pinned memory
     wall_e2e = time.perf_counter() - t
     out_np = outs[(args.steps - 1) % len(outs)]
@@ -570,6 +601,16 @@ def run_ours(args, cfg):
         cpu = cpu_sample(cfg, off, nb, sources, K, budget_s=args.cpu_budget)
         cpu["threads_1"] = cpu_latency_1thread(cfg, off, nb, sources, K)
     csr.close()
+
+    # Single-source: random 8-B gathers bound the step.  Report the step's gather
+    # rate beside the measured ceiling of the gather alone (tools/gather_l2.cu, 192-200 G/s).
+    gather_ceiling = {}
+    if not batched:
+        rate = steps_per_launch * (nnz / world) / (per_launch_ms / 1e3)
+        ceil = load_gather_ceiling()
+        gather_ceiling = {"gathers_per_s": rate, "gather_ceiling_per_s": ceil,
+                          "frac_gather_ceiling": rate / ceil if ceil else None,
+                          "gather_ceiling_source": "profiles/r02/gather/gather_l2_c3.json (ldg_U16_occ4)"}
 
     if rank == 0:
         line = {
@@ -597,14 +638,15 @@ def run_ours(args, cfg):
                                      "step" if nnz // world >= (8 << 20) else "cheby_batch_kernel")
                                     if batched else "cheby_step_kernel"),
                          "bytes_per_launch": bytes_launch, "launch_ms": per_launch_ms, "steps_per_launch": steps_per_launch,
-                         "step_share_of_device_time": step_share},
+                         "step_share_of_device_time": step_share, **gather_ceiling},
             "e2e": {"value": e2e_gteps, "unit": "GTEPS",
                     "h2d_bytes_per_step": int(src_np.nbytes + c_np.nbytes),
                     "d2h_bytes_per_step": int(len(sources) * n * 8), "queries_per_s": queries / wall_e2e,
                     "d2h_ranks": "rank 0 (the result is all-gathered onto every rank)" if world > 1 else "rank 0",
                     "api": (("cpg_chebypower_batched" if args.sync_e2e else
-                             "cpg_chebypower_batched_async (result D2H of step i overlaps step i+1; "
-                             "cpg_graph_sync before the clock stops)") if batched else "cpg_chebypower"),
+                             "cpg_chebypower_batched_async (result D2H of step i overlaps step i+1, step i+1 "
+                             "is enqueued while step i runs; cpg_graph_sync before the clock stops)")
+                            if batched else "cpg_chebypower"),
                     "host_out": "pinned, two buffers alternating" if batched else "pinned"},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
@@ -614,7 +656,7 @@ def run_ours(args, cfg):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+        emit(line)
     dg.close()
     if pg is not None:
         pg.destroy_process_group()

@@ -199,7 +199,9 @@ int cpg_chebypower_batched_device(cpg_graph* g, const double* coeffs, uint32_t K
  * once the steps are computed, with the device->host copy of the last tile into
  * `out` still in flight on the handle's copy stream, so it overlaps the next
  * call's steps.  `out` (pinned host memory for a true overlap) must stay valid
- * and unread until cpg_graph_sync returns. */
+ * and unread until cpg_graph_sync returns.  With stats == NULL the call does not
+ * wait for its steps either: it returns once everything is queued, so the host
+ * enqueues the next query while the GPU computes this one. */
 int cpg_chebypower_batched_async(cpg_graph* g, const double* coeffs, uint32_t K,
                                  const uint32_t* sources, uint32_t n_sources, uint32_t tile,
                                  double* out, cpg_stats* stats);

@@ -841,7 +841,10 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
             CPG_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(user_stream), w->ev[4], 0));
         }
         float ms = 0.f;
-        if (!user_stream || stats) {
+        // A pipelined call without stats returns with its steps still queued: the host
+        // enqueues the next query while the GPU works (cpg_graph_sync waits for all).
+        const bool defer = pipelined && !stats;
+        if (!defer && (!user_stream || stats)) {
             if (g->comm)
                 g->comm->sync(st);  // polls the communicator's async error
             else
