@@ -203,6 +203,23 @@ size_t default_max_ws(const cpg_graph* g) {
     return m;
 }
 
+// L2 set-aside for persisting lines (CPG_L2_PERSIST_MB, A/B hook; unset = leave the
+// device setting alone).  The hot prefix of the batched iterate is gathered with an
+// L2::evict_last policy; the set-aside is the portion of L2 such lines may claim.
+void l2_set_aside(int device) {
+    const char* e = std::getenv("CPG_L2_PERSIST_MB");
+    if (!e) return;
+    cudaDeviceProp prop{};
+    CPG_CUDA(cudaGetDeviceProperties(&prop, device));
+    const size_t want = std::min<size_t>(static_cast<size_t>(std::atoll(e)) << 20,
+                                         static_cast<size_t>(prop.persistingL2CacheMaxSize));
+    CPG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    std::fprintf(stderr, "[cpg] L2 persisting set-aside %zu MB (max %d MB)\n", got >> 20,
+                 prop.persistingL2CacheMaxSize >> 20);
+}
+
 cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t n, uint64_t nnz, int device,
                          int rank, int nranks, Comm* comm, int chunks = 0) {
     auto g = std::make_unique<cpg_graph>();
@@ -223,6 +240,7 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
                                            std::max(1, step_tiles_occupancy(g->tile))) * g->sm_count);
     g->comm = comm;
     g->max_ws = default_max_ws(g.get());
+    l2_set_aside(device);
     CPG_CUDA(cudaStreamSynchronize(g->stream));
     return g.release();
 }

@@ -47,6 +47,18 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 #define CPG_L2_HINTS 0  // measured neutral on configs 3-5 (profiles/r01/l2_hints_ab.txt)
 #endif
 
+__device__ __forceinline__ uint32_t ld_index(const uint32_t* p);
+__device__ __forceinline__ uint32_t ld_index_b(const uint32_t* p) {  // batched kernels' index stream
+#if CPG_STREAM_EF
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(p), "l"(policy_evict_first()));
+    return v;
+#else
+    return ld_index(p);
+#endif
+}
 __device__ __forceinline__ uint32_t ld_index(const uint32_t* p) {
     uint32_t v;
 #if CPG_L2_HINTS
@@ -139,6 +151,35 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// Batched-step streams (CPG_STREAM_EF, A/B hook): the epilogue's loads of w_{k-1}
+// and acc and its stores of w_{k+1} and acc touch each line once per step; with
+// an L2::evict_first policy they neither displace the gathered hot prefix
+// (evict_last) nor keep the previous step's hot lines -- the buffer now being
+// overwritten -- at evict_last priority beside the current ones.
+#ifndef CPG_STREAM_EF
+#define CPG_STREAM_EF 1  // +0.3-1.6% on configs 1-5 (profiles/r02/ab/ab_streamef.txt)
+#endif
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+#if CPG_STREAM_EF
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(policy_evict_first()));
+    return v;
+#else
+    return *reinterpret_cast<const double2*>(p);
+#endif
+}
+__device__ __forceinline__ void st_stream2(double* p, double2 v) {
+#if CPG_STREAM_EF
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "l"(policy_evict_first())
+                 : "memory");
+#else
+    *reinterpret_cast<double2*>(p) = v;
+#endif
+}
 
 // Deterministic CTA sum: xor butterfly per warp, warp partials summed in warp
 // order by thread 0.  Result valid in thread 0 only.
@@ -623,16 +664,16 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArg
         // sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v), per column
         batch_mass_add<B, MM>(msum, dd * w_new.x, dd * w_new.y);
     }
-    reinterpret_cast<double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl] = w_new;
+    st_stream2(a.w_io + static_cast<size_t>(gr) * B + 2 * cl, w_new);
     if (PEER) {  // fused all-gather: the row into every other rank's replica (NVLink stores)
         for (int p = 0; p < pa.n_peer; ++p)
             if (p != pa.self) reinterpret_cast<double2*>(pa.peer_io[p] + static_cast<size_t>(gr) * B)[cl] = w_new;
     }
     if (a.last) {
         const double dd = static_cast<double>(d);
-        reinterpret_cast<double2*>(a.out + static_cast<size_t>(r) * B)[cl] = make_double2(dd * acc_new.x, dd * acc_new.y);
+        st_stream2(a.out + static_cast<size_t>(r) * B + 2 * cl, make_double2(dd * acc_new.x, dd * acc_new.y));
     } else {
-        reinterpret_cast<double2*>(a.acc + static_cast<size_t>(r) * B)[cl] = acc_new;
+        st_stream2(a.acc + static_cast<size_t>(r) * B + 2 * cl, acc_new);
     }
 }
 
@@ -650,8 +691,8 @@ __device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, i
         wp = reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl];
         ac = make_double2(0.0, 0.0);
     } else {
-        wp = reinterpret_cast<const double2*>(a.w_io + static_cast<size_t>(gr) * B)[cl];
-        ac = reinterpret_cast<const double2*>(a.acc + static_cast<size_t>(r) * B)[cl];
+        wp = ld_stream2(a.w_io + static_cast<size_t>(gr) * B + 2 * cl);
+        ac = ld_stream2(a.acc + static_cast<size_t>(r) * B + 2 * cl);
     }
 }
 
@@ -699,7 +740,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const int t = v * L + cl;
-                cn[v] = t < m0 ? ld_index(a.col + j.e0 + t) : 0u;
+                cn[v] = t < m0 ? ld_index_b(a.col + j.e0 + t) : 0u;
             }
         }
         if (wait_pending) {  // the previous step's iterate, acc and hub tickets from here on
@@ -717,7 +758,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             for (int v = 0; v < V; ++v) {
                 c[v] = cn[v];
                 const int t = v * L + cl;
-                cn[v] = t < mn ? ld_index(a.col + en + t) : 0u;
+                cn[v] = t < mn ? ld_index_b(a.col + en + t) : 0u;
             }
 #pragma unroll
             for (int t0 = 0; t0 < 32; t0 += U) {
@@ -810,7 +851,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int t = v * L + cl;
-            c[v] = t < m ? ld_index(a.col + e + t) : 0u;
+            c[v] = t < m ? ld_index_b(a.col + e + t) : 0u;
         }
     };
     load_chunk(e0, e1);
@@ -840,7 +881,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const int t = v * L + cl;
-                    cn[v] = t < mn ? ld_index(a.col + en + t) : 0u;
+                    cn[v] = t < mn ? ld_index_b(a.col + en + t) : 0u;
                 }
             }
 #pragma unroll
@@ -913,7 +954,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int t = v * L + cl;
-            dst[v] = t < m ? ld_index(a.col + e + t) : 0u;
+            dst[v] = t < m ? ld_index_b(a.col + e + t) : 0u;
         }
     };
     uint32_t r, sb;
