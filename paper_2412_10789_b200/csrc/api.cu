@@ -144,7 +144,7 @@ void ws_destroy(cpg_graph* g, Workspace* w) {
     dfree_aligned(w->acc);
     w->acc = nullptr;
     for (void* p : {(void*)w->full, (void*)w->hub_partial, (void*)w->hub_count, (void*)w->bhub_partial,
-                    (void*)w->bhub_count, (void*)w->d_job_ctr, (void*)w->d_coeffs, (void*)w->d_sources,
+                    (void*)w->bhub_count, (void*)w->d_job_ctr, (void*)w->d_wctr, (void*)w->d_coeffs, (void*)w->d_sources,
                     (void*)w->d_mass_partial, (void*)w->d_step_mass, (void*)w->d_mass0, (void*)w->d_seeds,
                     (void*)w->d_stage, (void*)w->d_topk, (void*)w->d_peers_a, (void*)w->d_peers_b,
                     (void*)w->d_barrier})
@@ -235,6 +235,9 @@ cpg_graph* create_common(const uint64_t* d_off, const uint32_t* d_nbr, uint32_t 
     const int occ = std::max(1, step_occupancy(g->tile));
     g->step_grid = 1;  // max over chunks: the mass-partial stride
     for (const auto& t : g->tables) g->step_grid = std::max(g->step_grid, table_grid(g.get(), t.n_items, occ));
+    // the warp-tile step's hub + warp grids share one mass-partial row too
+    g->step_grid = std::max(g->step_grid, (std::max(1, step_hubs_occupancy()) +
+                                           std::max(1, step_warp_occupancy())) * g->sm_count);
     // the split step's two grids share one mass-partial row
     g->step_grid = std::max(g->step_grid, (std::max(1, step_hubs_occupancy()) +
                                            std::max(1, step_tiles_occupancy(g->tile))) * g->sm_count);
@@ -406,6 +409,13 @@ uint32_t single_hot_rows(const cpg_graph* g) {
     return static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (static_cast<uint64_t>(std::atoll(e)) << 20) / 8));
 }
 
+// Single-source step as CTA hub pieces + barrier-free warp tiles
+// (cheby_step_warp_kernel); CPG_WARP_TILES=1/0 (read per call).
+bool warp_tiles(const cpg_graph*) {
+    const char* e = std::getenv("CPG_WARP_TILES");
+    return e && e[0] == '1';
+}
+
 // Single-source step as hub-piece + row-tile kernels: by default when the
 // iterate exceeds L2 (build_device_graph); CPG_STEP_SPLIT=1/0 forces (read per call).
 bool step_split(const cpg_graph* g) {
@@ -424,6 +434,16 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
     // nothing else sits between them in the stream (one chunk, no data plane, no
     // profiling events)
     const bool pdl = !g->comm && C == 1 && !prof;
+    const bool wt = Q == 1 && warp_tiles(g);
+    if (wt) {  // one item counter per (step, chunk) of this call
+        const size_t need = static_cast<size_t>(k_last - k_first + 1) * C;
+        if (w->wctr_cap < need) {
+            dfree(w->d_wctr);
+            w->d_wctr = dalloc<unsigned int>(need);
+            w->wctr_cap = need;
+        }
+        CPG_CUDA(cudaMemsetAsync(w->d_wctr, 0, sizeof(unsigned int) * need, st));
+    }
     for (uint32_t k = k_first; k <= k_last; ++k) {
         StepArgs a;
         a.rowptr = g->rowptr;
@@ -462,7 +482,31 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
             a.n_items = t.n_items;
             a.row0 = chunk_row0(g, c);
             a.mass_partial = w->d_mass_partial + (static_cast<size_t>(k - 1) * C + c) * MG;
-            if (t.n_items && Q == 1 && step_split(g)) {  // hub pieces, then row tiles at higher occupancy
+            const ItemTable& tw = g->wtables[c];
+            if (wt && tw.n_items) {  // CTA hub pieces, then barrier-free warp tiles
+                if (prof) prof->before(st);
+                StepArgs h = a;
+                h.items = tw.items;
+                h.n_items = tw.n_hub_items;
+                const int gh = tw.n_hub_items ? table_grid(g, tw.n_hub_items, std::max(1, step_hubs_occupancy())) : 0;
+                if (gh) {
+                    launch_step_hubs(h, gh, st);
+                    ++launches;
+                }
+                StepArgs r = a;
+                r.items = tw.items + tw.n_hub_items;
+                r.n_items = tw.n_items - tw.n_hub_items;
+                r.mass_partial = a.mass_partial + gh;
+#if CPG_CHECKED
+                r.chk_mass = MG - static_cast<uint32_t>(gh);
+#endif
+                if (r.n_items) {
+                    launch_step_warp(r, w->d_wctr + static_cast<size_t>(k - k_first) * C + c,
+                                     std::max(1, step_warp_occupancy()) * g->sm_count, st);
+                    ++launches;
+                }
+                if (prof) prof->after(st);
+            } else if (t.n_items && Q == 1 && step_split(g)) {  // hub pieces, then row tiles at higher occupancy
                 if (prof) prof->before(st);
                 StepArgs h = a;
                 h.n_items = t.n_hub_items;
@@ -1053,6 +1097,7 @@ int cpg_graph_destroy(cpg_graph* g) {
         delete g->comm;
         g->comm = nullptr;
         for (auto& t : g->tables) cudaFree(t.items);
+        for (auto& t : g->wtables) cudaFree(t.items);
         for (auto& kv : g->btabs)
             for (auto& t : kv.second.tables)
                 if (t.items) cudaFree(t.items);

@@ -76,6 +76,8 @@ struct Workspace {
     unsigned int* bhub_count = nullptr; // [n_loc]
     unsigned int* d_job_ctr = nullptr;  // fused batched kernel: one job counter per (step, chunk)
     size_t job_ctr_cap = 0;
+    unsigned int* d_wctr = nullptr;     // warp-tile single-source step: one item counter per (step, chunk)
+    size_t wctr_cap = 0;
 
     double* d_coeffs = nullptr;
     size_t coeff_cap = 0;
@@ -123,6 +125,7 @@ struct cpg_graph {
     uint32_t* new_of_old = nullptr; // [n]
 
     std::vector<cpg::ItemTable> tables;   // single-source items, one table per chunk
+    std::vector<cpg::ItemTable> wtables;  // warp-tile items (cheby_step_warp_kernel), one per chunk
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0, n_tiles = 0, n_partials = 0;
     int tile = 0;                   // kTileSmall / kTileMid / kTileLarge
     bool step_split = false;        // single-source step as hub + tile kernels (iterate > L2)
@@ -157,7 +160,9 @@ const BatchTables& ensure_batch_tables(cpg_graph* g, int B);
 void* dalloc_aligned(size_t bytes);
 void dfree_aligned(void* p);
 ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t chunk, uint32_t max_rows,
-                           int64_t piece, uint32_t slot_off, cudaStream_t st);
+                           int64_t piece, uint32_t slot_off, cudaStream_t st, int64_t hub_thr = 0, int64_t solo = 0);
+void launch_step_warp(const StepArgs& a, unsigned int* ctr, int grid, cudaStream_t st);
+int step_warp_occupancy();
 
 // step_kernels.cu
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq = nullptr, bool pdl = false);

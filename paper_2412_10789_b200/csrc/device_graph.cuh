@@ -55,6 +55,9 @@ constexpr int kTileMid = 2048;                   // edges staged per tile (16 KB
 constexpr int kTileLarge = 4096;                 // edges staged per tile (32 KB smem)
 constexpr int kTileMaxRows = 512;                // rows per tile (2 epilogue rows per thread)
 constexpr int kHubPieceEdges = 4096;             // edges per hub piece (16 per thread)
+constexpr int kWarpTileEdges = 512;              // warp tiles: edges per tile (16 per lane)
+constexpr int kWarpTileRows = 64;                // warp tiles: rows per tile (2 epilogue rows per lane)
+constexpr int kWarpLongRow = 4096;               // warp tiles: longest row swept by one warp
 
 // Batched (SpMM) geometry: one warp per row job, 64 columns, double2 per lane.
 constexpr int kBatchCols = 64;

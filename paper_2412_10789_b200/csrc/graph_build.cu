@@ -132,12 +132,15 @@ __global__ void k_hub_items(const int64_t* rowptr, uint32_t row0, const uint32_t
 // A row starts a tile when its first edge falls in a new chunk of tile/2 edges
 // (or every kTileMaxRows rows).  All rows of a tile start inside one chunk and
 // non-hub rows have <= tile/2 edges, so a tile holds <= tile edges.
+// solo > 0: rows of more than `solo` edges form a tile of their own (warp tiles).
 __global__ void k_tile_flags(const int64_t* rowptr, uint32_t first, uint32_t n_loc, int64_t chunk, uint32_t max_rows,
-                             uint8_t* flags) {
+                             uint8_t* flags, int64_t solo = 0) {
     for (uint64_t j = first + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_loc;
          j += (uint64_t)gridDim.x * blockDim.x) {
         bool start = (j == first) || ((j - first) % max_rows == 0) ||
                      (rowptr[j] / chunk != rowptr[j - 1] / chunk);
+        if (solo > 0 && j > first)
+            start = start || rowptr[j + 1] - rowptr[j] > solo || rowptr[j] - rowptr[j - 1] > solo;
         flags[j - first] = start ? 1 : 0;
     }
 }
@@ -198,12 +201,13 @@ void build_hub_items(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_
 // split into `piece`-edge pieces, partial slots from slot_off) then row tiles
 // (<= 2*chunk edges, <= max_rows rows).
 ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_t chunk, uint32_t max_rows,
-                           int64_t piece, uint32_t slot_off, cudaStream_t st) {
+                           int64_t piece, uint32_t slot_off, cudaStream_t st, int64_t hub_thr, int64_t solo) {
     DevTemp tmp;
     size_t bytes = 0;
     WorkItem* hub_items = nullptr;
     uint32_t n_hub = 0, n_hub_items = 0;
-    build_hub_items(rowptr, row0, row1, chunk, piece, slot_off, &hub_items, &n_hub, &n_hub_items, 0, st);
+    build_hub_items(rowptr, row0, row1, hub_thr > 0 ? hub_thr : chunk, piece, slot_off, &hub_items, &n_hub,
+                    &n_hub_items, 0, st);
     uint32_t n_tiles = 0;
     uint32_t* starts = nullptr;
     const uint32_t first = row0 + n_hub;
@@ -212,7 +216,7 @@ ItemTable build_item_table(const int64_t* rowptr, uint32_t row0, uint32_t row1, 
         uint8_t* flags = dalloc<uint8_t>(rows);
         starts = dalloc<uint32_t>(rows);
         unsigned int* d_sel = dalloc<unsigned int>(1);
-        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(rowptr, first, row1, chunk, max_rows, flags);
+        k_tile_flags<<<grid_for(rows), kT, 0, st>>>(rowptr, first, row1, chunk, max_rows, flags, solo);
         cub::CountingInputIterator<uint32_t> it(first);
         cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, starts, d_sel, rows, st);
         tmp.ensure(bytes);
@@ -337,7 +341,18 @@ void build_device_graph(cpg_graph* g, const uint64_t* d_off, const uint32_t* d_n
         slots += t.n_hub_items;  // one partial slot per hub piece
         g->tables.push_back(t);
     }
-    g->n_partials = slots;
+    // warp-tile tables (cheby_step_warp_kernel): rows above kWarpLongRow edges are hub
+    // pieces, rows above kWarpTileEdges/2 single-row items, the rest tiles of <= 512 edges
+    // and <= 64 rows.  Their hub pieces take partial slots after the CTA tables'.
+    g->wtables.clear();
+    uint32_t wslots = 0;
+    for (uint32_t c = 0; c < C; ++c) {
+        ItemTable t = build_item_table(g->rowptr, c * g->cr, (c + 1) * g->cr, kWarpTileEdges / 2, kWarpTileRows,
+                                       kHubPieceEdges, wslots, st, kWarpLongRow, kWarpTileEdges / 2);
+        wslots += t.n_hub_items;
+        g->wtables.push_back(t);
+    }
+    g->n_partials = std::max(slots, wslots);
     g->n_items = g->n_hubs = g->n_hub_items = g->n_tiles = 0;
     for (const auto& t : g->tables) {
         g->n_items += t.n_items;

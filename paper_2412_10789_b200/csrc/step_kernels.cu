@@ -456,6 +456,122 @@ __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const S
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-tile single-source step (CPG_WARP_TILES; round 2): every warp works its
+// own items with no CTA barrier.  Items (graph_build.cu build_warp_table):
+//   * tiles of <= kWarpTileEdges edges and <= 64 rows of degree <= kWarpTileEdges/2:
+//     the warp loads the 16 indices per lane (coalesced), the rows' offsets and
+//     epilogue operands, issues its 16 gathers, stages them in its own shared
+//     slice, sums each row with a lane group sized to the tile's mean degree
+//     (__syncwarp only), and runs the fused epilogue for rows lane, lane + 32;
+//   * single rows of kWarpTileEdges/2 < degree <= kWarpLongRow: the warp sweeps
+//     the row 32*U edges at a time, sums in registers and reduces with shuffles;
+//   * rows above kWarpLongRow are CTA hub pieces (cheby_step_hubs_kernel).
+// Warps claim items from a per-(step, chunk) counter (one atomic per item).
+// Summation orders are fixed (lane groups / xor trees), so results are
+// bit-reproducible run to run, like the CTA tiles.
+struct WarpTileSmem {
+    double vals[kWarpTileEdges];
+    double ysum[kWarpTileRows];
+    int rp[kWarpTileRows + 1];
+};
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 4) cheby_step_warp_kernel(const StepArgs a, unsigned int* ctr) {
+    __shared__ WarpTileSmem smw[WARPS];
+    __shared__ double red[WARPS];
+    constexpr int PER = kWarpTileEdges / 32;  // indices / gathers per lane of a tile
+    constexpr int U = 16;                     // gathers in flight per lane on a long row
+    const int lane = threadIdx.x & 31;
+    WarpTileSmem& sm = smw[threadIdx.x >> 5];
+    double mass = 0.0;
+    for (;;) {
+        uint32_t i = 0;
+        if (lane == 0) i = atomicAdd(ctr, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= a.n_items) break;
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.items) + i);
+        const uint32_t rb = raw.x;
+        const int nrows = static_cast<int>(raw.y - raw.x);
+        const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+        const int64_t e0 = code_e0(c);
+        const int cnt = code_cnt(c);
+        const int lg = static_cast<int>((c >> 54) & 7);
+        CPG_CHECK(static_cast<uint64_t>(e0) + cnt <= a.chk_nnz && nrows <= kWarpTileRows, "warp tile", e0 + cnt,
+                  a.chk_nnz);
+        if (nrows == 1 && cnt > kWarpTileEdges / 2) {  // one long row, swept by the whole warp
+            double w_prev = 0.0, acc_old = 0.0;
+            if (lane == 0) load_prev(a, rb, w_prev, acc_old);
+            double s = 0.0;
+            for (int base = 0; base < cnt; base += 32 * U) {
+                uint32_t idx[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int j = base + q * 32 + lane;
+                    idx[q] = j < cnt ? ld_index(a.col + e0 + j) : 0u;
+                }
+                double v[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int j = base + q * 32 + lane;
+                    CPG_CHECK(j >= cnt || idx[q] < a.chk_npad, "warp long gather", idx[q], a.chk_npad);
+                    v[q] = j < cnt ? ld_gather(a.w_cur + idx[q]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q) s += v[q];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) step_epilogue(a, rb, s, cnt, w_prev, acc_old, mass);
+            continue;
+        }
+        uint32_t idx[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int j = q * 32 + lane;
+            idx[q] = j < cnt ? ld_index(a.col + e0 + j) : 0u;
+        }
+        for (int j = lane; j <= nrows; j += 32) sm.rp[j] = static_cast<int>(a.rowptr[rb + j] - e0);
+        double w_prev[2], acc_old[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int r = q * 32 + lane;
+            if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int j = q * 32 + lane;
+            CPG_CHECK(j >= cnt || idx[q] < a.chk_npad, "warp tile gather", idx[q], a.chk_npad);
+            if (j < cnt) sm.vals[j] = ld_gather(a.w_cur + idx[q]);
+        }
+        __syncwarp();
+        const int g = 1 << lg;
+        const int sub = lane & (g - 1);
+        const int grp = lane >> lg;
+        const int ngrp = 32 >> lg;
+        for (int base = 0; base < nrows; base += ngrp) {
+            const int r = base + grp;
+            double s = 0.0;
+            if (r < nrows) {
+                const int b1 = sm.rp[r + 1];
+                for (int j = sm.rp[r] + sub; j < b1; j += g) s += sm.vals[j];
+            }
+            for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (r < nrows && sub == 0) sm.ysum[r] = s;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int r = q * 32 + lane;
+            if (r < nrows) step_epilogue(a, rb + r, sm.ysum[r], sm.rp[r + 1] - sm.rp[r], w_prev[q], acc_old[q], mass);
+        }
+        __syncwarp();  // the warp's shared slice is reused by its next item
+    }
+    mass = block_sum<WARPS * 32>(mass, red);
+    CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
+    if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
+}
+
 // Query group: nq single-source queries per launch (small graphs, where one
 // query cannot fill the GPU).  Items x queries: job x = q * n_items + i, so a
 // CTA's queries are nondecreasing and its mass partial is flushed once per
@@ -1232,6 +1348,16 @@ void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st, b
 #define CPG_L(T, M) launch_pdl(false, cheby_step_tiles_kernel<kStepThreads, T, M>, grid, kStepThreads, st, a)
     CPG_TILES_SWITCH(CPG_L)
 #undef CPG_L
+}
+constexpr int kWarpKernelWarps = 8;
+void launch_step_warp(const StepArgs& a, unsigned int* ctr, int grid, cudaStream_t st) {
+    cheby_step_warp_kernel<kWarpKernelWarps><<<grid, kWarpKernelWarps * 32, 0, st>>>(a, ctr);
+}
+int step_warp_occupancy() {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_step_warp_kernel<kWarpKernelWarps>,
+                                                  kWarpKernelWarps * 32, 0);
+    return blocks;
 }
 int step_tiles_occupancy(int tile) {
     int blocks = 0;

@@ -297,6 +297,35 @@ def test_both_tile_widths(cpg, gpu, tile, monkeypatch):
             assert_parity(est.values, want)
 
 
+@pytest.mark.parametrize("graph", ["chunglu_hubs", "rmat", "ring"])
+def test_warp_tile_step(cpg, gpu, graph, monkeypatch):
+    """The barrier-free warp-tile single-source step (CPG_WARP_TILES=1): CTA hub pieces for
+    rows above 4096 edges, single-row warp sweeps for 256 < degree <= 4096, 512-edge
+    multi-row warp tiles below; against the reference, bit-reproducible, C13 mass."""
+    from oracle import Port
+
+    monkeypatch.setenv("CPG_WARP_TILES", "1")
+    if graph == "chunglu_hubs":
+        off, nb = cpg.gen_chunglu(60000, 900000, 2.1, 30.0, 20000, seed=8)  # rows of every class
+    elif graph == "rmat":
+        off, nb = cpg.gen_rmat(15, 16 << 15, seed=5)
+    else:
+        off, nb = Port.make_graph(3000, 5000, 3)
+    dg = cpg.DeviceGraph.from_host(off, nb, 0)
+    ref = _ref_graph(off, nb)
+    for fam, par, K in ((PPR, 0.2, 26), (HKPR, 5.0, 15)):
+        kern = cpg.Kernel.ppr(par) if fam == PPR else cpg.Kernel.hkpr(par)
+        for s in (0, 1, dg.n // 2, dg.n - 1):
+            est = cpg.cheby_power(dg, kern, s, K)
+            want, _, _ = ref.cheby_power(fam, par, s, K)
+            assert_parity(est.values, want)
+            assert est.stats.mass_err_max <= 1e-9
+    again = cpg.cheby_power(dg, cpg.Kernel.ppr(0.2), 1, 26).values
+    assert np.array_equal(again, cpg.cheby_power(dg, cpg.Kernel.ppr(0.2), 1, 26).values)
+    monkeypatch.setenv("CPG_WARP_TILES", "0")
+    assert np.abs(again - cpg.cheby_power(dg, cpg.Kernel.ppr(0.2), 1, 26).values).max() <= 1e-14
+
+
 def test_large_graph_default_tiles(cpg, gpu):
     """A graph big enough for the large-tile table (>= 4096*148*8 edges)."""
     off, nb = cpg.gen_rmat(18, 16 << 18, seed=12)
