@@ -15,6 +15,7 @@
 // threads on one handle run concurrently.  Sharded handles keep one workspace:
 // their collectives must be issued in the same order on every rank.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost a pointer check unless a tool is attached
 
 #include <algorithm>
 #include <atomic>
@@ -82,6 +83,15 @@ struct StepProf {
     ~StepProf() {
         for (auto e : ev) cudaEventDestroy(e);
     }
+};
+
+// NVTX range for the duration of a scope (calls, queries, steps show up by name in
+// Nsight Systems / ncu --nvtx; near-free without a tool).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 double now_s() {
@@ -445,6 +455,7 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
         CPG_CUDA(cudaMemsetAsync(w->d_wctr, 0, sizeof(unsigned int) * need, st));
     }
     for (uint32_t k = k_first; k <= k_last; ++k) {
+        NvtxRange step_range("cpg.step");
         StepArgs a;
         a.rowptr = g->rowptr;
         a.col = g->col;
@@ -622,6 +633,7 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         launch_init_onehot_batch(w->w_a, g->gdeg, g->new_of_old, w->d_sources, q0, count, B, st);
     ++launches;
     for (uint32_t k = 1; k <= K; ++k) {
+        NvtxRange step_range("cpg.batch_step");
         BatchArgs b;
         b.rowptr = g->rowptr;
         b.col = g->col;
@@ -787,6 +799,9 @@ void ensure_buf(T*& p, size_t& cap, size_t need) {
 int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* sources, const double* seeds_host,
           uint32_t nq, uint32_t tile, int mode, double* out, bool out_on_device, void* user_stream,
           cpg_stats* stats, double gp_a = 0.0, bool pipelined = false) {
+    static const char* const kModeName[] = {"cpg.chebypower", "cpg.chebypower_vec", "cpg.chebypower_batched",
+                                             "cpg.power_method", "cpg.general_gp"};
+    NvtxRange range(kModeName[mode >= 0 && mode <= 4 ? mode : 0]);
     return guarded([&] {
         require(g != nullptr, "null graph handle");
         require(std::isfinite(gp_a), "general_gp: exponent must be finite");
