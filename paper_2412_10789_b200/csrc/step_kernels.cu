@@ -684,6 +684,41 @@ __device__ __forceinline__ BatchJob<B> batch_job(const BatchArgs& a, uint32_t jo
 #ifndef CPG_MASS_MODE
 #define CPG_MASS_MODE -1
 #endif
+// Ordered sum of a hub row's P piece partials (rows of B doubles; this lane's
+// double2 at column pair cl): the loads go out 8 at a time, the adds stay in
+// piece order, so the result is the plain sequential sum -- bit-identical --
+// with P/8 dependent L2 round trips instead of one per piece.
+// UN = loads in flight.  The split path's piece kernel uses 8 (config 5: +0.9%); the
+// fused kernel keeps 1 -- its B = 16 instance spills more with 8 and lost 4% on configs
+// 1-2 (profiles/r02/ab/ab_unroll.txt).  CPG_PARTIAL_UNROLL overrides both (A/B hook).
+template <int B, uint32_t UN_DEFAULT>
+__device__ __forceinline__ double2 sum_partials(const double* hp, uint32_t slot, uint32_t P, int cl) {
+#ifdef CPG_PARTIAL_UNROLL
+    constexpr uint32_t UN = CPG_PARTIAL_UNROLL;
+#else
+    constexpr uint32_t UN = UN_DEFAULT;
+#endif
+    double2 y = make_double2(0.0, 0.0);
+    uint32_t p = 0;
+    for (; p + UN <= P; p += UN) {
+        double2 v[UN];
+#pragma unroll
+        for (uint32_t q = 0; q < UN; ++q)
+            v[q] = __ldcg(reinterpret_cast<const double2*>(hp + static_cast<size_t>(slot + p + q) * B) + cl);
+#pragma unroll
+        for (uint32_t q = 0; q < UN; ++q) {
+            y.x += v[q].x;
+            y.y += v[q].y;
+        }
+    }
+    for (; p < P; ++p) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(hp + static_cast<size_t>(slot + p) * B) + cl);
+        y.x += v.x;
+        y.y += v.y;
+    }
+    return y;
+}
+
 template <int PREF>
 constexpr int mass_mode() {
     return CPG_MASS_MODE >= 0 ? CPG_MASS_MODE : PREF;
@@ -912,13 +947,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             prev = __shfl_sync(0xffffffffu, prev, slot * L);
             if (j.hub && prev == j.P - 1) {
                 __threadfence();
-                y = make_double2(0.0, 0.0);
-                for (uint32_t p = 0; p < j.P; ++p) {
-                    const double2 v =
-                        __ldcg(reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(j.slot + p) * B) + cl);
-                    y.x += v.x;
-                    y.y += v.y;
-                }
+                y = sum_partials<B, 1>(a.hub_partial, j.slot, j.P, cl);
                 if (cl == 0) a.hub_count[j.r] = 0u;
                 batch_prefetch<B>(a, j.r, cl, wp, ac);
                 do_epi = true;
@@ -1132,13 +1161,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
         prev = __shfl_sync(0xffffffffu, prev, slot * L);
         if (live && prev == P - 1) {  // last piece of the row: ordered combine + epilogue
             __threadfence();
-            double2 y = {0.0, 0.0};
-            for (uint32_t p = 0; p < P; ++p) {
-                const double2 v =
-                    __ldcg(reinterpret_cast<const double2*>(a.hub_partial + static_cast<size_t>(sb + p) * B) + cl);
-                y.x += v.x;
-                y.y += v.y;
-            }
+            const double2 y = sum_partials<B, 8>(a.hub_partial, sb, P, cl);
             if (cl == 0) a.hub_count[r] = 0u;
             double2 wp, ac;
             batch_prefetch<B>(a, r, cl, wp, ac);
