@@ -152,6 +152,20 @@ int cpg_graph_create_loopback(const uint64_t* offsets, const uint32_t* neighbors
                               uint64_t nnz, int on_device, int device, int rank,
                               cpg_loopback_group* grp, cpg_graph** out);
 
+/* One handle over n_devices GPUs of THIS process (SURVEY.md 8b's cpg_graph_create
+ * with a device list): the host CSR is row-partitioned across the devices, one
+ * shard handle per device (cpg_graph_create_sharded, the NCCL communicator
+ * created from one host thread per device).  cpg_chebypower / _vec / _batched /
+ * _batched_async / _device, cpg_power_method and cpg_general_gp on it run every
+ * shard's call from its own host thread; rank 0 (devices[0]) writes the output
+ * and stats.  n_devices == 1 gives a plain single-GPU handle.  topk / measure /
+ * trace entries reject it (use them per process on shard handles). */
+int cpg_graph_create_multi(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                           const int* devices, int n_devices, cpg_graph** out);
+/* Test hook: the same facade over n_ranks shards on ONE device with the
+ * loopback data plane (no NCCL; rank r's "all-gather" copies peer slices). */
+int cpg_graph_create_multi_loopback(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                                    int device, int n_ranks, cpg_graph** out);
 /* Host restatement of the device relabel/partition (graph_build.cu): nodes
  * ordered by (degree desc, id asc); with cr = ceil(n / (nranks*chunks)),
  * position i goes to rank = i % nranks, t = i / nranks, chunk = t % chunks,

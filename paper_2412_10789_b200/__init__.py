@@ -301,6 +301,28 @@ class DeviceGraph:
         g._group = group  # the group outlives its handles
         return g
 
+    @classmethod
+    def multi(cls, offsets, neighbors, devices) -> "DeviceGraph":
+        """One handle over several GPUs of this process (cpg_graph_create_multi): the CSR is
+        row-partitioned across ``devices``; queries run every shard from its own host thread."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        _check(L.lib().cpg_graph_create_multi(_u64p(off), _u32p(nbr), len(off) - 1, len(nbr), devs, len(devices),
+                                              ctypes.byref(h)), "cpg_graph_create_multi")
+        return cls(h)
+
+    @classmethod
+    def multi_loopback(cls, offsets, neighbors, n_ranks: int, device: int = 0) -> "DeviceGraph":
+        """Test hook: the multi-device facade over ``n_ranks`` shards on one GPU (loopback plane)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _check(L.lib().cpg_graph_create_multi_loopback(_u64p(off), _u32p(nbr), len(off) - 1, len(nbr), device,
+                                                       n_ranks, ctypes.byref(h)), "cpg_graph_create_multi_loopback")
+        return cls(h)
+
     @property
     def handle(self):
         return self._h

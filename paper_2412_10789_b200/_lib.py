@@ -62,6 +62,8 @@ SIGNATURES = {
     "cpg_graph_create_sharded": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, c_int, c_int,
                                          c_int, c_void_p, POINTER(_G)]),
     "cpg_loopback_group_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "cpg_graph_create_multi": (c_int, [_u64p, _u32p, c_uint32, c_uint64, POINTER(c_int), c_int, POINTER(_G)]),
+    "cpg_graph_create_multi_loopback": (c_int, [_u64p, _u32p, c_uint32, c_uint64, c_int, c_int, POINTER(_G)]),
     "cpg_loopback_group_destroy": (c_int, [c_void_p]),
     "cpg_graph_create_loopback": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_int, c_int, c_int, c_void_p,
                                           POINTER(_G)]),

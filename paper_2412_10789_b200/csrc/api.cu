@@ -20,11 +20,13 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cpg_graph.hpp"
@@ -579,6 +581,8 @@ uint32_t run_single(cpg_graph* g, Workspace* w, uint32_t K, uint32_t q0, uint32_
     if (d_dst) {
         launch_unpermute(d_dst, gather_result(g, w, 1, st), g->n_loc, g->new_of_old, g->n, Q, g->gdeg, gp_a, st);
         ++launches;
+    } else if (g->comm) {
+        gather_result(g, w, 1, st);  // a collective: every rank takes part, with or without an output
     }
     CPG_CUDA(cudaGetLastError());
     return launches;
@@ -735,6 +739,8 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         launch_unpermute_batch(d_dst, gather_result(g, w, cols, st), g->new_of_old, g->n, count, B, g->gdeg, gp_a,
                                st);
         ++launches;
+    } else if (g->comm) {
+        gather_result(g, w, cols, st);  // a collective: every rank takes part, with or without an output
     }
     CPG_CUDA(cudaGetLastError());
     return launches;
@@ -802,6 +808,25 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
     static const char* const kModeName[] = {"cpg.chebypower", "cpg.chebypower_vec", "cpg.chebypower_batched",
                                              "cpg.power_method", "cpg.general_gp"};
     NvtxRange range(kModeName[mode >= 0 && mode <= 4 ? mode : 0]);
+    if (g && !g->members.empty()) {
+        // multi-device handle: every shard runs the same call from its own host thread (the
+        // per-step collectives meet across them); rank 0 writes the caller's output and stats
+        const size_t R = g->members.size();
+        std::vector<int> rc(R, CPG_OK);
+        std::vector<std::string> msg(R);
+        std::vector<std::thread> th;
+        for (size_t r = 0; r < R; ++r)
+            th.emplace_back([&, r] {
+                rc[r] = drive(g->members[r], coeffs, K, sources, seeds_host, nq, tile, mode, r == 0 ? out : nullptr,
+                              out_on_device, r == 0 ? user_stream : nullptr, r == 0 ? stats : nullptr, gp_a,
+                              pipelined);
+                if (rc[r] != CPG_OK) msg[r] = cpg_last_error();
+            });
+        for (auto& t : th) t.join();
+        for (size_t r = 0; r < R; ++r)
+            if (rc[r] != CPG_OK) return guarded([&] { fail(rc[r], "shard " + std::to_string(r) + ": " + msg[r]); });
+        return CPG_OK;
+    }
     return guarded([&] {
         require(g != nullptr, "null graph handle");
         require(std::isfinite(gp_a), "general_gp: exponent must be finite");
@@ -1077,6 +1102,74 @@ int cpg_graph_create_loopback(const uint64_t* offsets, const uint32_t* neighbors
                           [&]() -> Comm* { return make_loopback_comm(lg, rank); }, out);
 }
 
+}  // extern "C"
+
+namespace {
+// A multi-device facade over one shard handle per rank, created from R host threads
+// (the shards' communicator inits meet across them).
+int create_multi(int R, const std::function<int(int, cpg_graph**)>& make_shard, LoopbackGroup* own, cpg_graph** out) {
+    return guarded([&] {
+        std::vector<cpg_graph*> shards(static_cast<size_t>(R), nullptr);
+        std::vector<int> rc(static_cast<size_t>(R), CPG_OK);
+        std::vector<std::string> msg(static_cast<size_t>(R));
+        std::vector<std::thread> th;
+        for (int r = 0; r < R; ++r)
+            th.emplace_back([&, r] {
+                rc[r] = make_shard(r, &shards[r]);
+                if (rc[r] != CPG_OK) msg[r] = cpg_last_error();
+            });
+        for (auto& t : th) t.join();
+        for (int r = 0; r < R; ++r)
+            if (rc[r] != CPG_OK) {
+                for (cpg_graph* s : shards) cpg_graph_destroy(s);
+                if (own) loopback_group_destroy(own);
+                fail(rc[r], "shard " + std::to_string(r) + ": " + msg[r]);
+            }
+        auto g = std::make_unique<cpg_graph>();
+        const cpg_graph* s0 = shards[0];
+        g->device = s0->device;
+        g->rank = 0;
+        g->nranks = R;
+        g->chunks = s0->chunks;
+        g->n = s0->n;
+        g->nnz = s0->nnz;
+        g->n_loc = s0->n;
+        g->nnz_loc = s0->nnz;
+        g->n_pad = s0->n_pad;
+        g->hash = s0->hash;
+        g->max_degree = s0->max_degree;
+        g->members = shards;
+        g->own_group = own;
+        *out = g.release();
+    });
+}
+}  // namespace
+
+extern "C" {
+
+int cpg_graph_create_multi(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                           const int* devices, int n_devices, cpg_graph** out) {
+    if (!devices || n_devices < 1 || n_devices > 64)
+        return guarded([&] { fail(CPG_EINVAL, "multi-device graph: 1..64 devices"); });
+    if (n_devices == 1) return cpg_graph_create(offsets, neighbors, n, nnz, devices[0], 0, out);
+    unsigned char id[128];
+    const int rc = cpg_nccl_unique_id(id);
+    if (rc != CPG_OK) return rc;
+    return create_multi(n_devices, [&](int r, cpg_graph** s) {
+        return cpg_graph_create_sharded(offsets, neighbors, n, nnz, 0, devices[r], r, n_devices, id, s);
+    }, nullptr, out);
+}
+
+int cpg_graph_create_multi_loopback(const uint64_t* offsets, const uint32_t* neighbors, uint32_t n, uint64_t nnz,
+                                    int device, int n_ranks, cpg_graph** out) {
+    if (n_ranks < 1 || n_ranks > 64) return guarded([&] { fail(CPG_EINVAL, "loopback: 1..64 ranks"); });
+    LoopbackGroup* grp = loopback_group_create(n_ranks);
+    return create_multi(n_ranks, [&](int r, cpg_graph** s) {
+        return cpg_graph_create_loopback(offsets, neighbors, n, nnz, 0, device, r,
+                                         reinterpret_cast<cpg_loopback_group*>(grp), s);
+    }, grp, out);
+}
+
 int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info) {
     return guarded([&] {
         require(g && info, "null argument");
@@ -1100,6 +1193,13 @@ int cpg_graph_info_get(const cpg_graph* g, cpg_graph_info* info) {
 
 int cpg_graph_destroy(cpg_graph* g) {
     if (!g) return CPG_OK;
+    if (!g->members.empty()) {  // multi-device facade: its shards, then its loopback group
+        int rc = CPG_OK;
+        for (cpg_graph* s : g->members) rc = std::max(rc, cpg_graph_destroy(s));
+        if (g->own_group) loopback_group_destroy(g->own_group);
+        delete g;
+        return rc;
+    }
     return guarded([&] {
         DeviceGuard dg(g->device);
         cudaDeviceSynchronize();
@@ -1151,6 +1251,11 @@ int cpg_chebypower_batched_async(cpg_graph* g, const double* coeffs, uint32_t K,
 }
 
 int cpg_graph_sync(cpg_graph* g) {
+    if (g && !g->members.empty()) {
+        int rc = CPG_OK;
+        for (cpg_graph* s : g->members) rc = std::max(rc, cpg_graph_sync(s));
+        return rc;
+    }
     return guarded([&] {
         require(g != nullptr, "null graph handle");
         DeviceGuard dg(g->device);
@@ -1198,6 +1303,7 @@ int cpg_chebypower_topk(cpg_graph* g, const double* coeffs, uint32_t K, const ui
                         uint32_t k, uint32_t* ids, double* vals, cpg_stats* stats) {
     return guarded([&] {
         check_query(g, coeffs, K, sources, n_sources);
+        require(g->members.empty(), "topk: not supported on a multi-device handle (use one shard per process)");
         require(k >= 1 && ids && vals, "topk: k >= 1 and output arrays required");
         const uint32_t kk = std::min(k, g->n);
         DeviceGuard dg(g->device);
@@ -1241,6 +1347,7 @@ int cpg_measure(cpg_graph* g, const double* truth, const double* estimate, uint3
                 cpg_error_report* reports) {
     return guarded([&] {
         require(g && truth && estimate && (reports || n_cols == 0), "null argument");
+        require(g->members.empty(), "measure: not supported on a multi-device handle");
         if (!n_cols) return;
         DeviceGuard dg(g->device);
         WsLease lease(g);
@@ -1277,6 +1384,7 @@ int cpg_chebypower_measure(cpg_graph* g, const double* coeffs, uint32_t K, const
                            cpg_error_report* reports, cpg_stats* stats) {
     return guarded([&] {
         check_query(g, coeffs, K, sources, n_sources);
+        require(g->members.empty(), "measure: not supported on a multi-device handle");
         require(truths && reports, "null argument");
         DeviceGuard dg(g->device);
         const size_t n = g->n;
@@ -1358,7 +1466,7 @@ int trace_impl(cpg_graph* g, const double* coeffs, uint32_t K, uint32_t source, 
         } else {
             check_query(g, coeffs, K, &source, 1);
         }
-        require(g->nranks == 1, "trace is single-GPU only");
+        require(g->nranks == 1 && g->members.empty(), "trace is single-GPU only");
         DeviceGuard dg(g->device);
         WsLease lease(g);
         Workspace* w = lease.w;
@@ -1424,6 +1532,7 @@ int cpg_chebypower_vec_trace(cpg_graph* g, const double* coeffs, uint32_t K, con
 
 double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile) {
     if (!g) return 0.0;
+    if (!g->members.empty()) return cpg_bytes_per_step(g->members[0], tile);  // per rank
     // 4 B index + 8*B B gathered row per edge, 8 B row pointer
     // per row, 4 streams of 8*B B per row (read w_{k-1}, write w_{k+1}, read+write
     // acc); sharded adds the received all-gather bytes 8*B*n*(R-1)/R.

@@ -144,6 +144,8 @@ struct cpg_graph {
     std::mutex ws_mu;
     std::condition_variable ws_cv;
 
+    std::vector<cpg_graph*> members;  // multi-device facade (cpg_graph_create_multi): one shard per rank
+    cpg::LoopbackGroup* own_group = nullptr;  // facade over loopback shards: the group it owns
     cpg::Comm* comm = nullptr;      // data plane when sharded (NCCL or test loopback), else null
     bool p2p = false;               // fused all-gather through NCCL symmetric windows
     int p2p_self = 0;               // test hook: also store through this rank's own LSA alias

@@ -135,3 +135,34 @@ def test_pipelined_slot_layout_change(cpg, graph):
     cpg.sync(dg)
     assert np.array_equal(out4, want4)
     assert np.array_equal(pinned[1], want16)
+
+
+@pytest.mark.parametrize("R", [1, 3])
+def test_multi_device_facade(cpg, graph, R):
+    """cpg_graph_create_multi's facade (one handle over a device list): one
+    host call fans out to every shard's thread; rank 0's output equals the reference.  On
+    one GPU the shards use the loopback plane; a one-device list is a plain handle."""
+    from oracle import Port, RefGraph
+
+    off, nb = graph
+    n = len(off) - 1
+    dg = cpg.DeviceGraph.multi_loopback(off, nb, R) if R > 1 else cpg.DeviceGraph.multi(off, nb, [0])
+    assert dg.info.nranks == R and dg.info.n == n
+    ref = RefGraph.from_csr(off, nb)
+    k = cpg.Kernel.ppr(0.2)
+    src = [0, 9, n // 3, n - 1]
+    single, st = cpg.cheby_power_many(dg, k, src, 26)
+    batched, bst = cpg.cheby_power_many(dg, k, src, 26, batched=True, tile=4)
+    for j, s in enumerate(src):
+        want, _, _ = ref.cheby_power(PPR, 0.2, s, 26)
+        assert_parity(single[j], want)
+        assert_parity(batched[j], want)
+    assert st.mass_err_max <= 1e-9 and bst.mass_err_max <= 1e-9
+    x = Port.random_vector(n, 3, 0.0, 1.0)
+    got = cpg.cheby_power_vec(dg, cpg.Kernel.hkpr(5.0), x, 15).values
+    want = ref.cheby_power_vec(HKPR, 5.0, x, 15)
+    assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+    if R > 1:
+        with pytest.raises(cpg.ParameterError):
+            cpg.cheby_power_topk(dg, k, src, 26, k=5)
+    dg.close()
