@@ -423,6 +423,17 @@ def main():
     run_ours(args, cfg)
 
 
+def sparse_steps_used(batched, sharded, K):
+    """Steps of each query that gather only the nonzero rows of w_{k-1} (DESIGN.md 4.7;
+    the library's rule in api.cu sparse_steps: 3 single-source, 2 batched, 1 sharded)."""
+    m = 2 if batched else 3
+    if "CPG_SPARSE_STEPS" in os.environ:
+        m = max(0, int(os.environ["CPG_SPARSE_STEPS"]))
+    if sharded:
+        m = min(m, 1)
+    return min(m, K)
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -516,6 +527,11 @@ def run_ours(args, cfg):
     gteps = K * nnz * queries / (ms / 1e3) / 1e9
 
     # ---- roofline: per-launch step-kernel time (events bracket each launch) ----------------
+    # The roofline characterises the full step kernel: the sparse early steps (DESIGN.md
+    # 4.7, which gather only the nonzero rows of w_{k-1}) are switched off for this call,
+    # so every timed launch is a full-support step.  `value` keeps them on.
+    sparse_env = os.environ.get("CPG_SPARSE_STEPS")
+    os.environ["CPG_SPARSE_STEPS"] = "0"
     L.cpg_set_profiling(1)
     s = P._lib.cpg_stats()
     if batched:
@@ -524,6 +540,10 @@ def run_ours(args, cfg):
     else:
         P._check(L.cpg_chebypower(dg.handle, P._f64p(c_np), K, P._u32p(src_np), len(src_np), None, ctypes.byref(s)))
     L.cpg_set_profiling(0)
+    if sparse_env is None:
+        del os.environ["CPG_SPARSE_STEPS"]
+    else:
+        os.environ["CPG_SPARSE_STEPS"] = sparse_env
     launches_per_step = int(s.launches)  # kernels the library launched for one step (its own count)
     # one timed launch = one step of a source tile (batched) or of a query group (single-source:
     # several queries per launch on small graphs), so scale the per-step bytes by the steps it ran
@@ -626,8 +646,9 @@ def run_ours(args, cfg):
                        "allgather": (("fused NVLink stores" if dg.info.fused_allgather else
                                       f"NCCL, {dg.info.chunks} chunks overlapped")
                                      if world > 1 or args.sharded else None),
-                       "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                       "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)",
+                       "sparse_early_steps": sparse_steps_used(batched, world > 1 or args.sharded, K)},
+            "roofline": {"bound": "hbm", "timed": "every step full-support (sparse early steps off for this call)", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "basis": basis,
                          "frac_model": achieved_model / peak, "achieved_model": achieved_model,
                          # the committed ncu capture is of the one-GPU step; a rank's share differs

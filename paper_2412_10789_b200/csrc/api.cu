@@ -22,6 +22,7 @@
 #include <chrono>
 #include <functional>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -83,6 +84,17 @@ struct StepProf {
         return t;
     }
     ~StepProf() {
+        // CPG_PROF_DUMP=1 (diagnostics): each bracketed step's milliseconds on stderr
+        if (const char* d = std::getenv("CPG_PROF_DUMP"); d && d[0] == '1' && ev.size() >= 2) {
+            std::fprintf(stderr, "[cpg prof] step ms:");
+            for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+                float ms = 0.f;
+                cudaEventSynchronize(ev[i + 1]);
+                cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+                std::fprintf(stderr, " %.3f", ms);
+            }
+            std::fprintf(stderr, "\n");
+        }
         for (auto e : ev) cudaEventDestroy(e);
     }
 };
@@ -159,7 +171,7 @@ void ws_destroy(cpg_graph* g, Workspace* w) {
                     (void*)w->bhub_count, (void*)w->d_job_ctr, (void*)w->d_wctr, (void*)w->d_coeffs, (void*)w->d_sources,
                     (void*)w->d_mass_partial, (void*)w->d_step_mass, (void*)w->d_mass0, (void*)w->d_seeds,
                     (void*)w->d_stage, (void*)w->d_topk, (void*)w->d_peers_a, (void*)w->d_peers_b,
-                    (void*)w->d_barrier})
+                    (void*)w->d_barrier, (void*)w->d_nz})
         if (p) cudaFree(p);
     if (w->d_mass_err) cudaFreeHost(w->d_mass_err);
     for (auto e : w->ev)
@@ -341,6 +353,36 @@ void ensure_group(cpg_graph* g, Workspace* w, uint32_t K, uint32_t Q) {
     ensure_mass(w, static_cast<size_t>(K) * g->chunks * mass_cols(g, Q) * Q, static_cast<size_t>(K) * Q);
 }
 
+// Sparse early steps: the first M steps of a one-hot query gather
+// only rows of w_{k-1} whose support bit is set (the reference's scatter skips
+// zero entries the same way, graph.cpp:262).  Step k reads bitmap k-1 and, for
+// k < M, builds bitmap k in its epilogue; the init kernel sets bitmap 0 (the
+// sources).  Results are bit-identical to the unmasked steps.  A sharded rank
+// builds only its own rows' bits, so there only step 1 (the sources' bitmap,
+// known to every rank) is masked; the fused all-gather path is never masked.
+// Defaults: 3 steps for one source (its 1- and 2-hop balls stay small), 2 for a
+// batched tile; CPG_SPARSE_STEPS=M overrides (0 = off).
+uint32_t sparse_steps(const cpg_graph* g, bool single, uint32_t K) {
+    if (g->p2p) return 0;
+    uint32_t M = single ? 3 : 2;
+    if (const char* e = std::getenv("CPG_SPARSE_STEPS")) M = static_cast<uint32_t>(std::max(0, std::atoi(e)));
+    if (g->comm) M = std::min<uint32_t>(M, 1);
+    return std::min(M, K);
+}
+
+// M zeroed bitmaps (stream-ordered), or null for M = 0.
+uint32_t* ensure_nz(cpg_graph* g, Workspace* w, uint32_t M, cudaStream_t st) {
+    if (!M) return nullptr;
+    const size_t need = static_cast<size_t>(M) * nz_words(g->n_pad);
+    if (w->nz_cap < need) {
+        dfree(w->d_nz);
+        w->d_nz = dalloc<uint32_t>(need);
+        w->nz_cap = need;
+    }
+    CPG_CUDA(cudaMemsetAsync(w->d_nz, 0, sizeof(uint32_t) * need, st));
+    return w->d_nz;
+}
+
 void ensure_params(Workspace* w, uint32_t K, uint32_t n_sources) {
     if (w->coeff_cap < K + 1) {
         dfree(w->d_coeffs);
@@ -437,7 +479,8 @@ bool step_split(const cpg_graph* g) {
 
 // The K fused steps of one query (group), chunk by chunk (last = write d*acc).
 uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last, uint32_t K, bool last_writes_out,
-                   cudaStream_t st, StepProf* prof, bool taylor = false, uint32_t Q = 1) {
+                   cudaStream_t st, StepProf* prof, bool taylor = false, uint32_t Q = 1, uint32_t M = 0,
+                   uint32_t* nz = nullptr) {
     uint32_t launches = 0;
     const int occ = std::max(1, step_occupancy(g->tile));
     const uint32_t C = static_cast<uint32_t>(g->chunks);
@@ -474,6 +517,9 @@ uint32_t run_steps(cpg_graph* g, Workspace* w, uint32_t k_first, uint32_t k_last
         a.first = k == 1;
         a.taylor = taylor;
         a.last = last_writes_out && k == K;
+        const size_t nzw = nz_words(g->n_pad);
+        a.nz_in = nz && k <= M ? nz + (k - 1) * nzw : nullptr;  // masked (sparse early) step
+        a.nz_out = nz && k < M ? nz + k * nzw : nullptr;
 #if CPG_CHECKED
         a.chk_nnz = g->nnz_loc;
         a.chk_npad = g->n_pad;
@@ -567,12 +613,14 @@ uint32_t run_single(cpg_graph* g, Workspace* w, uint32_t K, uint32_t q0, uint32_
     const size_t mstride = static_cast<size_t>(K) * C * mass_cols(g, Q);
     CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * g->n_pad * Q, st));
     CPG_CUDA(cudaMemsetAsync(w->d_mass_partial, 0, sizeof(double) * mstride * Q, st));
+    const uint32_t M = !seed_dev && Q == 1 && !warp_tiles(g) ? sparse_steps(g, true, K) : 0;
+    uint32_t* nz = ensure_nz(g, w, M, st);
     if (seed_dev)
         launch_init_dense(w->w_a, g->gdeg, g->new_of_old, seed_dev, g->n, gp_a, st);
     else
-        launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, q0, Q, st);
+        launch_init_onehot(w->w_a, g->n_pad, g->gdeg, g->new_of_old, w->d_sources, q0, Q, st, nz);
     ++launches;
-    launches += run_steps(g, w, 1, K, K, true, st, prof, taylor, Q);
+    launches += run_steps(g, w, 1, K, K, true, st, prof, taylor, Q, M, nz);
     launch_mass_steps(w->d_mass_partial, C * mass_cols(g, Q), mstride, K, Q, w->d_step_mass, st);
     ++launches;
     if (g->comm) g->comm->allreduce_sum(w->d_step_mass, static_cast<size_t>(K) * Q, st);
@@ -631,10 +679,25 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         }
         CPG_CUDA(cudaMemsetAsync(w->d_job_ctr, 0, sizeof(unsigned int) * need, st));
     }
+    const uint32_t M = seeds_dev ? 0 : sparse_steps(g, false, K);
+    // bitmaps [0, M): supports of w_0 .. w_{M-1}; [M, 2M): rows done by each sparse step's scan;
+    // then the coarse bitmap of the current sparse step's input (coarse_words words)
+    const int cshift = coarse_shift(g->n_pad);
+    const uint32_t cwords = coarse_words(g->n_pad, cshift);
+    const size_t nzw = nz_words(g->n_pad);
+    uint32_t* nz = ensure_nz(g, w, 2 * M + (M ? (cwords + nzw - 1) / nzw : 0), st);
+    uint32_t* coarse = nz ? nz + 2 * M * nzw : nullptr;
+    const int64_t hb = split ? batch_piece_edges(static_cast<int>(B)) : batch_hub_edges(static_cast<int>(B));
+    const bool sparse_kern = [] {  // CPG_SPARSE_KERNEL=0: masked full-step kernels instead (A/B; read per call)
+        const char* e = std::getenv("CPG_SPARSE_KERNEL");
+        return !e || e[0] != '0';
+    }();
+    // a sparse step writes fewer mass rows than a full one: the rows it leaves are zero
+    if (M) CPG_CUDA(cudaMemsetAsync(w->d_mass_partial, 0, sizeof(double) * K * step_rows * B, st));
     if (seeds_dev)
         launch_init_dense_batch(w->w_a, g->gdeg, g->new_of_old, seeds_dev, g->n, count, B, gp_a, st);
     else
-        launch_init_onehot_batch(w->w_a, g->gdeg, g->new_of_old, w->d_sources, q0, count, B, st);
+        launch_init_onehot_batch(w->w_a, g->gdeg, g->new_of_old, w->d_sources, q0, count, B, st, nz);
     ++launches;
     for (uint32_t k = 1; k <= K; ++k) {
         NvtxRange step_range("cpg.batch_step");
@@ -653,6 +716,8 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         b.first = k == 1;
         b.last = k == K;
         b.job_ctr = nullptr;
+        b.nz_in = nz && k <= M ? nz + (k - 1) * nzw : nullptr;  // masked (sparse early) step
+        b.nz_out = nz && k < M ? nz + k * nzw : nullptr;
 #if CPG_CHECKED
         b.chk_nnz = g->nnz_loc;
         b.chk_npad = g->n_pad;
@@ -677,7 +742,30 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
-            if (split) {
+            if (sparse_kern && b.nz_in) {  // sparse early step: edge scan + fill
+                b.mass_partial = mp_step + rows * B;
+#if CPG_CHECKED
+                b.chk_mass = step_rows - rows;
+#endif
+                if (prof) prof->before(st);
+                // rows that can change with y = 0: those with w_{k-2} != 0 (first step: w_0 != 0, the
+                // rest pre-zeroed below); every row on the last step (it writes d * acc)
+                const uint32_t* fill_mask = b.last ? nullptr : (k == 1 ? b.nz_in : nz + (k - 2) * nzw);
+                if (c == 0 && k == 1 && !b.last) {  // w_1 and acc start at zero off the sources' rows
+                    CPG_CUDA(cudaMemsetAsync(b.w_io, 0, sizeof(double) * g->n_pad * cols, st));
+                    CPG_CUDA(cudaMemsetAsync(w->acc, 0, sizeof(double) * g->n_loc * cols, st));
+                }
+                if (k == 1 && !b.last && !g->comm && C == 1) {  // one-term sums: push from the sources (exact)
+                    rows += W * launch_first_push(b, g->gdeg, g->new_of_old, w->d_sources, q0, count,
+                                                  static_cast<uint32_t>(B), 2 * g->sm_count, st);
+                } else {
+                    if (c == 0) launch_coarsen(b.nz_in, nzw, coarse, cwords, cshift, st);
+                    rows += W * launch_sparse_step(b, static_cast<int>(B), nz + (M + k - 1) * nzw, fill_mask, coarse,
+                                                   cwords, cshift, t.row_begin, hb, occ * g->sm_count, st);
+                }
+                if (prof) prof->after(st);
+                launches += 2;
+            } else if (split) {
                 // hub pieces (fused kernel with no plain rows), then the plain rows
                 if (prof) prof->before(st);
                 if (t.n_hub_items) {
@@ -721,8 +809,8 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
             if (!g->p2p) gather_chunk(g, w, b.w_io, c, cols, st);
         }
         if (rows > step_rows) fail(CPG_ECUDA, "batched mass partials overflow");
-        if (k > 1 && rows != used) fail(CPG_ECUDA, "batched launches differ between steps");
-        used = rows;
+        if (k > 1 && rows != used && !M) fail(CPG_ECUDA, "batched launches differ between steps");
+        used = std::max(used, rows);
         // iteration barrier: every rank's rows of w_k are in every replica before step k+1
         if (g->p2p) g->comm->allreduce_sum(w->d_barrier, 1, st);
     }

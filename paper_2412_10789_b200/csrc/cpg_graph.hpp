@@ -99,6 +99,8 @@ struct Workspace {
     size_t stage_slot = 0;              // doubles per slot of the last call (slot layout)
     double* d_topk = nullptr;           // device-ranked queries: [Q][n] results
     size_t topk_cap = 0;
+    uint32_t* d_nz = nullptr;           // support bitmaps of w_0 .. w_{M-1} (sparse early steps), nz_words(n_pad) each
+    size_t nz_cap = 0;                  // words
 
     // Fused all-gather (CPG_P2P=1 on a sharded graph): w_a / w_b are NCCL
     // symmetric windows and the batched epilogue stores each computed row into
@@ -179,12 +181,28 @@ int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const Pee
 int batch_occupancy();
 bool batch_split(uint64_t nnz_loc);
 int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
+// Sparse early batched step (scan + fill kernels); returns the mass rows in CTAs.
+int launch_sparse_step(const BatchArgs& a, int B, uint32_t* done, const uint32_t* fill_mask, const uint32_t* coarse,
+                       uint32_t coarse_words, int cshift, uint32_t row_begin, int64_t hb, int grid, cudaStream_t st);
+int launch_first_push(const BatchArgs& a, const uint32_t* gdeg, const uint32_t* new_of_old, const uint32_t* sources,
+                      uint32_t q0, uint32_t count, uint32_t B, int grid, cudaStream_t st);
+void launch_coarsen(const uint32_t* fine, uint64_t fine_words, uint32_t* coarse, uint32_t coarse_words, int cshift,
+                    cudaStream_t st);
+// Coarse-bitmap geometry for n_pad rows: rows per bit = 1 << cshift (>= 64), at most 8192 words (32 KB).
+inline int coarse_shift(uint64_t n_pad) {
+    int s = 6;
+    while ((n_pad >> s) > 8192ull * 32) ++s;
+    return s;
+}
+inline uint32_t coarse_words(uint64_t n_pad, int cshift) {
+    return static_cast<uint32_t>((((n_pad + (1ull << cshift) - 1) >> cshift) + 31) / 32);
+}
 int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa = nullptr);
 
 void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                        uint32_t q0, uint32_t count, cudaStream_t st);
+                        uint32_t q0, uint32_t count, cudaStream_t st, uint32_t* nz0 = nullptr);
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st);
+                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st, uint32_t* nz0 = nullptr);
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
                        uint32_t n, double a, cudaStream_t st);
 void launch_init_dense_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const double* X, uint32_t n,

@@ -120,6 +120,8 @@ struct StepArgs {
     int first;             // k == 1: w_k = D^-1 A w_0, acc = c0 w0 + c1 w1
     int taylor;            // power method (PwMethod, solvers.cpp:87-116): w_k = D^-1 A w_{k-1}
     int last;              // write out = d * acc instead of acc
+    const uint32_t* nz_in; // MASK instances: support bitmap of w_cur (bit u = row u may be nonzero)
+    uint32_t* nz_out;      // MASK instances: support bitmap of w_{k+1} to build (pre-zeroed), or null
     CPG_CHK_FIELDS         // CPG_CHECKED builds only: nnz_loc, n_pad, n_loc, hub partial slots, mass slots
 };
 
@@ -154,8 +156,24 @@ struct BatchArgs {
     int k, first, last;
     unsigned int* job_ctr;      // fused kernel: zeroed job counter (warps claim RPW jobs each); null = static stride
     double* mass_partial;       // [gridDim.x * warps][B] per-warp column sums of d_v w_{k+1}(v) (acceptance C13); null = off
+    const uint32_t* nz_in;      // MASK instances: support bitmap of w_cur's rows (any column nonzero)
+    uint32_t* nz_out;           // MASK instances: support bitmap of w_{k+1}'s rows to build (pre-zeroed), or null
     CPG_CHK_FIELDS              // CPG_CHECKED builds only (partial / mass bounds in rows of B doubles)
 };
+
+// Support bitmaps (sparse early steps).  The reference's scatter
+// skips every source entry that is exactly zero (graph.cpp:262: `if (xu == 0.0)
+// continue;`); the pull step does the same with one bit per row of the iterate:
+// a gather of row u is issued only if bit u is set, and a row whose bit is clear
+// holds exact zeros, so skipping its add leaves every sum bit-identical.  Bit u of
+// nz is set if row u of the iterate may be nonzero (a superset is always exact).
+#ifdef __CUDACC__
+__device__ __forceinline__ bool nz_bit(const uint32_t* nz, uint32_t u) {
+    return (__ldg(nz + (u >> 5)) >> (u & 31)) & 1u;
+}
+__device__ __forceinline__ void nz_set(uint32_t* nz, uint32_t u) { atomicOr(nz + (u >> 5), 1u << (u & 31)); }
+#endif
+__host__ __device__ inline uint64_t nz_words(uint64_t n_pad) { return (n_pad + 31) / 32; }
 
 // Fused all-gather (second parameter of the PEER instances of the batched
 // kernels): w_io's row also goes to peer_io[p] for p in [0, n_peer), p != self.

@@ -201,6 +201,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // Recurrence + accumulation + mass for local row r with neighbour sum y.
 // w_prev = w_{k-1}(v) (for the first step: w_0(v)), acc_old = acc(v) (unused
 // in the first step).
+template <bool MASK = false>
 __device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, double y, int64_t d, double w_prev,
                                               double acc_old, double& mass) {
     const uint32_t gr = a.row0 + r;
@@ -220,6 +221,7 @@ __device__ __forceinline__ void step_epilogue(const StepArgs& a, uint32_t r, dou
         mass += dd * w_new;
     }
     CPG_CHECK(gr < a.chk_npad && r < a.chk_nloc, "step epilogue row", gr, a.chk_npad);
+    if (MASK && a.nz_out && w_new != 0.0) nz_set(a.nz_out, gr);  // support of w_{k+1} for the next masked step
     a.w_io[gr] = w_new;
     if (a.last)
         a.out[r] = static_cast<double>(d) * acc_new;
@@ -249,7 +251,7 @@ struct TileSmem {
 // stream, the epilogue operands of the rows this thread finalises), then the
 // gathers; one barrier; lane-group row sums from shared memory; one barrier;
 // the fused epilogue with thread t owning rows t and t + 256.
-template <int THREADS, int TILE, bool PDL>
+template <int THREADS, int TILE, bool PDL, bool MASK = false>
 __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem it, TileSmem<TILE>& sm,
                                              double& mass, bool& wait_pending) {
     constexpr int PER = TILE / THREADS;
@@ -280,7 +282,19 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
         const int r = q * THREADS + threadIdx.x;
         if (r < nrows) load_prev(a, rb + r, w_prev[q], acc_old[q]);
     }
-    if (a.hot_rows) {
+    if constexpr (MASK) {  // masked (sparse early) step: every support word first, then the set rows
+        uint32_t wd[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = i * THREADS + threadIdx.x;
+            wd[i] = j < cnt ? __ldg(a.nz_in + (idx[i] >> 5)) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = i * THREADS + threadIdx.x;
+            if (j < cnt) sm.vals[j] = (wd[i] >> (idx[i] & 31)) & 1u ? ld_gather(a.w_cur + idx[i]) : 0.0;
+        }
+    } else if (a.hot_rows) {
         const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -317,12 +331,12 @@ __device__ __forceinline__ void process_tile(const StepArgs& a, const WorkItem i
     for (int q = 0; q < RPT; ++q) {
         const int r = q * THREADS + threadIdx.x;
         if (r < nrows)
-            step_epilogue(a, rb + r, sm.ysum[r], sm.rp[r + 1] - sm.rp[r], w_prev[q], acc_old[q], mass);
+            step_epilogue<MASK>(a, rb + r, sm.ysum[r], sm.rp[r + 1] - sm.rp[r], w_prev[q], acc_old[q], mass);
     }
     __syncthreads();  // shared memory is reused by the next item
 }
 
-template <int THREADS, bool PDL>
+template <int THREADS, bool PDL, bool MASK = false>
 __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it, double* red,
                                             int* flag, double& mass, bool& wait_pending) {
     constexpr int PER = kHubPieceEdges / THREADS;
@@ -350,7 +364,19 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
         const int64_t e = p0 + i * THREADS + threadIdx.x;
         CPG_CHECK(e >= p1 || (idx[i] < a.chk_npad && static_cast<uint64_t>(e) < a.chk_nnz), "hub gather", idx[i],
                   a.chk_npad);
-        vals[i] = e < p1 ? ld_gather(a.w_cur + idx[i]) : 0.0;
+        if constexpr (MASK) {
+            vals[i] = 0.0;
+        } else {
+            vals[i] = e < p1 ? ld_gather(a.w_cur + idx[i]) : 0.0;
+        }
+    }
+    if constexpr (MASK) {  // support words first, then the set rows (see process_tile)
+        uint32_t wd[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) wd[i] = p0 + i * THREADS + threadIdx.x < p1 ? __ldg(a.nz_in + (idx[i] >> 5)) : 0u;
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if ((wd[i] >> (idx[i] & 31)) & 1u) vals[i] = ld_gather(a.w_cur + idx[i]);
     }
     double s = 0.0;
 #pragma unroll
@@ -361,7 +387,7 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
         if (threadIdx.x == 0) {
             double wp, ao;
             load_prev(a, r, wp, ao);
-            step_epilogue(a, r, s, d, wp, ao, mass);
+            step_epilogue<MASK>(a, r, s, d, wp, ao, mass);
         }
         return;
     }
@@ -383,13 +409,13 @@ __device__ __forceinline__ void process_hub(const StepArgs& a, const WorkItem it
             a.hub_count[hub] = 0u;  // re-arm for the next step
             double wp, ao;
             load_prev(a, r, wp, ao);
-            step_epilogue(a, r, y, d, wp, ao, mass);
+            step_epilogue<MASK>(a, r, y, d, wp, ao, mass);
         }
     }
     __syncthreads();
 }
 
-template <int THREADS, int TILE>
+template <int THREADS, int TILE, bool MASK = false>
 __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
     __shared__ TileSmem<TILE> sm;
     __shared__ double red[THREADS / 32];
@@ -404,9 +430,9 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
         if (it.c & kHubBit)
-            process_hub<THREADS, true>(a, it, red, &flag, mass, wait_pending);
+            process_hub<THREADS, true, MASK>(a, it, red, &flag, mass, wait_pending);
         else
-            process_tile<THREADS, TILE, true>(a, it, sm, mass, wait_pending);
+            process_tile<THREADS, TILE, true, MASK>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
@@ -418,7 +444,7 @@ __global__ void __launch_bounds__(THREADS) cheby_step_kernel(const StepArgs a) {
 // tile kernel drops the hub path's registers and fits more CTAs per SM.  Each
 // writes its own CTAs' mass partials (the tile kernel's start after the hub
 // kernel's grid).
-template <int THREADS>
+template <int THREADS, bool MASK = false>
 __global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs a) {
     __shared__ double red[THREADS / 32];
     __shared__ int flag;
@@ -430,14 +456,14 @@ __global__ void __launch_bounds__(THREADS) cheby_step_hubs_kernel(const StepArgs
         it.a = raw.x;
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        process_hub<THREADS, false>(a, it, red, &flag, mass, wait_pending);
+        process_hub<THREADS, false, MASK>(a, it, red, &flag, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
     if (threadIdx.x == 0) a.mass_partial[blockIdx.x] = mass;
 }
 
-template <int THREADS, int TILE, int MINB>
+template <int THREADS, int TILE, int MINB, bool MASK = false>
 __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const StepArgs a) {
     __shared__ TileSmem<TILE> sm;
     __shared__ double red[THREADS / 32];
@@ -449,7 +475,7 @@ __global__ void __launch_bounds__(THREADS, MINB) cheby_step_tiles_kernel(const S
         it.a = raw.x;
         it.b = raw.y;
         it.c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
-        process_tile<THREADS, TILE, false>(a, it, sm, mass, wait_pending);
+        process_tile<THREADS, TILE, false, MASK>(a, it, sm, mass, wait_pending);
     }
     mass = block_sum<THREADS>(mass, red);
     CPG_CHECK(threadIdx.x != 0 || blockIdx.x < a.chk_mass, "step mass slot", blockIdx.x, a.chk_mass);
@@ -792,7 +818,34 @@ __device__ __forceinline__ void batch_mass_flush(const BatchArgs& a, double2 msu
     }
 }
 
-template <int B, bool PEER, int MM>
+// U row gathers of a masked (sparse early) step: the U edges' support words
+// are loaded together first (one L2 round trip for all U), then only the rows
+// whose bit is set are gathered -- testing and gathering edge by edge would
+// chain U dependent round trips.
+template <int B, int U>
+__device__ __forceinline__ void gather_rows_masked(const BatchArgs& a, const uint32_t* c, int t0, int m, int slot,
+                                                   int cl, double2* val, uint64_t pol_last, uint64_t pol_first) {
+    constexpr int L = B / 2;
+    uint32_t uq[U], wd[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int t = t0 + q;
+        uq[q] = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+        CPG_CHECK(t >= m || uq[q] < a.chk_npad, "batch gather", uq[q], a.chk_npad);
+        wd[q] = t < m ? __ldg(a.nz_in + (uq[q] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const uint32_t u = uq[q];
+        val[q] = (wd[q] >> (u & 31)) & 1u
+                     ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl, u < a.hot_rows,
+                                                    pol_last, pol_first)
+                                   : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                     : make_double2(0.0, 0.0);
+    }
+}
+
+template <int B, bool PEER, int MM, bool MASK = false>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArgs& pa, uint32_t r, double2 y,
                                                int64_t d, int cl, double2 wp, double2 ac, double2& msum) {
     const uint32_t gr = a.row0 + r;
@@ -815,6 +868,8 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs& a, const PeerArg
         // sum_v d_v w_{k+1}(v) = sum_v T_{k+1}(v), per column
         batch_mass_add<B, MM>(msum, dd * w_new.x, dd * w_new.y);
     }
+    // support of w_{k+1} for the next masked step (any column of the row nonzero)
+    if (MASK && a.nz_out && (w_new.x != 0.0 || w_new.y != 0.0)) nz_set(a.nz_out, gr);
     st_stream2(a.w_io + static_cast<size_t>(gr) * B + 2 * cl, w_new);
     if (PEER) {  // fused all-gather: the row into every other rank's replica (NVLink stores)
         for (int p = 0; p < pa.n_peer; ++p)
@@ -849,7 +904,7 @@ __device__ __forceinline__ void batch_prefetch(const BatchArgs& a, uint32_t r, i
 
 // Occupancy over registers: 4 CTAs x 8 warps per SM (64 regs) measured best
 // for B = 16 and 64 (profiles/r01/slot_sweep.txt), even with small spills.
-template <int B, int U = 8, int MINB = 4, bool PEER = false>
+template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false>
 __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;      // lanes per row slot
     constexpr int RPW = 32 / L;   // row slots per warp
@@ -915,15 +970,19 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             for (int t0 = 0; t0 < 32; t0 += U) {
                 if (!__any_sync(0xffffffffu, t0 < m)) break;
                 double2 val[U];
+                if constexpr (MASK) {
+                    gather_rows_masked<B, U>(a, c, t0, m, slot, cl, val, pol_last, pol_first);
+                } else {
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int t = t0 + q;
-                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
-                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                  u < a.hot_rows, pol_last, pol_first)
-                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                   : make_double2(0.0, 0.0);
+                    for (int q = 0; q < U; ++q) {
+                        const int t = t0 + q;
+                        const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                        CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
+                        val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                      u < a.hot_rows, pol_last, pol_first)
+                                                     : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                       : make_double2(0.0, 0.0);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
@@ -954,7 +1013,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
             }
         }
         (void)smask;
-        if (do_epi) batch_epilogue<B, PEER, MM>(a, pa, j.r, y, j.d, cl, wp, ac, msum);
+        if (do_epi) batch_epilogue<B, PEER, MM, MASK>(a, pa, j.r, y, j.d, cl, wp, ac, msum);
         if (!ctr) {
             base_job += nw * RPW;
         } else if (base_job + RPW < claim_end) {
@@ -972,7 +1031,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 // in cheby_batch_kernel first).  Without the hub path the kernel fits more
 // warps, and the next row's range and first index chunk are prefetched while
 // the current row's gathers and epilogue are in flight.
-template <int B, int U = 8, int MINB = 4, bool PEER = false>
+template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false>
 __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;     // lanes per row slot
     constexpr int RPW = 32 / L;  // row slots per warp
@@ -1033,15 +1092,19 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
             for (int t0 = 0; t0 < 32; t0 += U) {
                 if (!__any_sync(0xffffffffu, t0 < m)) break;
                 double2 val[U];
+                if constexpr (MASK) {
+                    gather_rows_masked<B, U>(a, c, t0, m, slot, cl, val, pol_last, pol_first);
+                } else {
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int t = t0 + q;
-                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
-                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                  u < a.hot_rows, pol_last, pol_first)
-                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                   : make_double2(0.0, 0.0);
+                    for (int q = 0; q < U; ++q) {
+                        const int t = t0 + q;
+                        const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                        CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
+                        val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                      u < a.hot_rows, pol_last, pol_first)
+                                                     : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                       : make_double2(0.0, 0.0);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
@@ -1051,7 +1114,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
             }
         }
         load_chunk(ne0, ne1);  // next row's first chunk, overlapping this epilogue
-        if (r < r_end) batch_epilogue<B, PEER, MM>(a, pa, r, s, e1 - e0, cl, wp, ac, msum);
+        if (r < r_end) batch_epilogue<B, PEER, MM, MASK>(a, pa, r, s, e1 - e0, cl, wp, ac, msum);
         r = rn;
         e0 = ne0;
         e1 = ne1;
@@ -1065,7 +1128,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
 // piece's item and first index chunk are prefetched while the current piece's
 // gathers are in flight (as in cheby_batch_rows_kernel); pieces are combined
 // by the ordered last-arriver reduction.
-template <int B, int U = 8, int MINB = 4, bool PEER = false>
+template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false>
 __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;
     constexpr int RPW = 32 / L;
@@ -1130,15 +1193,19 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             for (int t0 = 0; t0 < 32; t0 += U) {
                 if (!__any_sync(0xffffffffu, t0 < m)) break;
                 double2 val[U];
+                if constexpr (MASK) {
+                    gather_rows_masked<B, U>(a, c, t0, m, slot, cl, val, pol_last, pol_first);
+                } else {
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int t = t0 + q;
-                    const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                    CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
-                    val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                  u < a.hot_rows, pol_last, pol_first)
-                                                 : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                   : make_double2(0.0, 0.0);
+                    for (int q = 0; q < U; ++q) {
+                        const int t = t0 + q;
+                        const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                        CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
+                        val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                      u < a.hot_rows, pol_last, pol_first)
+                                                     : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                       : make_double2(0.0, 0.0);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
@@ -1165,7 +1232,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             if (cl == 0) a.hub_count[r] = 0u;
             double2 wp, ac;
             batch_prefetch<B>(a, r, cl, wp, ac);
-            batch_epilogue<B, PEER, MM>(a, pa, r, y, d, cl, wp, ac, msum);
+            batch_epilogue<B, PEER, MM, MASK>(a, pa, r, y, d, cl, wp, ac, msum);
         }
         (void)smask;
         job += stride;
@@ -1179,26 +1246,305 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
 }
 
 // ---------------------------------------------------------------------------
+// Sparse early steps of the batched step.  In the first steps
+// of a one-hot query only a few rows of w_{k-1} are nonzero (the sources, then
+// their neighbours); the reference's scatter skips every zero entry
+// (graph.cpp:262).  The pull step does the same in two kernels:
+//   * scan: a warp per job (a hub piece of the batched table, or a block of 32
+//     plain rows) streams the index once, one edge per lane, tests each edge's
+//     support bit (bitmap nz_in), and gathers only the rows whose bit is set, in
+//     edge order -- so every row / piece sum is the same sequential sum as in
+//     the full step, bit for bit (adding an exact zero changes nothing).  Rows
+//     with a set edge, and every hub row (through the ordered last-arriver
+//     combine of its pieces), get the epilogue here and a `done` bit;
+//   * fill: every other row has y = 0: w_{k+1} = -w_{k-1} (first step: 0), acc
+//     += c_k w_{k+1}, streamed and coalesced; a row whose w_{k-1} is zero keeps
+//     its (zero) iterate and acc, so only the first step (acc starts there) and
+//     the last (writes d*acc) store it.
+// The per-warp mass rows (C13) are written as in the full step.
+// ---------------------------------------------------------------------------
+struct SparseExtra {
+    uint32_t* done;              // rows finished by the scan kernel (global ids), pre-zeroed
+    const uint32_t* fill_mask;   // fill kernel: rows that can change with y = 0 (support of w_{k-1}'s
+                                 // predecessor; first step: of w_0); null = every row (last step)
+    const uint32_t* coarse;      // coarse support bitmap: bit i = any of rows [i << cshift, (i+1) << cshift)
+    uint32_t coarse_words;       // staged in shared memory by the scan kernel
+    int cshift;
+    uint32_t row_begin;          // first row of the chunk (fill kernel)
+    int64_t hb;                  // piece length of the batched table's hub rows
+};
+
+// Coarse support bitmap: word i, bit b = OR of the fine bits of rows
+// [(32 i + b) << cshift, (32 i + b + 1) << cshift).
+__global__ void coarsen_kernel(const uint32_t* fine, uint64_t fine_words, uint32_t* coarse, uint32_t coarse_words,
+                               int cshift) {
+    const uint32_t per = 1u << (cshift - 5);  // fine words per coarse bit
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < coarse_words; i += gridDim.x * blockDim.x) {
+        uint32_t out = 0;
+        for (uint32_t b = 0; b < 32; ++b) {
+            const uint64_t f0 = (static_cast<uint64_t>(i) * 32 + b) * per;
+            uint32_t any = 0;
+            for (uint32_t j = 0; j < per && f0 + j < fine_words; ++j) any |= fine[f0 + j];
+            out |= (any ? 1u : 0u) << b;
+        }
+        coarse[i] = out;
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void sparse_finalize(const BatchArgs& a, const SparseExtra& x, uint32_t r, double2 y,
+                                                int64_t d, int lane, double2& msum) {
+    constexpr int L = B / 2;
+    if (lane < L) {
+        double2 wp, ac;
+        batch_prefetch<B>(a, r, lane, wp, ac);
+        batch_epilogue<B, false, 1, true>(a, PeerArgs{}, r, y, d, lane, wp, ac, msum);
+    }
+    if (lane == 0) nz_set(x.done, a.row0 + r);
+}
+
+// Edge scan of [e0, e1): SC chunks of 32 edges per round, their index loads and then
+// their support-word loads all in flight together (a round trip per round, not per
+// chunk); each set edge, in edge order, goes to visit(edge, source row).
+constexpr int kSparseChunks = 8;
+template <typename Visit>
+__device__ __forceinline__ void sparse_scan_edges(const BatchArgs& a, const uint32_t* cs, int cshift, int64_t e0,
+                                                  int64_t e1, int lane, Visit visit) {
+    constexpr int SC = kSparseChunks;
+    uint32_t un[SC];  // next round's indices: in flight while this round is tested and visited
+#pragma unroll
+    for (int j = 0; j < SC; ++j) {
+        const int64_t ej = e0 + 32 * j + lane;
+        un[j] = ej < e1 ? ld_index_b(a.col + ej) : 0u;
+    }
+    for (int64_t e = e0; e < e1; e += 32 * SC) {
+        uint32_t u[SC];
+        bool bit[SC];
+#pragma unroll
+        for (int j = 0; j < SC; ++j) u[j] = un[j];
+        if (e + 32 * SC < e1) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) {
+                const int64_t ej = e + 32 * (SC + j) + lane;
+                un[j] = ej < e1 ? ld_index_b(a.col + ej) : 0u;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < SC; ++j) {  // the coarse bit (shared memory) gates the fine test
+            const uint32_t c = u[j] >> cshift;
+            bit[j] = e + 32 * j + lane < e1 && ((cs[c >> 5] >> (c & 31)) & 1u) && nz_bit(a.nz_in, u[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < SC; ++j) {
+            unsigned m = __ballot_sync(0xffffffffu, bit[j]);
+            while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1;
+                visit(e + 32 * j + i, __shfl_sync(0xffffffffu, u[j], i));
+            }
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kBatchThreads, 4) cheby_sparse_scan_kernel(const BatchArgs a, const SparseExtra x) {
+    constexpr int L = B / 2;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_plain = a.n_loc - a.hub_rows;
+    const uint32_t n_jobs = a.n_hub_items + (n_plain + 31) / 32;
+    extern __shared__ uint32_t cs[];  // coarse support bitmap
+    for (uint32_t i = threadIdx.x; i < x.coarse_words; i += blockDim.x) cs[i] = x.coarse[i];
+    __syncthreads();
+    double2 msum = make_double2(0.0, 0.0);
+    for (uint32_t job = wg; job < n_jobs; job += nw) {
+        if (job < a.n_hub_items) {  // one hub piece: [e0, e1) of row r
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + job);
+            const uint32_t r = raw.x, sb = raw.y;
+            const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
+            const int64_t e0 = code_e0(c), e1 = e0 + code_cnt(c);
+            const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1], d = re - rs;
+            const uint32_t P = static_cast<uint32_t>((d + x.hb - 1) / x.hb);
+            const uint32_t piece = static_cast<uint32_t>((e0 - rs) / x.hb);
+            double2 s = make_double2(0.0, 0.0);
+            sparse_scan_edges(a, cs, x.cshift, e0, e1, lane, [&](int64_t, uint32_t v) {
+                if (lane < L) {
+                    const double2 g = ld_gather2(a.w_cur + static_cast<size_t>(v) * B + 2 * lane);
+                    s.x += g.x;
+                    s.y += g.y;
+                }
+            });
+            if (P == 1) {
+                sparse_finalize<B>(a, x, r, s, d, lane, msum);
+                continue;
+            }
+            CPG_CHECK(sb + piece < a.chk_parts, "sparse hub slot", sb + piece, a.chk_parts);
+            if (lane < L) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[lane] = s;
+            __threadfence();
+            __syncwarp();
+            unsigned prev = 0;
+            if (lane == 0) prev = atomicAdd(&a.hub_count[r], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == P - 1) {  // last piece: ordered combine, as sum_partials in the full step
+                __threadfence();
+                double2 y = make_double2(0.0, 0.0);
+                if (lane < L) y = sum_partials<B, 8>(a.hub_partial, sb, P, lane);
+                if (lane == 0) a.hub_count[r] = 0u;
+                sparse_finalize<B>(a, x, r, y, d, lane, msum);
+            }
+        } else {  // 32 plain rows [r0, r0 + nr)
+            const uint32_t r0 = a.hub_rows + (job - a.n_hub_items) * 32;
+            const uint32_t nr = min(32u, a.n_loc - r0);
+            const int64_t rp = lane < static_cast<int>(nr) ? a.rowptr[r0 + lane] : INT64_MAX;
+            const int64_t E0 = __shfl_sync(0xffffffffu, rp, 0);
+            const int64_t E1 = a.rowptr[r0 + nr];
+            int cur = -1;
+            double2 s = make_double2(0.0, 0.0);
+            sparse_scan_edges(a, cs, x.cshift, E0, E1, lane, [&](int64_t ee, uint32_t v) {
+                const int rr = __popc(__ballot_sync(0xffffffffu, rp <= ee)) - 1;  // row of edge ee
+                if (rr != cur) {
+                    if (cur >= 0) {
+                        const int64_t b0 = __shfl_sync(0xffffffffu, rp, cur);
+                        const int64_t b1 = cur + 1 < static_cast<int>(nr) ? __shfl_sync(0xffffffffu, rp, cur + 1) : E1;
+                        sparse_finalize<B>(a, x, r0 + cur, s, b1 - b0, lane, msum);
+                    }
+                    cur = rr;
+                    s = make_double2(0.0, 0.0);
+                }
+                if (lane < L) {
+                    const double2 g = ld_gather2(a.w_cur + static_cast<size_t>(v) * B + 2 * lane);
+                    s.x += g.x;
+                    s.y += g.y;
+                }
+            });
+            if (cur >= 0) {
+                const int64_t b0 = __shfl_sync(0xffffffffu, rp, cur);
+                const int64_t b1 = cur + 1 < static_cast<int>(nr) ? __shfl_sync(0xffffffffu, rp, cur + 1) : E1;
+                sparse_finalize<B>(a, x, r0 + cur, s, b1 - b0, lane, msum);
+            }
+        }
+    }
+    batch_mass_flush<B, 1>(a, msum);
+}
+
+template <int B>
+__global__ void __launch_bounds__(kBatchThreads, 4) cheby_sparse_fill_kernel(const BatchArgs a, const SparseExtra x) {
+    constexpr int L = B / 2;
+    constexpr int RPW = 32 / L;
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / L, cl = lane % L;
+    const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    double2 msum = make_double2(0.0, 0.0);
+    constexpr int FU = 4;  // rows per lane per round: their loads in flight together
+    const uint32_t stride = nw * RPW;
+    for (uint32_t rb = x.row_begin + wg * RPW + slot; rb < a.n_loc; rb += FU * stride) {
+        bool live[FU];
+        int64_t d[FU];
+        double2 wp[FU];
+#pragma unroll
+        for (int f = 0; f < FU; ++f) {
+            const uint32_t r = rb + f * stride;
+            live[f] = r < a.n_loc && !nz_bit(x.done, a.row0 + r) && (!x.fill_mask || nz_bit(x.fill_mask, a.row0 + r));
+            d[f] = 0;
+            wp[f] = make_double2(0.0, 0.0);
+            if (live[f]) {
+                const uint32_t gr = a.row0 + r;
+                d[f] = a.rowptr[r + 1] - a.rowptr[r];
+                wp[f] = a.first ? reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl]
+                                : ld_stream2(a.w_io + static_cast<size_t>(gr) * B + 2 * cl);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < FU; ++f) {
+            const uint32_t r = rb + f * stride;
+            // w_{k-1} = 0 and y = 0: w_{k+1} = 0 is already stored and acc += 0 keeps acc
+            if (!live[f] || (!a.first && !a.last && wp[f].x == 0.0 && wp[f].y == 0.0)) continue;
+            const double2 ac = a.first ? make_double2(0.0, 0.0) : ld_stream2(a.acc + static_cast<size_t>(r) * B + 2 * cl);
+            batch_epilogue<B, false, 1, true>(a, PeerArgs{}, r, make_double2(0.0, 0.0), d[f], cl, wp[f], ac, msum);
+        }
+    }
+    batch_mass_flush<B, 1>(a, msum);
+}
+
+// First step of a one-hot batched query by push (unsharded graphs).  Column q of
+// w_0 has one nonzero, at s_q, and rows never list themselves, so
+//   w_1(v, q) = w_0(s_q, q) / d_v   for v in N(s_q)      (a one-term sum: exact)
+//   acc(v, q) = c_1 w_1(v, q)  ( = c_0 * 0 + c_1 w_1 ),   acc(s_q, q) = c_0 w_0(s_q, q)
+// and every other entry of w_1 and acc is zero (pre-zeroed by the caller).  This
+// is the full step's result bit for bit.  CTA b takes pieces b, b + G, ... of
+// every column's adjacency list, so each CTA's per-column mass partial (one row of
+// B doubles, mass_partial + b * warps * B) has a fixed order.
+constexpr int kPushThreads = 256;
+constexpr int kPushPer = 8;  // edges per thread per piece
+__global__ void __launch_bounds__(kPushThreads) cheby_first_push_kernel(const BatchArgs a, const uint32_t* gdeg,
+                                                                        const uint32_t* new_of_old,
+                                                                        const uint32_t* sources, uint32_t q0,
+                                                                        uint32_t count, uint32_t B) {
+    __shared__ double red[kPushThreads / 32];
+    __shared__ double mrow[kBatchCols];
+    constexpr int64_t PIECE = static_cast<int64_t>(kPushThreads) * kPushPer;
+    for (uint32_t q = threadIdx.x; q < B; q += blockDim.x) mrow[q] = 0.0;
+    __syncthreads();
+    const double c1 = a.coeffs[1];
+    for (uint32_t q = 0; q < count; ++q) {
+        const uint32_t s = new_of_old[sources[q0 + q]];
+        const int64_t rs = a.rowptr[s], re = a.rowptr[s + 1];
+        const double w0 = a.w_cur[static_cast<size_t>(s) * B + q];
+        const int64_t P = (re - rs + PIECE - 1) / PIECE;
+        if (blockIdx.x == 0 && threadIdx.x == 0)  // the source's own row: w_1 = 0 there, acc = c_0 w_0
+            a.acc[static_cast<size_t>(s) * B + q] = re > rs ? a.coeffs[0] * w0 : 0.0;
+        for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+            double m = 0.0;
+#pragma unroll
+            for (int i = 0; i < kPushPer; ++i) {
+                const int64_t e = rs + p * PIECE + i * kPushThreads + threadIdx.x;
+                if (e < re) {
+                    const uint32_t v = a.col[e];
+                    const double dd = static_cast<double>(gdeg[v]);
+                    const double w1 = w0 / dd;
+                    a.w_io[static_cast<size_t>(v) * B + q] = w1;
+                    a.acc[static_cast<size_t>(v) * B + q] = c1 * w1;
+                    if (a.nz_out) nz_set(a.nz_out, v);
+                    m += dd * w1;
+                }
+            }
+            m = block_sum<kPushThreads>(m, red);
+            if (threadIdx.x == 0) mrow[q] += m;
+        }
+    }
+    __syncthreads();
+    if (a.mass_partial)
+        for (uint32_t q = threadIdx.x; q < B; q += blockDim.x)
+            a.mass_partial[static_cast<size_t>(blockIdx.x) * (kBatchThreads / 32) * B + q] = mrow[q];
+}
+
+// ---------------------------------------------------------------------------
 // Small kernels around the steps.
 // ---------------------------------------------------------------------------
 
 // w_0 = D^-1 e_s in the global (relabelled) ids; vector pre-zeroed.
 // Query group: thread t seeds slice t (w + t*stride) for source q0 + t.
+// nz0 (optional, pre-zeroed): support bitmap of w_0 (the union over the group).
 __global__ void init_onehot_kernel(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* new_of_old,
-                                   const uint32_t* sources, uint32_t q0, uint32_t count) {
+                                   const uint32_t* sources, uint32_t q0, uint32_t count, uint32_t* nz0) {
     const uint32_t t = threadIdx.x;
     if (t >= count) return;
     const uint32_t s = new_of_old[sources[q0 + t]];
     w[t * stride + s] = 1.0 / static_cast<double>(gdeg[s]);
+    if (nz0) nz_set(nz0, s);
 }
 
 // Batched: column j of W_0 = D^-1 e_{s_j}; matrix [n_pad][B] pre-zeroed.
 __global__ void init_onehot_batch_kernel(double* W, const uint32_t* gdeg, const uint32_t* new_of_old,
-                                         const uint32_t* sources, uint32_t q0, uint32_t count, uint32_t B) {
+                                         const uint32_t* sources, uint32_t q0, uint32_t count, uint32_t B,
+                                         uint32_t* nz0) {
     const uint32_t j = threadIdx.x;
     if (j < count) {
         const uint32_t s = new_of_old[sources[q0 + j]];
         W[static_cast<size_t>(s) * B + j] = 1.0 / static_cast<double>(gdeg[s]);
+        if (nz0) nz_set(nz0, s);
     }
 }
 
@@ -1337,6 +1683,15 @@ void launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStrea
 
 void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* gq, bool pdl) {
     const bool group = gq && gq->nq > 1;
+    if (a.nz_in && !group) {  // masked (sparse early) step
+        if (a.tile == kTileMid)
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileMid, true>, grid, kStepThreads, st, a);
+        else if (a.tile == kTileLarge)
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileLarge, true>, grid, kStepThreads, st, a);
+        else
+            launch_pdl(pdl, cheby_step_kernel<kStepThreads, kTileSmall, true>, grid, kStepThreads, st, a);
+        return;
+    }
     // query groups launch plainly: PDL measured 3% slower on config 1 (profiles/r02/pdl_ab.txt)
     if (a.tile == kTileMid) {
         if (group)
@@ -1365,9 +1720,18 @@ void launch_step(const StepArgs& a, int grid, cudaStream_t st, const StepGroup* 
 void launch_step_hubs(const StepArgs& a, int grid, cudaStream_t st, bool) {
     // the split step launches plainly: no PDL gain at its 20 ms steps, and the
     // post-wait L1 invalidation cost 3% (profiles/r02/ab_fence.txt)
-    launch_pdl(false, cheby_step_hubs_kernel<kStepThreads>, grid, kStepThreads, st, a);
+    if (a.nz_in)
+        launch_pdl(false, cheby_step_hubs_kernel<kStepThreads, true>, grid, kStepThreads, st, a);
+    else
+        launch_pdl(false, cheby_step_hubs_kernel<kStepThreads>, grid, kStepThreads, st, a);
 }
 void launch_step_tiles(const StepArgs& a, int tile, int grid, cudaStream_t st, bool) {
+    if (a.nz_in) {
+#define CPG_L(T, M) launch_pdl(false, cheby_step_tiles_kernel<kStepThreads, T, M, true>, grid, kStepThreads, st, a)
+        CPG_TILES_SWITCH(CPG_L)
+#undef CPG_L
+        return;
+    }
 #define CPG_L(T, M) launch_pdl(false, cheby_step_tiles_kernel<kStepThreads, T, M>, grid, kStepThreads, st, a)
     CPG_TILES_SWITCH(CPG_L)
 #undef CPG_L
@@ -1459,6 +1823,16 @@ int launch_batch(const BatchArgs& a, int B, int grid, cudaStream_t st, const Pee
         CPG_PEER_SWITCH(cheby_batch_kernel, B, grid, st, a, *pa);
         return grid;
     }
+    if (a.nz_in) {  // masked (sparse early) step: the default geometry of each width
+        switch (B) {
+        case 4: launch_pdl(pdl, cheby_batch_kernel<4, 8, 4, false, true>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+        case 8: launch_pdl(pdl, cheby_batch_kernel<8, 8, 4, false, true>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+        case 16: launch_pdl(pdl, cheby_batch_kernel<16, 8, 4, false, true>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+        case 32: launch_pdl(pdl, cheby_batch_kernel<32, 4, 4, false, true>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+        default: launch_pdl(pdl, cheby_batch_kernel<64, 4, 4, false, true>, grid, kBatchThreads, st, a, PeerArgs{}); break;
+        }
+        return grid;
+    }
     static const int cfg = [] {  // tuning hook: CPG_SLOT_CFG = U*10 + MINB
         const char* e = std::getenv("CPG_SLOT_CFG");
         return e ? std::atoi(e) : 0;
@@ -1518,11 +1892,22 @@ int split_cfg(const char* env, int B) {
     default: return launch_capped(KERNEL<B, 8, 4>, a, grid, st);                                    \
     }
 
+// Masked (sparse early) instances of the split kernels, at the default geometry of each width.
+#define CPG_MASK_SWITCH(KERNEL, B)                                                                   \
+    switch (B) {                                                                                    \
+    case 4: return launch_capped(KERNEL<4, 8, 4, false, true>, a, grid, st);                        \
+    case 8: return launch_capped(KERNEL<8, 8, 4, false, true>, a, grid, st);                        \
+    case 16: return launch_capped(KERNEL<16, 8, 3, false, true>, a, grid, st);                      \
+    case 32: return launch_capped(KERNEL<32, 8, 4, false, true>, a, grid, st);                      \
+    default: return launch_capped(KERNEL<64, 8, 4, false, true>, a, grid, st);                      \
+    }
+
 int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_pieces_kernel, B, grid, st, a, *pa);
         return grid;
     }
+    if (a.nz_in) CPG_MASK_SWITCH(cheby_batch_pieces_kernel, B)
     static const int cfg16 = split_cfg("CPG_PIECES_CFG", 16), cfg64 = split_cfg("CPG_PIECES_CFG", 64);
     if (B == 16) {
         const int cfg = cfg16;
@@ -1545,6 +1930,7 @@ int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, cons
         CPG_PEER_SWITCH(cheby_batch_rows_kernel, B, grid, st, a, *pa);
         return grid;
     }
+    if (a.nz_in) CPG_MASK_SWITCH(cheby_batch_rows_kernel, B)
     static const int cfg16 = split_cfg("CPG_ROWS_CFG", 16), cfg64 = split_cfg("CPG_ROWS_CFG", 64);
     if (B == 16) {
         const int cfg = cfg16;
@@ -1562,18 +1948,51 @@ int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, cons
     return grid;
 }
 
+int launch_first_push(const BatchArgs& a, const uint32_t* gdeg, const uint32_t* new_of_old, const uint32_t* sources,
+                      uint32_t q0, uint32_t count, uint32_t B, int grid, cudaStream_t st) {
+    cheby_first_push_kernel<<<grid, kPushThreads, 0, st>>>(a, gdeg, new_of_old, sources, q0, count, B);
+    return grid;  // mass rows in CTAs (one row per CTA written, the rest stay zero)
+}
+
+void launch_coarsen(const uint32_t* fine, uint64_t fine_words, uint32_t* coarse, uint32_t coarse_words, int cshift,
+                    cudaStream_t st) {
+    coarsen_kernel<<<(coarse_words + 255) / 256, 256, 0, st>>>(fine, fine_words, coarse, coarse_words, cshift);
+}
+
+int launch_sparse_step(const BatchArgs& a, int B, uint32_t* done, const uint32_t* fill_mask, const uint32_t* coarse,
+                       uint32_t coarse_words, int cshift, uint32_t row_begin, int64_t hb, int grid, cudaStream_t st) {
+    const SparseExtra x{done, fill_mask, coarse, coarse_words, cshift, row_begin, hb};
+    const size_t smem = sizeof(uint32_t) * coarse_words;
+#define CPG_SPARSE(BB)                                                                   \
+    cheby_sparse_scan_kernel<BB><<<grid, kBatchThreads, smem, st>>>(a, x);               \
+    {                                                                                    \
+        BatchArgs f = a;                                                                 \
+        f.mass_partial = a.mass_partial ? a.mass_partial + static_cast<size_t>(grid) * (kBatchThreads / 32) * BB : nullptr; \
+        cheby_sparse_fill_kernel<BB><<<grid, kBatchThreads, 0, st>>>(f, x);              \
+    }
+    switch (B) {
+    case 4: CPG_SPARSE(4) break;
+    case 8: CPG_SPARSE(8) break;
+    case 16: CPG_SPARSE(16) break;
+    case 32: CPG_SPARSE(32) break;
+    default: CPG_SPARSE(64) break;
+    }
+#undef CPG_SPARSE
+    return 2 * grid;  // mass rows: one per warp of each kernel, in units of CTAs
+}
+
 int batch_occupancy() {
     int blocks = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, cheby_batch_kernel<64>, kBatchThreads, 0);
     return blocks;
 }
 void launch_init_onehot(double* w, uint64_t stride, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                        uint32_t q0, uint32_t count, cudaStream_t st) {
-    init_onehot_kernel<<<1, 32, 0, st>>>(w, stride, gdeg, no, src, q0, count);
+                        uint32_t q0, uint32_t count, cudaStream_t st, uint32_t* nz0) {
+    init_onehot_kernel<<<1, 32, 0, st>>>(w, stride, gdeg, no, src, q0, count, nz0);
 }
 void launch_init_onehot_batch(double* W, const uint32_t* gdeg, const uint32_t* no, const uint32_t* src,
-                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st) {
-    init_onehot_batch_kernel<<<1, 64, 0, st>>>(W, gdeg, no, src, q0, count, B);
+                              uint32_t q0, uint32_t count, uint32_t B, cudaStream_t st, uint32_t* nz0) {
+    init_onehot_batch_kernel<<<1, 64, 0, st>>>(W, gdeg, no, src, q0, count, B, nz0);
 }
 void launch_init_dense(double* w, const uint32_t* gdeg, const uint32_t* no, const double* seed,
                        uint32_t n, double a, cudaStream_t st) {
