@@ -423,17 +423,6 @@ def main():
     run_ours(args, cfg)
 
 
-def sparse_steps_used(batched, sharded, K):
-    """Steps of each query that gather only the nonzero rows of w_{k-1} (DESIGN.md 4.7;
-    the library's rule in api.cu sparse_steps: 3 single-source, 2 batched, 1 sharded)."""
-    m = 2 if batched else 3
-    if "CPG_SPARSE_STEPS" in os.environ:
-        m = max(0, int(os.environ["CPG_SPARSE_STEPS"]))
-    if sharded:
-        m = min(m, 1)
-    return min(m, K)
-
-
 def run_ours(args, cfg):
     import torch
 
@@ -647,7 +636,7 @@ def run_ours(args, cfg):
                                       f"NCCL, {dg.info.chunks} chunks overlapped")
                                      if world > 1 or args.sharded else None),
                        "l2": "inputs larger than L2 (index stream 4*nnz bytes per step, re-read every step)",
-                       "sparse_early_steps": sparse_steps_used(batched, world > 1 or args.sharded, K)},
+                       "sparse_early_steps": dg.sparse_early_steps(tile if batched else 1, K)},
             "roofline": {"bound": "hbm", "timed": "every step full-support (sparse early steps off for this call)", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "basis": basis,
                          "frac_model": achieved_model / peak, "achieved_model": achieved_model,

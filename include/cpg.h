@@ -260,6 +260,13 @@ int cpg_apply_walk(cpg_graph* g, const double* x, double* y);
 /* Algorithmic bytes of one single-source step for this handle. */
 double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile);
 
+/* Steps at the head of a one-hot query on this handle that gather only the rows
+ * of w_{k-1} with a nonzero entry, as the reference's scatter skips zero entries
+ * (graph.cpp:262); tile <= 1 = the single-source step.  Results are bit-identical
+ * to full steps; the count is the library's measured default or
+ * the CPG_SPARSE_STEPS override. */
+uint32_t cpg_sparse_early_steps(const cpg_graph* g, uint32_t tile, uint32_t K);
+
 /* ---- synthetic inputs (bench/test harness; deterministic, seed-addressed) ----
  * R-MAT (a,b,c,d) with 2^scale ids and n_samples draws, or Chung-Lu with
  * power-law weights; both symmetrised, deduplicated, self-loops dropped,

@@ -334,6 +334,10 @@ class DeviceGraph:
     def bytes_per_step(self, tile: int = 1) -> float:
         return float(L.lib().cpg_bytes_per_step(self._h, tile))
 
+    def sparse_early_steps(self, tile: int, K: int) -> int:
+        """Steps at the head of a one-hot query that gather only nonzero rows."""
+        return int(L.lib().cpg_sparse_early_steps(self._h, tile, K))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             L.lib().cpg_graph_destroy(self._h)  # synchronises the device first

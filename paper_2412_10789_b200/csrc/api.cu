@@ -360,11 +360,17 @@ void ensure_group(cpg_graph* g, Workspace* w, uint32_t K, uint32_t Q) {
 // sources).  Results are bit-identical to the unmasked steps.  A sharded rank
 // builds only its own rows' bits, so there only step 1 (the sources' bitmap,
 // known to every rank) is masked; the fused all-gather path is never masked.
-// Defaults: 3 steps for one source (its 1- and 2-hop balls stay small), 2 for a
-// batched tile; CPG_SPARSE_STEPS=M overrides (0 = off).
+// Defaults from the A/B on one B200 (profiles/r02/sparse/): a batched tile masks
+// its first 2 steps on graphs of >= 1.5 M directed edges (configs 2-5: +3..11%;
+// config 1's 31-us steps lose more to the extra launches than the skipped
+// gathers give back, and a third masked step always loses: the 2-hop ball already
+// carries most of the volume); one source masks 2 steps only where the iterate
+// exceeds the L2 (split step, config 5: +1%; an L2-resident iterate loses 3-5%).
+// CPG_SPARSE_STEPS=M overrides (0 = off).
 uint32_t sparse_steps(const cpg_graph* g, bool single, uint32_t K) {
     if (g->p2p) return 0;
-    uint32_t M = single ? 3 : 2;
+    uint32_t M = single ? (g->step_split ? 2 : 0)
+                        : (g->nnz_loc >= 1500000ull ? 2 : 0);
     if (const char* e = std::getenv("CPG_SPARSE_STEPS")) M = static_cast<uint32_t>(std::max(0, std::atoi(e)));
     if (g->comm) M = std::min<uint32_t>(M, 1);
     return std::min(M, K);
@@ -1616,6 +1622,12 @@ int cpg_chebypower_vec_trace(cpg_graph* g, const double* coeffs, uint32_t K, con
                              double* r_trace, double* est_trace) {
     if (!seed) return guarded([] { require(false, "null argument"); });
     return trace_impl(g, coeffs, K, 0, seed, out, r_trace, est_trace);
+}
+
+uint32_t cpg_sparse_early_steps(const cpg_graph* g, uint32_t tile, uint32_t K) {
+    if (!g) return 0;
+    if (!g->members.empty()) return cpg_sparse_early_steps(g->members[0], tile, K);
+    return sparse_steps(g, tile <= 1, K);
 }
 
 double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile) {

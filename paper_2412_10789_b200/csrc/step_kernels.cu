@@ -1437,6 +1437,51 @@ __global__ void __launch_bounds__(kBatchThreads, 4) cheby_sparse_fill_kernel(con
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     double2 msum = make_double2(0.0, 0.0);
+    if (x.fill_mask) {
+        // Few rows to fill (the support of an early iterate): a lane tests 32 rows with one
+        // word of each bitmap, the warp skips 1024 rows per round, and the slots share the
+        // set bits of a live word, RPW at a time.
+        const uint64_t g0 = static_cast<uint64_t>(a.row0) + x.row_begin, g1 = static_cast<uint64_t>(a.row0) + a.n_loc;
+        const uint32_t w0 = static_cast<uint32_t>(g0 >> 5), w1 = static_cast<uint32_t>((g1 + 31) >> 5);
+        for (uint64_t wb = static_cast<uint64_t>(w0) + static_cast<uint64_t>(wg) * 32; wb < w1;
+             wb += static_cast<uint64_t>(nw) * 32) {
+            const uint64_t wi = wb + lane;
+            uint32_t live = 0;
+            if (wi < w1) {
+                live = __ldg(x.fill_mask + wi) & ~x.done[wi];
+                const uint64_t b0 = wi * 32;
+                if (b0 < g0) live &= ~0u << (g0 - b0);
+                if (b0 + 32 > g1) live &= (1u << (g1 - b0)) - 1u;
+            }
+            unsigned any = __ballot_sync(0xffffffffu, live != 0u);
+            while (any) {
+                const int src = __ffs(any) - 1;
+                any &= any - 1;
+                uint32_t word = __shfl_sync(0xffffffffu, live, src);
+                const uint64_t base = (wb + src) * 32;
+                while (word) {
+                    uint32_t mine = word;
+                    for (int s = 0; s < slot; ++s) mine &= mine - 1;  // slot s takes the s-th set bit
+                    if (mine) {
+                        const uint32_t gr = static_cast<uint32_t>(base) + static_cast<uint32_t>(__ffs(mine) - 1);
+                        const uint32_t r = gr - a.row0;
+                        const int64_t d = a.rowptr[r + 1] - a.rowptr[r];
+                        const double2 wp = a.first ? reinterpret_cast<const double2*>(a.w_cur + static_cast<size_t>(gr) * B)[cl]
+                                                   : ld_stream2(a.w_io + static_cast<size_t>(gr) * B + 2 * cl);
+                        // w_{k-1} = 0 and y = 0: w_{k+1} = 0 is already stored and acc += 0 keeps acc
+                        if (a.first || a.last || wp.x != 0.0 || wp.y != 0.0) {
+                            const double2 ac = a.first ? make_double2(0.0, 0.0)
+                                                       : ld_stream2(a.acc + static_cast<size_t>(r) * B + 2 * cl);
+                            batch_epilogue<B, false, 1, true>(a, PeerArgs{}, r, make_double2(0.0, 0.0), d, cl, wp, ac, msum);
+                        }
+                    }
+                    for (int s = 0; s < RPW && word; ++s) word &= word - 1;
+                }
+            }
+        }
+        batch_mass_flush<B, 1>(a, msum);
+        return;
+    }
     constexpr int FU = 4;  // rows per lane per round: their loads in flight together
     const uint32_t stride = nw * RPW;
     for (uint32_t rb = x.row_begin + wg * RPW + slot; rb < a.n_loc; rb += FU * stride) {
