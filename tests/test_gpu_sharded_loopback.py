@@ -49,18 +49,24 @@ def _run_ranks(fn, R):
     return out
 
 
-@pytest.mark.parametrize("R", [2, 3, 8])
-@pytest.mark.parametrize("C", [1, 4])
-def test_loopback_sharded_matches_reference(cpg, graph, R, C, monkeypatch):
+@pytest.mark.parametrize("R,C,sparse", [(2, 1, None), (3, 1, None), (8, 1, None), (2, 4, None), (3, 4, None),
+                                        (8, 4, None), (3, 1, "2"), (2, 4, "2"), (8, 4, "1")])
+def test_loopback_sharded_matches_reference(cpg, graph, R, C, sparse, monkeypatch):
     from oracle import RefGraph
 
     off, nb = graph
     monkeypatch.setenv("CPG_CHUNKS", str(C))
+    # sparse early steps: a sharded rank masks step 1 only (the sources'
+    # bitmap); this graph is below the default's edge threshold, so force it too
+    if sparse is not None:
+        monkeypatch.setenv("CPG_SPARSE_STEPS", sparse)
     grp = cpg.LoopbackGroup(R)
     shards = [cpg.DeviceGraph.loopback(off, nb, r, grp) for r in range(R)]
     n = len(off) - 1
     for r, dg in enumerate(shards):
         assert (dg.info.rank, dg.info.nranks, dg.info.chunks) == (r, R, C)
+        if sparse is not None:
+            assert dg.sparse_early_steps(8, 26) == 1 and dg.sparse_early_steps(1, 26) == 1
         assert dg.info.n_padded % (R * C) == 0
     # the shards partition the rows and the edges
     assert sum(d.info.n_local for d in shards) == shards[0].info.n_padded

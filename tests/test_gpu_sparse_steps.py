@@ -123,3 +123,30 @@ def test_small_graphs_and_star_sources(cpg, gpu, monkeypatch):
             for j in range(min(n, 8)):
                 want, _, _ = ref.cheby_power(PPR, 0.2, j, K)
                 assert_parity(gotb[j], want)
+
+
+def test_default_rule_and_override(cpg, gpu, hub_graph, monkeypatch):
+    """cpg_sparse_early_steps reports the library's rule (api.cu sparse_steps): batched tiles
+    mask 2 steps from 1.5 M directed edges, one source only where the iterate exceeds the L2;
+    CPG_SPARSE_STEPS overrides; never more than K."""
+    off, nb = hub_graph
+    monkeypatch.delenv("CPG_SPARSE_STEPS", raising=False)
+    small = cpg.Graph.from_csr(off, nb).device(0)          # ~1 M directed edges
+    assert len(nb) < 1500000
+    assert small.sparse_early_steps(16, 26) == 0 and small.sparse_early_steps(1, 26) == 0
+    boff, bnb = cpg.gen_chunglu(60000, 1200000, 2.0, 40.0, 12000, seed=5)
+    assert len(bnb) >= 1500000
+    big = cpg.Graph.from_csr(boff, bnb).device(0)
+    assert big.sparse_early_steps(16, 26) == 2 and big.sparse_early_steps(16, 1) == 1
+    assert big.sparse_early_steps(1, 26) == 0               # iterate fits the L2
+    monkeypatch.setenv("CPG_SPARSE_STEPS", "5")
+    assert small.sparse_early_steps(16, 26) == 5 and small.sparse_early_steps(1, 3) == 3
+    # the default batched path on the bigger graph (masks on) against the reference
+    monkeypatch.delenv("CPG_SPARSE_STEPS")
+    ref = _ref(boff, bnb)
+    src = _sources(boff, ref)
+    got, st = cpg.cheby_power_many(big, cpg.Kernel.ppr(0.2), src, 26, batched=True, tile=8)
+    for j, s in enumerate(src):
+        want, _, _ = ref.cheby_power(PPR, 0.2, s, 26)
+        assert_parity(got[j], want)
+    assert st.mass_err_max <= 1e-9
