@@ -673,7 +673,10 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         return !e || e[0] != '0';
     }();
     const bool split = batch_split(g->nnz_loc);
-    const bool use_ctr = dyn_jobs && !split;
+    // column-window piece tables: the piece kernel claims its pieces in list order
+    bool cw_tables = false;
+    for (const ItemTable& t : bt.tables) cw_tables = cw_tables || t.meta != nullptr;
+    const bool use_ctr = (dyn_jobs && !split) || cw_tables;
     // PDL between the fused step kernels (see run_steps): one chunk, no data plane, no profiling
     const bool pdl = !g->comm && C == 1 && !prof;
     if (use_ctr) {
@@ -694,7 +697,7 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
     uint32_t* nz = ensure_nz(g, w, 2 * M + (M ? (cwords + nzw - 1) / nzw : 0), st);
     uint32_t* coarse = nz ? nz + 2 * M * nzw : nullptr;
     const int64_t hb = split ? batch_piece_edges(static_cast<int>(B)) : batch_hub_edges(static_cast<int>(B));
-    const bool sparse_kern = [] {  // CPG_SPARSE_KERNEL=0: masked full-step kernels instead (A/B; read per call)
+    const bool sparse_kern = cw_tables || [] {  // CPG_SPARSE_KERNEL=0: masked full-step kernels instead (A/B; read per call)
         const char* e = std::getenv("CPG_SPARSE_KERNEL");
         return !e || e[0] != '0';
     }();
@@ -724,6 +727,9 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
         b.job_ctr = nullptr;
         b.nz_in = nz && k <= M ? nz + (k - 1) * nzw : nullptr;  // masked (sparse early) step
         b.nz_out = nz && k < M ? nz + k * nzw : nullptr;
+        b.hub_meta = nullptr;
+        b.meta_row0 = 0;
+        b.n_pad_rows = g->n_pad;
 #if CPG_CHECKED
         b.chk_nnz = g->nnz_loc;
         b.chk_npad = g->n_pad;
@@ -748,6 +754,8 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
             b.hub_rows = t.row_begin + t.n_hubs;  // first non-hub row of the chunk
             b.n_loc = t.row_end;                  // end row of the chunk
             b.row0 = chunk_row0(g, c);
+            b.hub_meta = t.meta;
+            b.meta_row0 = t.row_begin;
             if (sparse_kern && b.nz_in) {  // sparse early step: edge scan + fill
                 b.mass_partial = mp_step + rows * B;
 #if CPG_CHECKED
@@ -777,14 +785,19 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                 if (t.n_hub_items) {
                     BatchArgs h = b;
                     h.n_loc = b.hub_rows;
+                    if (t.meta) h.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
                     h.mass_partial = mp_step + rows * B;
 #if CPG_CHECKED
                     h.chk_mass = step_rows - rows;
 #endif
                     const uint32_t warps = (t.n_hub_items + 64 / B - 1) / (64 / B);
+                    // (launch_capped trims the grid to the instance's own occupancy)
+                    const int hocc = t.meta ? kBatchMaxCtasPerSm : occ;
                     const int hgrid = static_cast<int>(std::max<uint32_t>(
-                        1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(occ * g->sm_count))));
-                    rows += W * launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
+                        1, std::min<uint32_t>((warps + 7) / 8, static_cast<uint32_t>(hocc * g->sm_count))));
+                    const int pg = launch_batch_pieces(h, static_cast<int>(B), hgrid, st, pa);
+                    if (pg < 0) fail(CPG_ECUDA, "column-window pieces: unsupported launch");
+                    rows += W * pg;
                     ++launches;
                 }
                 if (t.row_end > b.hub_rows) {
@@ -1309,7 +1322,10 @@ int cpg_graph_destroy(cpg_graph* g) {
         for (auto& t : g->wtables) cudaFree(t.items);
         for (auto& kv : g->btabs)
             for (auto& t : kv.second.tables)
+            {
                 if (t.items) cudaFree(t.items);
+                if (t.meta) cudaFree(t.meta);
+            }
         for (void* p : {(void*)g->rowptr, (void*)g->col})
             dfree_aligned(p);
         for (void* p : {(void*)g->gdeg, (void*)g->new_of_old})

@@ -18,6 +18,7 @@ struct ItemTable {
     WorkItem* items = nullptr;
     uint32_t n_items = 0, n_hubs = 0, n_hub_items = 0;
     uint32_t row_begin = 0, row_end = 0;
+    uint2* meta = nullptr;  // column-window hub pieces: (first slot, piece count) per hub row, or null
 };
 } // namespace cpg
 

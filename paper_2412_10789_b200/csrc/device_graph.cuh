@@ -94,6 +94,10 @@ struct __align__(16) WorkItem {
     uint64_t c;
 };
 constexpr uint64_t kHubBit = 1ull << 63;
+// Column-window hub pieces: b = the piece's OWN partial slot (the row's
+// first slot and piece count come from BatchArgs::hub_meta), and bit 54 marks a piece
+// whose columns all lie in one window of the warm tier of the iterate.
+constexpr uint64_t kWarmBit = 1ull << 54;
 __host__ __device__ inline uint64_t tile_code(uint64_t e0, uint32_t cnt, uint32_t lg) {
     return e0 | (static_cast<uint64_t>(cnt) << 40) | (static_cast<uint64_t>(lg) << 54);
 }
@@ -158,6 +162,9 @@ struct BatchArgs {
     double* mass_partial;       // [gridDim.x * warps][B] per-warp column sums of d_v w_{k+1}(v) (acceptance C13); null = off
     const uint32_t* nz_in;      // MASK instances: support bitmap of w_cur's rows (any column nonzero)
     uint32_t* nz_out;           // MASK instances: support bitmap of w_{k+1}'s rows to build (pre-zeroed), or null
+    const uint2* hub_meta;      // column-window pieces: (first partial slot, piece count) of hub row meta_row0 + i; null = uniform pieces
+    uint32_t meta_row0;
+    uint32_t n_pad_rows;        // rows of the replicated iterate (range-policy window)
     CPG_CHK_FIELDS              // CPG_CHECKED builds only (partial / mass bounds in rows of B doubles)
 };
 

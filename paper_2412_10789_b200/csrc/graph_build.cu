@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <unordered_map>
@@ -193,6 +194,162 @@ void build_hub_items(const int64_t* rowptr, uint32_t row0, uint32_t row1, int64_
     *out = items;
     *n_hub_out = n_hub;
     *n_items_out = total;
+}
+
+// ---------------------------------------------------------------------------
+// Column-window hub pieces.  The gathers of a hub row are column
+// sorted.  The rows of the iterate past the L2-resident hot prefix but still
+// gathered hundreds of times per step (the "warm tier", [lo, lo + W*S) in the
+// degree order) are cut into W windows of S rows, each small enough to stay in
+// L2; the biggest hubs (degree > cw_deg) are cut at those boundaries, and the
+// piece list is ordered window-major, so the pieces in flight (claimed in list
+// order by the piece kernel) gather from one window at a time.
+// ---------------------------------------------------------------------------
+
+// bnd[h * (W + 1) + j] = first edge of hub row row0 + h with column >= lo + j * S.
+__global__ void k_cw_bounds(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t n_cw, uint32_t lo,
+                            uint32_t S, uint32_t W, int64_t* bnd) {
+    const uint64_t total = static_cast<uint64_t>(n_cw) * (W + 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t h = static_cast<uint32_t>(i / (W + 1)), j = static_cast<uint32_t>(i % (W + 1));
+        int64_t a = rowptr[row0 + h], b = rowptr[row0 + h + 1];
+        const uint64_t key = static_cast<uint64_t>(lo) + static_cast<uint64_t>(j) * S;
+        while (a < b) {
+            const int64_t mid = a + (b - a) / 2;
+            if (col[mid] < key) a = mid + 1;
+            else b = mid;
+        }
+        bnd[i] = a;
+    }
+}
+
+// Segment s of a column-window row: 0 = hot prefix, 1..W = warm windows, W + 1 = cold tail.
+__device__ __forceinline__ void cw_segment(const int64_t* bnd_h, int64_t rs, int64_t re, uint32_t W, uint32_t s,
+                                           int64_t& b, int64_t& e) {
+    b = s == 0 ? rs : bnd_h[s - 1];
+    e = s == W + 1 ? re : bnd_h[s];
+}
+
+__global__ void k_cw_pieces(const int64_t* rowptr, uint32_t row0, uint32_t n_hub, uint32_t n_cw, const int64_t* bnd,
+                            uint32_t W, int64_t piece, uint32_t* P) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= n_hub; j += gridDim.x * blockDim.x) {
+        uint32_t p = 0;
+        if (j < n_hub) {
+            const int64_t rs = rowptr[row0 + j], re = rowptr[row0 + j + 1];
+            if (j < n_cw) {
+                for (uint32_t s = 0; s <= W + 1; ++s) {
+                    int64_t b, e;
+                    cw_segment(bnd + static_cast<size_t>(j) * (W + 1), rs, re, W, s, b, e);
+                    p += static_cast<uint32_t>((e - b + piece - 1) / piece);
+                }
+            } else {
+                p = static_cast<uint32_t>((re - rs + piece - 1) / piece);
+            }
+        }
+        P[j] = p;
+    }
+}
+
+// One warp per hub row: the row's pieces in column order (piece index = slot order, so
+// the ordered combine adds them left to right), each with its own slot and a sort key
+// phase << 32 | list index.  Warm-window pieces get phase = window; the others phase 0,
+// or (spread) one of the W phases round-robin, so every phase mixes L2-resident window
+// gathers with DRAM-bound ones.
+__global__ void k_cw_items(const int64_t* rowptr, uint32_t row0, const uint32_t* P, const uint32_t* base,
+                           uint32_t n_hub, uint32_t n_cw, const int64_t* bnd, uint32_t W, int64_t piece,
+                           uint32_t slot_off, int spread, WorkItem* items, uint64_t* keys, uint2* meta) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_hub; j += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t rs = rowptr[row0 + j], re = rowptr[row0 + j + 1];
+        if (lane == 0) meta[j] = make_uint2(slot_off + base[j], P[j]);
+        uint32_t p0 = 0;
+        const uint32_t n_seg = j < n_cw ? W + 2 : 1;
+        for (uint32_t s = 0; s < n_seg; ++s) {
+            int64_t b = rs, e = re;
+            if (j < n_cw) cw_segment(bnd + static_cast<size_t>(j) * (W + 1), rs, re, W, s, b, e);
+            const uint32_t np = static_cast<uint32_t>((e - b + piece - 1) / piece);
+            const bool warm = j < n_cw && s >= 1 && s <= W;
+            for (uint32_t p = lane; p < np; p += 32) {
+                const int64_t e0 = b + static_cast<int64_t>(p) * piece;
+                const uint32_t cnt = static_cast<uint32_t>(min(piece, e - e0));
+                const uint32_t idx = base[j] + p0 + p;
+                items[idx] = WorkItem{row0 + j, slot_off + idx,
+                                      tile_code(static_cast<uint64_t>(e0), cnt, 0) | kHubBit | (warm ? kWarmBit : 0ull)};
+                const uint32_t phase = warm ? s : ((spread & 1) ? 1 + idx % W : 0);
+                // spread & 2: the pieces of a window longest first (a warp's RPW pieces run in lock-step)
+                const uint32_t sec = warm && (spread & 2) ? ((static_cast<uint32_t>(piece) - cnt) << 20) | (idx & 0xfffffu) : idx;
+                keys[idx] = (static_cast<uint64_t>(phase) << 32) | sec;
+            }
+            p0 += np;
+        }
+    }
+}
+
+__global__ void k_permute_items(const WorkItem* in, const uint32_t* perm, uint32_t n, WorkItem* out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[perm[i]];
+}
+
+__global__ void k_iota(uint32_t* v, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+// Column-window hub items of rows [row0, row1): hubs = rows of degree > piece (as in
+// build_hub_items), the first n_cw of them (degree > cw_deg) cut at the window
+// boundaries.  Returns false (nothing allocated) when no row qualifies.
+bool build_cw_hub_items(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t row1, int64_t piece,
+                        int64_t cw_deg, uint32_t lo, uint32_t S, uint32_t W, int spread, uint32_t slot_off,
+                        ItemTable* t, cudaStream_t st) {
+    const uint32_t n_rows = row1 - row0;
+    if (!n_rows || !W) return false;
+    unsigned int* d_cnt = dalloc<unsigned int>(2);
+    CPG_CUDA(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned int), st));
+    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, piece, d_cnt);
+    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, std::max(cw_deg, piece), d_cnt + 1);
+    unsigned int cnt[2] = {0, 0};
+    CPG_CUDA(cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    CPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_cnt);
+    const uint32_t n_hub = cnt[0], n_cw = cnt[1];
+    if (!n_cw) return false;
+    int64_t* bnd = dalloc<int64_t>(static_cast<size_t>(n_cw) * (W + 1));
+    k_cw_bounds<<<grid_for(static_cast<uint64_t>(n_cw) * (W + 1)), kT, 0, st>>>(rowptr, col, row0, n_cw, lo, S, W, bnd);
+    uint32_t* P = dalloc<uint32_t>(n_hub + 1);
+    uint32_t* base = dalloc<uint32_t>(n_hub + 1);
+    k_cw_pieces<<<grid_for(n_hub + 1), kT, 0, st>>>(rowptr, row0, n_hub, n_cw, bnd, W, piece, P);
+    DevTemp tmp;
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, P, base, n_hub + 1, st);
+    tmp.ensure(bytes);
+    CPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, P, base, n_hub + 1, st));
+    uint32_t total = 0;
+    CPG_CUDA(cudaMemcpyAsync(&total, base + n_hub, sizeof(total), cudaMemcpyDeviceToHost, st));
+    CPG_CUDA(cudaStreamSynchronize(st));
+    WorkItem* unsorted = dalloc<WorkItem>(total);
+    uint64_t* keys = dalloc<uint64_t>(total);
+    uint64_t* keys_out = dalloc<uint64_t>(total);
+    uint32_t* iota = dalloc<uint32_t>(total);
+    uint32_t* perm = dalloc<uint32_t>(total);
+    t->meta = dalloc<uint2>(n_hub);
+    k_cw_items<<<grid_for(static_cast<uint64_t>(n_hub) * 32), kT, 0, st>>>(rowptr, row0, P, base, n_hub, n_cw, bnd, W,
+                                                                            piece, slot_off, spread, unsorted, keys,
+                                                                            t->meta);
+    k_iota<<<grid_for(total), kT, 0, st>>>(iota, total);
+    bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_out, iota, perm, total, 0, 40, st);
+    tmp.ensure(bytes);
+    CPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys, keys_out, iota, perm, total, 0, 40, st));
+    t->items = dalloc<WorkItem>(total);
+    k_permute_items<<<grid_for(total), kT, 0, st>>>(unsorted, perm, total, t->items);
+    CPG_CUDA(cudaStreamSynchronize(st));
+    for (void* q : {(void*)bnd, (void*)P, (void*)base, (void*)unsorted, (void*)keys, (void*)keys_out, (void*)iota,
+                    (void*)perm})
+        cudaFree(q);
+    t->n_hubs = n_hub;
+    t->n_hub_items = total;
+    if (std::getenv("CPG_CW_DEBUG"))
+        std::fprintf(stderr, "[cpg] column-window pieces: rows [%u, %u): %u hubs, %u cut (degree > %lld), %u windows x %u rows "
+                     "from row %u, %u pieces\n", row0, row1, n_hub, n_cw, static_cast<long long>(cw_deg), W, S, lo, total);
+    return true;
 }
 
 } // namespace
@@ -399,6 +556,33 @@ void dfree_aligned(void* p) {
     cudaFree(base);
 }
 
+namespace {
+struct CwParams {
+    int64_t deg = 0;
+    uint32_t lo = 0, S = 0, W = 0;
+    int spread = 1;
+};
+uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* e = std::getenv(name);
+    return e ? static_cast<uint64_t>(std::atoll(e)) : dflt;
+}
+CwParams cw_params(const cpg_graph* g, int B, bool split) {
+    CwParams p;
+    p.deg = static_cast<int64_t>(env_u64("CPG_CW_DEG", 2048));
+    if (!split || p.deg <= 0 || g->comm || g->p2p || (B != 16 && B != 64)) return p;
+    const uint64_t row_bytes = 8ull * static_cast<uint64_t>(B);
+    const uint64_t lo = (env_u64("CPG_HOT_MB", 64) << 20) / row_bytes;
+    const uint64_t S = std::max<uint64_t>(1024, (env_u64("CPG_CW_MB", 48) << 20) / row_bytes);
+    const uint64_t end = std::min<uint64_t>(g->n_pad, (env_u64("CPG_CW_WARM_MB", 1024) << 20) / row_bytes);
+    if (end <= lo + S / 2) return p;  // no warm tier: the iterate is (almost) inside the hot prefix
+    p.lo = static_cast<uint32_t>(lo);
+    p.S = static_cast<uint32_t>(S);
+    p.W = static_cast<uint32_t>(std::min<uint64_t>(64, (end - lo + S - 1) / S));
+    p.spread = static_cast<int>(env_u64("CPG_CW_SPREAD", 0));
+    return p;
+}
+}  // namespace
+
 const BatchTables& ensure_batch_tables(cpg_graph* g, int B) {
     const bool split = batch_split(g->nnz_loc);  // piece length depends on the kernel that runs them
     const int key = B * 2 + (split ? 1 : 0);
@@ -411,10 +595,23 @@ const BatchTables& ensure_batch_tables(cpg_graph* g, int B) {
     const int64_t hb = split ? batch_piece_edges(B) : batch_hub_edges(B);
     cudaStream_t st = nullptr;
     CPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // Column-window pieces (split path, one GPU, B = 16 or 64).  Measured
+    // defaults (profiles/r02/cw/): rows above 2048 edges are cut, 48 MB windows, warm tier
+    // up to 1 GB of the iterate.  CPG_CW_DEG = min degree of the rows cut (0 = off),
+    // CPG_CW_MB = window, CPG_CW_WARM_MB = end of the warm tier, CPG_CW_SPREAD = 1 spreads
+    // the uncut pieces over the windows (slower), 2 orders a window's pieces longest first.
+    const CwParams cw = cw_params(g, B, split);
     for (uint32_t c = 0; c < C; ++c) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
+        if (cw.W && build_cw_hub_items(g->rowptr, g->col, t.row_begin, t.row_end, hb, cw.deg, cw.lo, cw.S, cw.W,
+                                       cw.spread, slots, &t, st)) {
+            t.n_items = t.n_hub_items;
+            slots += t.n_hub_items;
+            bt.tables.push_back(t);
+            continue;
+        }
         build_hub_items(g->rowptr, t.row_begin, t.row_end, hb, hb, slots, &t.items, &t.n_hubs, &t.n_hub_items, 0, st);
         t.n_items = t.n_hub_items;
         slots += t.n_hub_items;

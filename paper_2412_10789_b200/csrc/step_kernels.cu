@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_graph.cuh"
 
@@ -35,6 +36,11 @@ namespace cpg {
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -125,6 +131,28 @@ __device__ __forceinline__ double2 ld_gather2_hot(const double* p, bool hot, uin
     asm volatile("ld.global.nc" CPG_GL1 ".L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                  : "=d"(v.x), "=d"(v.y)
                  : "l"(p), "l"(hot ? pol_last : pol_first));
+    return v;
+}
+
+// One warp-uniform policy for the whole gathered iterate: addresses in the hot prefix
+// [base, base + hot_bytes) are loaded evict_last, the rest of the window (up to 4 GB - 1:
+// the sizes are 32-bit) evict_first.  A per-row choice between two policies costs ~9
+// instructions per gather (compare, two selects, two moves to uniform registers, two
+// predicated loads); this costs none.
+__device__ __forceinline__ uint64_t policy_range_hot(const double* base, uint64_t hot_bytes, uint64_t total_bytes) {
+    uint64_t p;
+    const uint32_t prim = static_cast<uint32_t>(hot_bytes < 0xffffffffull ? hot_bytes : 0xffffffffull);
+    const uint32_t tot = static_cast<uint32_t>(total_bytes < 0xffffffffull ? total_bytes : 0xffffffffull);
+    asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(base), "r"(prim), "r"(tot));
+    return p;
+}
+__device__ __forceinline__ double2 ld_gather2_pol(const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc" CPG_GL1 ".L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
     return v;
 }
 
@@ -1031,12 +1059,16 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_kernel(const 
 // in cheby_batch_kernel first).  Without the hub path the kernel fits more
 // warps, and the next row's range and first index chunk are prefetched while
 // the current row's gathers and epilogue are in flight.
-template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false>
+template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false, bool RP = false>
 __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;     // lanes per row slot
     constexpr int RPW = 32 / L;  // row slots per warp
     constexpr int V = 32 / L;    // indices per lane per 32-edge chunk
     const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    // RP instances: one range policy over the iterate instead of a policy choice per row
+    const uint64_t pol_range = RP ? policy_range_hot(a.w_cur, static_cast<uint64_t>(a.hot_rows) * B * 8,
+                                                     static_cast<uint64_t>(a.n_pad_rows) * B * 8)
+                                  : pol_first;
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1100,10 +1132,15 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
                         const int t = t0 + q;
                         const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
                         CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
-                        val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                      u < a.hot_rows, pol_last, pol_first)
-                                                     : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                       : make_double2(0.0, 0.0);
+                        if constexpr (RP) {
+                            val[q] = t < m ? ld_gather2_pol(a.w_cur + static_cast<size_t>(u) * B + 2 * cl, pol_range)
+                                           : make_double2(0.0, 0.0);
+                        } else {
+                            val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
+                                                                          u < a.hot_rows, pol_last, pol_first)
+                                                         : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
+                                           : make_double2(0.0, 0.0);
+                        }
                     }
                 }
 #pragma unroll
@@ -1128,13 +1165,24 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_rows_kernel(c
 // piece's item and first index chunk are prefetched while the current piece's
 // gathers are in flight (as in cheby_batch_rows_kernel); pieces are combined
 // by the ordered last-arriver reduction.
-template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false>
+// CW instances (column-window piece tables): the pieces are claimed in list
+// order from a.job_ctr (RPW per warp per claim, the next claim made while the current
+// pieces run), so the pieces in flight are consecutive in the window-major list; an item
+// carries its own partial slot and a.hub_meta the row's first slot and piece count; the
+// gathers of a warm-window piece are loaded with the normal L2 priority (they are re-read
+// by the other rows' pieces of the same window, then age out when the sweep moves on).
+template <int B, int U = 8, int MINB = 4, bool PEER = false, bool MASK = false, bool CW = false, bool RP = false>
 __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel(const BatchArgs a, const PeerArgs pa) {
     constexpr int L = B / 2;
     constexpr int RPW = 32 / L;
     constexpr int V = 32 / L;
     constexpr int HB = batch_piece_edges(B);
     const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    const uint64_t pol_normal = CW ? policy_evict_normal() : pol_first;
+    // RP instances: one range policy over the iterate instead of a policy choice per row
+    const uint64_t pol_range = RP ? policy_range_hot(a.w_cur, static_cast<uint64_t>(a.hot_rows) * B * 8,
+                                                     static_cast<uint64_t>(a.n_pad_rows) * B * 8)
+                                  : pol_first;
     const int lane = threadIdx.x & 31;
     const int slot = lane / L, cl = lane % L;
     const unsigned smask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (slot * L));
@@ -1142,8 +1190,9 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_jobs = a.n_hub_items;
     const uint32_t stride = nw * RPW;
-    uint32_t job = wg * RPW + slot;
-    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& sb, int64_t& e0, int64_t& e1) {
+    uint32_t job = CW ? claim_jobs(a.job_ctr, lane, RPW) + slot : wg * RPW + slot;
+    bool warm = false, nwarm = false;
+    auto load_item = [&](uint32_t jb, uint32_t& r, uint32_t& sb, int64_t& e0, int64_t& e1, bool& wm) {
         if (jb < n_jobs) {
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + jb);
             const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
@@ -1151,9 +1200,11 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             sb = raw.y;
             e0 = code_e0(c);
             e1 = e0 + code_cnt(c);
+            wm = CW && (c & kWarmBit) != 0;
         } else {
             r = sb = 0;
             e0 = e1 = 0;
+            wm = false;
         }
     };
     uint32_t c[V], cn[V];
@@ -1167,7 +1218,7 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     };
     uint32_t r, sb;
     int64_t e0, e1;
-    load_item(job, r, sb, e0, e1);
+    load_item(job, r, sb, e0, e1, warm);
     load_chunk(c, e0, e1);
     constexpr int MM = mass_mode<0>();
     double2 msum;
@@ -1175,52 +1226,82 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
     while (__any_sync(0xffffffffu, job < n_jobs)) {
         uint32_t nr, nsb;
         int64_t ne0, ne1;
-        load_item(job + stride, nr, nsb, ne0, ne1);  // in flight during this piece
+        const uint32_t njob = CW ? claim_jobs(a.job_ctr, lane, RPW) + slot : job + stride;
+        load_item(njob, nr, nsb, ne0, ne1, nwarm);  // in flight during this piece
         int64_t rs = 0, re = 0;
+        uint2 meta = make_uint2(0u, 0u);
         if (job < n_jobs) {
             rs = a.rowptr[r];
             re = a.rowptr[r + 1];
+            if (CW) meta = __ldg(a.hub_meta + (r - a.meta_row0));
         }
+        const uint64_t pol_cold = warm ? pol_normal : pol_first;
         double2 s = {0.0, 0.0};
-        for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
-            const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
-            if (e != e0) {
+        // GM = 0: a policy per gathered row (hot prefix evict_last, the rest pol_cold);
+        // 1: plain loads (normal L2 priority: a warp whose pieces are all warm-window pieces);
+        // 2: one range policy over the iterate (RP instances).
+        auto sweep = [&](auto mode) {
+            constexpr int GM = decltype(mode)::value;
+            for (int64_t e = e0; __any_sync(0xffffffffu, e < e1); e += 32) {
+                const int m = static_cast<int>(e < e1 ? (e1 - e < 32 ? e1 - e : 32) : 0);
+                if (e != e0) {
 #pragma unroll
-                for (int v = 0; v < V; ++v) c[v] = cn[v];
-            }
-            if (__any_sync(0xffffffffu, e + 32 < e1)) load_chunk(cn, e + 32, e1);
+                    for (int v = 0; v < V; ++v) c[v] = cn[v];
+                }
+                if (__any_sync(0xffffffffu, e + 32 < e1)) load_chunk(cn, e + 32, e1);
 #pragma unroll
-            for (int t0 = 0; t0 < 32; t0 += U) {
-                if (!__any_sync(0xffffffffu, t0 < m)) break;
-                double2 val[U];
-                if constexpr (MASK) {
-                    gather_rows_masked<B, U>(a, c, t0, m, slot, cl, val, pol_last, pol_first);
-                } else {
+                for (int t0 = 0; t0 < 32; t0 += U) {
+                    if (!__any_sync(0xffffffffu, t0 < m)) break;
+                    double2 val[U];
+                    if constexpr (MASK) {
+                        gather_rows_masked<B, U>(a, c, t0, m, slot, cl, val, pol_last, pol_cold);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < U; ++q) {
+                            const int t = t0 + q;
+                            const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
+                            CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
+                            const double* src = a.w_cur + static_cast<size_t>(u) * B + 2 * cl;
+                            if constexpr (GM == 1) {
+                                val[q] = t < m ? __ldg(reinterpret_cast<const double2*>(src)) : make_double2(0.0, 0.0);
+                            } else if constexpr (GM == 2) {
+                                val[q] = t < m ? ld_gather2_pol(src, pol_range) : make_double2(0.0, 0.0);
+                            } else {
+                                val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(src, u < a.hot_rows, pol_last, pol_cold)
+                                                             : ld_gather2(src))
+                                               : make_double2(0.0, 0.0);
+                            }
+                        }
+                    }
 #pragma unroll
                     for (int q = 0; q < U; ++q) {
-                        const int t = t0 + q;
-                        const uint32_t u = __shfl_sync(0xffffffffu, c[t / L], slot * L + (t % L));
-                        CPG_CHECK(t >= m || u < a.chk_npad, "batch gather", u, a.chk_npad);
-                        val[q] = t < m ? (a.hot_rows ? ld_gather2_hot(a.w_cur + static_cast<size_t>(u) * B + 2 * cl,
-                                                                      u < a.hot_rows, pol_last, pol_first)
-                                                     : ld_gather2(a.w_cur + static_cast<size_t>(u) * B + 2 * cl))
-                                       : make_double2(0.0, 0.0);
+                        s.x += val[q].x;
+                        s.y += val[q].y;
                     }
                 }
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    s.x += val[q].x;
-                    s.y += val[q].y;
-                }
             }
+        };
+        if constexpr (CW) {
+            if (__all_sync(0xffffffffu, warm || job >= n_jobs))
+                sweep(std::integral_constant<int, 1>{});
+            else
+                sweep(std::integral_constant<int, RP ? 2 : 0>{});
+        } else {
+            sweep(std::integral_constant<int, 0>{});
         }
         load_chunk(c, ne0, ne1);  // next piece's first chunk
         const bool live = job < n_jobs;
         const int64_t d = re - rs;
-        const uint32_t P = live ? static_cast<uint32_t>((d + HB - 1) / HB) : 0u;
-        const uint32_t piece = live ? static_cast<uint32_t>((e0 - rs) / HB) : 0u;
+        const uint32_t P = live ? (CW ? meta.y : static_cast<uint32_t>((d + HB - 1) / HB)) : 0u;
+        const uint32_t piece = live && !CW ? static_cast<uint32_t>((e0 - rs) / HB) : 0u;  // CW: sb is the piece's own slot
+        if (CW) {
+            const uint32_t own = sb;
+            sb = meta.x;
+            CPG_CHECK(!live || (own >= sb && own - sb < P), "column-window piece slot", own, sb);
+            if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(own) * B)[cl] = s;
+        }
         CPG_CHECK(!live || sb + piece < a.chk_parts, "piece hub slot", sb + piece, a.chk_parts);
-        if (live) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[cl] = s;
+        if (live && !CW) reinterpret_cast<double2*>(a.hub_partial + static_cast<size_t>(sb + piece) * B)[cl] = s;
         __threadfence();
         __syncwarp();
         unsigned prev = 0;
@@ -1235,11 +1316,12 @@ __global__ void __launch_bounds__(kBatchThreads, MINB) cheby_batch_pieces_kernel
             batch_epilogue<B, PEER, MM, MASK>(a, pa, r, y, d, cl, wp, ac, msum);
         }
         (void)smask;
-        job += stride;
+        job = njob;
         r = nr;
         sb = nsb;
         e0 = ne0;
         e1 = ne1;
+        warm = nwarm;
     }
     if (PEER) __threadfence_system();  // peer stores performed before the iteration barrier
     batch_mass_flush<B, MM>(a, msum);
@@ -1361,12 +1443,19 @@ __global__ void __launch_bounds__(kBatchThreads, 4) cheby_sparse_scan_kernel(con
     for (uint32_t job = wg; job < n_jobs; job += nw) {
         if (job < a.n_hub_items) {  // one hub piece: [e0, e1) of row r
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.hub_items) + job);
-            const uint32_t r = raw.x, sb = raw.y;
+            const uint32_t r = raw.x;
             const uint64_t c = (static_cast<uint64_t>(raw.w) << 32) | raw.z;
             const int64_t e0 = code_e0(c), e1 = e0 + code_cnt(c);
             const int64_t rs = a.rowptr[r], re = a.rowptr[r + 1], d = re - rs;
-            const uint32_t P = static_cast<uint32_t>((d + x.hb - 1) / x.hb);
-            const uint32_t piece = static_cast<uint32_t>((e0 - rs) / x.hb);
+            uint32_t P = static_cast<uint32_t>((d + x.hb - 1) / x.hb);
+            uint32_t piece = static_cast<uint32_t>((e0 - rs) / x.hb);
+            uint32_t sb = raw.y;
+            if (a.hub_meta) {  // column-window table: the item holds its own slot
+                const uint2 meta = __ldg(a.hub_meta + (r - a.meta_row0));
+                P = meta.y;
+                piece = raw.y - meta.x;
+                sb = meta.x;
+            }
             double2 s = make_double2(0.0, 0.0);
             sparse_scan_edges(a, cs, x.cshift, e0, e1, lane, [&](int64_t, uint32_t v) {
                 if (lane < L) {
@@ -1948,6 +2037,26 @@ int split_cfg(const char* env, int B) {
     }
 
 int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, const PeerArgs* pa) {
+    if (a.hub_meta) {  // column-window piece table (built for B = 16 and 64, one GPU, unmasked)
+        if (pa || a.nz_in || !a.job_ctr || (B != 16 && B != 64)) return -1;  // api.cu never builds such a launch
+        static const int cw16 = split_cfg("CPG_CW_CFG", 16);
+        if (B == 16) {
+            switch (cw16) {
+            case 84: return launch_capped(cheby_batch_pieces_kernel<16, 8, 4, false, false, true>, a, grid, st);
+            case 85: return launch_capped(cheby_batch_pieces_kernel<16, 8, 5, false, false, true>, a, grid, st);
+            case 162: return launch_capped(cheby_batch_pieces_kernel<16, 16, 2, false, false, true>, a, grid, st);
+            case 163: return launch_capped(cheby_batch_pieces_kernel<16, 16, 3, false, false, true>, a, grid, st);
+            case 44: return launch_capped(cheby_batch_pieces_kernel<16, 4, 4, false, false, true>, a, grid, st);
+            case 46: return launch_capped(cheby_batch_pieces_kernel<16, 4, 6, false, false, true>, a, grid, st);
+            case 830: return launch_capped(cheby_batch_pieces_kernel<16, 8, 3, false, false, true>, a, grid, st);
+            case 841: return launch_capped(cheby_batch_pieces_kernel<16, 8, 4, false, false, true, true>, a, grid, st);
+            case 1631: return launch_capped(cheby_batch_pieces_kernel<16, 16, 3, false, false, true, true>, a, grid, st);
+            default: return launch_capped(cheby_batch_pieces_kernel<16, 8, 3, false, false, true, true>, a, grid, st);
+            }
+        }
+        if (cw16 == 830) return launch_capped(cheby_batch_pieces_kernel<64, 8, 4, false, false, true>, a, grid, st);
+        return launch_capped(cheby_batch_pieces_kernel<64, 8, 4, false, false, true, true>, a, grid, st);
+    }
     if (pa) {
         CPG_PEER_SWITCH(cheby_batch_pieces_kernel, B, grid, st, a, *pa);
         return grid;
@@ -1976,6 +2085,16 @@ int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, cons
         return grid;
     }
     if (a.nz_in) CPG_MASK_SWITCH(cheby_batch_rows_kernel, B)
+    // One range policy over the iterate instead of a policy choice per gathered row
+    // (CPG_ROWS_RP=0/1 forces): config 4 (B = 64) +2.6%, config 5 (B = 16) level, so on at B = 64.
+    static const int rows_rp = [] {
+        const char* e = std::getenv("CPG_ROWS_RP");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (a.hot_rows && B == 16 && rows_rp == 1)
+        return launch_capped(cheby_batch_rows_kernel<16, 8, 3, false, false, true>, a, grid, st);
+    if (a.hot_rows && B == 64 && rows_rp != 0)
+        return launch_capped(cheby_batch_rows_kernel<64, 8, 4, false, false, true>, a, grid, st);
     static const int cfg16 = split_cfg("CPG_ROWS_CFG", 16), cfg64 = split_cfg("CPG_ROWS_CFG", 64);
     if (B == 16) {
         const int cfg = cfg16;

@@ -179,7 +179,10 @@ int main(int argc, char** argv) {
     CK(cudaSetDevice(0));
     CK(cudaFree(0));
     CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0));
-    const size_t table_bytes = (argc > 1 ? static_cast<size_t>(std::atoll(argv[1])) : 8) << 30;
+    // argv[2] = table size in MB: the plain-cudaMalloc case only (an L2-resident table gives
+    // the gather rate of L2 hits)
+    const size_t table_bytes = argc > 2 ? static_cast<size_t>(std::atoll(argv[2])) << 20
+                                        : (argc > 1 ? static_cast<size_t>(std::atoll(argv[1])) : 8) << 30;
     CK(cudaMalloc(&g_sink, sizeof(double)));
     CK(cudaMalloc(&g_idx, (256ull << 20) * sizeof(uint32_t)));
 
@@ -198,6 +201,7 @@ int main(int argc, char** argv) {
         if (run_table("cudaMalloc", static_cast<double*>(p), table_bytes, 0)) return 1;
         CK(cudaFree(p));
     }
+    if (argc > 2) return 0;
     {  // cudaMalloc, 512 MB aligned (the library's dalloc_aligned)
         const size_t align = 512ull << 20;
         void* p = nullptr;
