@@ -260,6 +260,12 @@ int cpg_apply_walk(cpg_graph* g, const double* x, double* y);
 /* Algorithmic bytes of one single-source step for this handle. */
 double cpg_bytes_per_step(const cpg_graph* g, uint32_t tile);
 
+/* After a call made under cpg_set_profiling(1): the mean CUDA-event time of the two
+ * kernels of its split batched steps (hub-piece kernel, plain-row kernel) and how many
+ * steps were bracketed (0 when the call ran no split step).  bench.py's roofline of
+ * the dominant kernel. */
+int cpg_last_split_profile(cpg_graph* g, double* pieces_ms, double* rows_ms, uint32_t* steps);
+
 /* Steps at the head of a one-hot query on this handle that gather only the rows
  * of w_{k-1} with a nonzero entry, as the reference's scatter skips zero entries
  * (graph.cpp:262); tile <= 1 = the single-source step.  Results are bit-identical

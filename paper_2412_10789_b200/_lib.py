@@ -90,6 +90,7 @@ SIGNATURES = {
                                POINTER(cpg_stats)]),
     "cpg_bytes_per_step": (c_double, [_G, c_uint32]),
     "cpg_sparse_early_steps": (c_uint32, [_G, c_uint32, c_uint32]),
+    "cpg_last_split_profile": (c_int, [_G, POINTER(c_double), POINTER(c_double), POINTER(c_uint32)]),
     "cpg_gen_rmat": (c_int, [c_uint32, c_uint64, c_double, c_double, c_double, c_uint64, c_int,
                              POINTER(c_void_p), POINTER(c_void_p), _u32p, _u64p]),
     "cpg_gen_chunglu": (c_int, [c_uint32, c_uint64, c_double, c_double, c_uint32, c_uint64, c_int,

@@ -65,6 +65,7 @@ std::atomic<int> g_profile{0};
 // Event pairs around step-kernel launches (profiling mode only).
 struct StepProf {
     std::vector<cudaEvent_t> ev;
+    std::vector<cudaEvent_t> mid;  // split batched step: between the piece kernel and the row kernel
     void before(cudaStream_t st) { rec(st); }
     void after(cudaStream_t st) { rec(st); }
     void rec(cudaStream_t st) {
@@ -72,6 +73,33 @@ struct StepProf {
         CPG_CUDA(cudaEventCreate(&e));
         CPG_CUDA(cudaEventRecord(e, st));
         ev.push_back(e);
+    }
+    void between(cudaStream_t st) {  // pairs with the last before()
+        cudaEvent_t e;
+        CPG_CUDA(cudaEventCreate(&e));
+        CPG_CUDA(cudaEventRecord(e, st));
+        mid.resize(ev.size() / 2 + 1, nullptr);
+        mid[ev.size() / 2] = e;
+    }
+    // mean milliseconds of the two kernels of the split steps that recorded a mid event
+    uint32_t split_ms(double* first, double* second) {
+        double a = 0.0, b = 0.0;
+        uint32_t n = 0;
+        for (size_t i = 0; i < mid.size() && 2 * i + 1 < ev.size(); ++i) {
+            if (!mid[i]) continue;
+            float m0 = 0.f, m1 = 0.f;
+            cudaEventSynchronize(ev[2 * i + 1]);
+            cudaEventElapsedTime(&m0, ev[2 * i], mid[i]);
+            cudaEventElapsedTime(&m1, mid[i], ev[2 * i + 1]);
+            a += m0;
+            b += m1;
+            ++n;
+        }
+        if (n) {
+            *first = a / n;
+            *second = b / n;
+        }
+        return n;
     }
     double total_ms() {
         double t = 0.0;
@@ -96,6 +124,8 @@ struct StepProf {
             std::fprintf(stderr, "\n");
         }
         for (auto e : ev) cudaEventDestroy(e);
+        for (auto e : mid)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -659,6 +689,10 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
     uint64_t hot_mb = 64;
     if (const char* e = std::getenv("CPG_HOT_MB")) hot_mb = static_cast<uint64_t>(std::atoll(e));
     const uint32_t hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (hot_mb << 20) / (8 * cols)));
+    // the plain-row kernel's own hot prefix (CPG_ROWS_HOT_MB; default: the same)
+    uint32_t rows_hot_rows = hot_rows;
+    if (const char* e = std::getenv("CPG_ROWS_HOT_MB"))
+        rows_hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (static_cast<uint64_t>(std::atoll(e)) << 20) / (8 * cols)));
     CPG_CUDA(cudaMemsetAsync(w->w_a, 0, sizeof(double) * g->n_pad * cols, st));
     // mass partials: one [B] row per warp of every launch, packed per step (the
     // launches, and so the rows, are the same every step: `used` rows per step)
@@ -800,8 +834,10 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                     rows += W * pg;
                     ++launches;
                 }
+                if (prof && t.n_hub_items && t.row_end > b.hub_rows) prof->between(st);
                 if (t.row_end > b.hub_rows) {
                     BatchArgs r = b;
+                    r.hot_rows = rows_hot_rows;
                     r.mass_partial = mp_step + rows * B;
 #if CPG_CHECKED
                     r.chk_mass = step_rows - rows;
@@ -1066,6 +1102,10 @@ int drive(cpg_graph* g, const double* coeffs, uint32_t K, const uint32_t* source
         if (stats && prof) {
             stats->step_ms = prof->total_ms();
             stats->step_launches = static_cast<uint32_t>(prof->ev.size() / 2);
+        }
+        if (prof) {
+            std::lock_guard<std::mutex> lock(g->ws_mu);
+            g->split_prof_steps = prof->split_ms(&g->split_prof_pieces_ms, &g->split_prof_rows_ms);
         }
     });
 }
@@ -1638,6 +1678,17 @@ int cpg_chebypower_vec_trace(cpg_graph* g, const double* coeffs, uint32_t K, con
                              double* r_trace, double* est_trace) {
     if (!seed) return guarded([] { require(false, "null argument"); });
     return trace_impl(g, coeffs, K, 0, seed, out, r_trace, est_trace);
+}
+
+int cpg_last_split_profile(cpg_graph* g, double* pieces_ms, double* rows_ms, uint32_t* steps) {
+    return guarded([&] {
+        require(g != nullptr && pieces_ms && rows_ms && steps, "null argument");
+        cpg_graph* h = g->members.empty() ? g : g->members[0];
+        std::lock_guard<std::mutex> lock(h->ws_mu);
+        *pieces_ms = h->split_prof_pieces_ms;
+        *rows_ms = h->split_prof_rows_ms;
+        *steps = h->split_prof_steps;
+    });
 }
 
 uint32_t cpg_sparse_early_steps(const cpg_graph* g, uint32_t tile, uint32_t K) {

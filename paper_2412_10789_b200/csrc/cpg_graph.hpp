@@ -115,6 +115,9 @@ struct Workspace {
 } // namespace cpg
 
 struct cpg_graph {
+    // last profiled call (cpg_set_profiling): mean ms of the piece / row kernels of its split batched steps
+    double split_prof_pieces_ms = 0.0, split_prof_rows_ms = 0.0;
+    uint32_t split_prof_steps = 0;
     int device = 0;
     int rank = 0, nranks = 1;
     int chunks = 1;                 // row chunks per rank (one all-gather each)

@@ -275,9 +275,13 @@ __global__ void k_cw_items(const int64_t* rowptr, uint32_t row0, const uint32_t*
                 const uint32_t idx = base[j] + p0 + p;
                 items[idx] = WorkItem{row0 + j, slot_off + idx,
                                       tile_code(static_cast<uint64_t>(e0), cnt, 0) | kHubBit | (warm ? kWarmBit : 0ull)};
-                const uint32_t phase = warm ? s : ((spread & 1) ? 1 + idx % W : 0);
+                // spread & 4: the uncut pieces go to the window phases in blocks of 256 list positions, and
+                // inside a block the warm pieces come first, so a warp's RPW pieces stay of one kind while
+                // DRAM-bound and L2-bound warps run side by side in every phase
+                const uint32_t phase = warm ? s : ((spread & 4) ? 1 + (idx >> 8) % W : ((spread & 1) ? 1 + idx % W : 0));
                 // spread & 2: the pieces of a window longest first (a warp's RPW pieces run in lock-step)
-                const uint32_t sec = warm && (spread & 2) ? ((static_cast<uint32_t>(piece) - cnt) << 20) | (idx & 0xfffffu) : idx;
+                uint32_t sec = warm && (spread & 2) ? ((static_cast<uint32_t>(piece) - cnt) << 20) | (idx & 0xfffffu) : idx;
+                if (spread & 4) sec = ((idx >> 8) << 9) | (warm ? 0u : 256u) | (idx & 255u);
                 keys[idx] = (static_cast<uint64_t>(phase) << 32) | sec;
             }
             p0 += np;
@@ -297,14 +301,14 @@ __global__ void k_iota(uint32_t* v, uint32_t n) {
 // build_hub_items), the first n_cw of them (degree > cw_deg) cut at the window
 // boundaries.  Returns false (nothing allocated) when no row qualifies.
 bool build_cw_hub_items(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t row1, int64_t piece,
-                        int64_t cw_deg, uint32_t lo, uint32_t S, uint32_t W, int spread, uint32_t slot_off,
-                        ItemTable* t, cudaStream_t st) {
+                        int64_t hub_thr, int64_t cw_deg, uint32_t lo, uint32_t S, uint32_t W, int spread,
+                        uint32_t slot_off, ItemTable* t, cudaStream_t st) {
     const uint32_t n_rows = row1 - row0;
     if (!n_rows || !W) return false;
     unsigned int* d_cnt = dalloc<unsigned int>(2);
     CPG_CUDA(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned int), st));
-    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, piece, d_cnt);
-    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, std::max(cw_deg, piece), d_cnt + 1);
+    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, hub_thr, d_cnt);
+    k_count_above<<<grid_for(n_rows), kT, 0, st>>>(rowptr + row0, n_rows, std::max(cw_deg, hub_thr), d_cnt + 1);
     unsigned int cnt[2] = {0, 0};
     CPG_CUDA(cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, st));
     CPG_CUDA(cudaStreamSynchronize(st));
@@ -558,7 +562,7 @@ void dfree_aligned(void* p) {
 
 namespace {
 struct CwParams {
-    int64_t deg = 0;
+    int64_t deg = 0, hub = 1 << 30;  // rows above `hub` edges run in the piece kernel (default: the piece length)
     uint32_t lo = 0, S = 0, W = 0;
     int spread = 1;
 };
@@ -569,7 +573,8 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 CwParams cw_params(const cpg_graph* g, int B, bool split) {
     CwParams p;
     p.deg = static_cast<int64_t>(env_u64("CPG_CW_DEG", 2048));
-    if (!split || p.deg <= 0 || g->comm || g->p2p || (B != 16 && B != 64)) return p;
+    // (the fused all-gather's PEER instances keep uniform pieces)
+    if (!split || p.deg <= 0 || g->p2p || (B != 16 && B != 64)) return p;
     const uint64_t row_bytes = 8ull * static_cast<uint64_t>(B);
     const uint64_t lo = (env_u64("CPG_HOT_MB", 64) << 20) / row_bytes;
     const uint64_t S = std::max<uint64_t>(1024, (env_u64("CPG_CW_MB", 48) << 20) / row_bytes);
@@ -579,6 +584,7 @@ CwParams cw_params(const cpg_graph* g, int B, bool split) {
     p.S = static_cast<uint32_t>(S);
     p.W = static_cast<uint32_t>(std::min<uint64_t>(64, (end - lo + S - 1) / S));
     p.spread = static_cast<int>(env_u64("CPG_CW_SPREAD", 0));
+    p.hub = static_cast<int64_t>(env_u64("CPG_CW_HUB", 1 << 30));
     return p;
 }
 }  // namespace
@@ -605,8 +611,8 @@ const BatchTables& ensure_batch_tables(cpg_graph* g, int B) {
         ItemTable t;
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
-        if (cw.W && build_cw_hub_items(g->rowptr, g->col, t.row_begin, t.row_end, hb, cw.deg, cw.lo, cw.S, cw.W,
-                                       cw.spread, slots, &t, st)) {
+        if (cw.W && build_cw_hub_items(g->rowptr, g->col, t.row_begin, t.row_end, hb, std::min<int64_t>(hb, cw.hub),
+                                       cw.deg, cw.lo, cw.S, cw.W, cw.spread, slots, &t, st)) {
             t.n_items = t.n_hub_items;
             slots += t.n_hub_items;
             bt.tables.push_back(t);

@@ -70,3 +70,46 @@ def test_column_window_pieces_match_reference(cpg, gpu, hub_graph, tile, spread,
         want, _, _ = ref.cheby_power(PPR, 0.2, src[j], 26)
         assert_parity(few[j], want)
     dg.close()
+
+
+@pytest.mark.parametrize("R,C", [(2, 1), (3, 2)])
+def test_column_window_pieces_on_sharded_ranks(cpg, gpu, hub_graph, R, C, monkeypatch):
+    """A row-sharded rank cuts its own hub rows at the same (global) column windows: R ranks on one
+    GPU through the loopback data plane, every rank's gathered result against the reference."""
+    import threading
+
+    from oracle import RefGraph
+
+    off, nb = hub_graph
+    _env(monkeypatch, 512)
+    monkeypatch.setenv("CPG_CHUNKS", str(C))
+    ref = RefGraph.from_csr(off, nb)
+    deg = np.diff(off)
+    src = [int(np.argmax(deg)), 5, 77, len(off) - 2] + [int(s) for s in ref.select_sources_uniform(12, 4)]
+    grp = cpg.LoopbackGroup(R)
+    shards = [cpg.DeviceGraph.loopback(off, nb, r, grp) for r in range(R)]
+    out, errs = [None] * R, []
+
+    def work(r):
+        try:
+            out[r] = cpg.cheby_power_many(shards[r], cpg.Kernel.ppr(0.2), src, 26, batched=True, tile=16)
+        except BaseException as e:
+            errs.append((r, e))
+
+    for sparse in ("0", "1"):
+        monkeypatch.setenv("CPG_SPARSE_STEPS", sparse)
+        th = [threading.Thread(target=work, args=(r,)) for r in range(R)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        assert not errs, errs
+        for j in (0, 1, 5, len(src) - 1):
+            want, _, _ = ref.cheby_power(PPR, 0.2, src[j], 26)
+            for r in range(R):
+                assert_parity(out[r][0][j], want)
+        for r in range(R):
+            assert out[r][1].mass_err_max <= 1e-9
+            assert np.array_equal(out[r][0], out[0][0])
+    for dg in shards:
+        dg.close()

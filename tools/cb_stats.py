@@ -26,7 +26,7 @@ nnz = int(deg.sum())
 B = 16 if cfg.get("tile", 64) == 16 else 64
 hot = (64 << 20) // (8 * B)
 tiers = [(mb, (mb << 20) // (8 * B)) for mb in (128, 256, 512, 1024, 2048)]
-Ts = (1024, 2048, 4096, 8192, 16384, 32768)
+Ts = (32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768)
 res = {T: {"rows": int((deg > T).sum()), "edges": 0, "hot": 0, **{mb: 0 for mb, _ in tiers}} for T in Ts}
 nbt = torch.from_numpy(nb.view(np.int32))
 off_t = torch.from_numpy(off.astype(np.int64))
