@@ -572,7 +572,10 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 }
 CwParams cw_params(const cpg_graph* g, int B, bool split) {
     CwParams p;
-    p.deg = static_cast<int64_t>(env_u64("CPG_CW_DEG", 2048));
+    // B = 64 (512-B rows): a short window segment still moves kilobytes, so more rows pay: 768 at
+    // both thresholds (config 3 831 -> 870-880 GTEPS, config 4 1584 -> 1617); at B = 16 rows of
+    // 513-1024 edges lose 5% when cut (profiles/r02/cw/ab_column_windows.txt)
+    p.deg = static_cast<int64_t>(env_u64("CPG_CW_DEG", B == 64 ? 768 : 2048));
     // (the fused all-gather's PEER instances keep uniform pieces)
     if (!split || p.deg <= 0 || g->p2p || (B != 16 && B != 64)) return p;
     const uint64_t row_bytes = 8ull * static_cast<uint64_t>(B);
@@ -584,7 +587,7 @@ CwParams cw_params(const cpg_graph* g, int B, bool split) {
     p.S = static_cast<uint32_t>(S);
     p.W = static_cast<uint32_t>(std::min<uint64_t>(64, (end - lo + S - 1) / S));
     p.spread = static_cast<int>(env_u64("CPG_CW_SPREAD", 0));
-    p.hub = static_cast<int64_t>(env_u64("CPG_CW_HUB", 1 << 30));
+    p.hub = static_cast<int64_t>(env_u64("CPG_CW_HUB", B == 64 ? 768 : 1 << 30));
     return p;
 }
 }  // namespace
