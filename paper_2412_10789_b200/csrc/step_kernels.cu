@@ -2051,7 +2051,11 @@ int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, co
             case 830: return launch_capped(cheby_batch_pieces_kernel<16, 8, 3, false, false, true>, a, grid, st);
             case 841: return launch_capped(cheby_batch_pieces_kernel<16, 8, 4, false, false, true, true>, a, grid, st);
             case 1631: return launch_capped(cheby_batch_pieces_kernel<16, 16, 3, false, false, true, true>, a, grid, st);
-            default: return launch_capped(cheby_batch_pieces_kernel<16, 8, 3, false, false, true, true>, a, grid, st);
+            case 1031: return launch_capped(cheby_batch_pieces_kernel<16, 10, 3, false, false, true, true>, a, grid, st);
+            case 1041: return launch_capped(cheby_batch_pieces_kernel<16, 10, 4, false, false, true, true>, a, grid, st);
+            case 831: return launch_capped(cheby_batch_pieces_kernel<16, 8, 3, false, false, true, true>, a, grid, st);
+            // 12 gathers in flight per lane at 3 CTAs/SM (80 registers, no spills): 21.0 ms against 21.9 at 8
+            default: return launch_capped(cheby_batch_pieces_kernel<16, 12, 3, false, false, true, true>, a, grid, st);
             }
         }
         if (cw16 == 830) return launch_capped(cheby_batch_pieces_kernel<64, 8, 4, false, false, true>, a, grid, st);
@@ -2086,13 +2090,27 @@ int launch_batch_rows(const BatchArgs& a, int B, int grid, cudaStream_t st, cons
     }
     if (a.nz_in) CPG_MASK_SWITCH(cheby_batch_rows_kernel, B)
     // One range policy over the iterate instead of a policy choice per gathered row
-    // (CPG_ROWS_RP=0/1 forces): config 4 (B = 64) +2.6%, config 5 (B = 16) level, so on at B = 64.
+    // (CPG_ROWS_RP=0 = a policy per row): config 4 (B = 64) +2.6%; at B = 16 level at the same
+    // geometry, but it frees the registers for more gathers in flight (below).
     static const int rows_rp = [] {
         const char* e = std::getenv("CPG_ROWS_RP");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    if (a.hot_rows && B == 16 && rows_rp == 1)
-        return launch_capped(cheby_batch_rows_kernel<16, 8, 3, false, false, true>, a, grid, st);
+    // B = 16: without the per-row policy registers the range-policy instance fits 10 gathers in
+    // flight per lane at 4 CTAs/SM in 64 registers, no spills (the per-row-policy instance needs 80
+    // for 8 at 3 CTAs/SM): config 5 row kernel 31.8 -> 30.7 ms, 1131 -> 1160 GTEPS
+    // (profiles/r02/cw/ab_rows_geometry.txt; CPG_ROWS_RP_CFG = 83, 84, 123, 163 select others).
+    if (a.hot_rows && B == 16 && rows_rp != 0) {
+        static const int cfg_rp = [] {
+            const char* e = std::getenv("CPG_ROWS_RP_CFG");
+            return e ? std::atoi(e) : 104;
+        }();
+        if (cfg_rp == 84) return launch_capped(cheby_batch_rows_kernel<16, 8, 4, false, false, true>, a, grid, st);
+        if (cfg_rp == 83) return launch_capped(cheby_batch_rows_kernel<16, 8, 3, false, false, true>, a, grid, st);
+        if (cfg_rp == 123) return launch_capped(cheby_batch_rows_kernel<16, 12, 3, false, false, true>, a, grid, st);
+        if (cfg_rp == 163) return launch_capped(cheby_batch_rows_kernel<16, 16, 3, false, false, true>, a, grid, st);
+        return launch_capped(cheby_batch_rows_kernel<16, 10, 4, false, false, true>, a, grid, st);
+    }
     if (a.hot_rows && B == 64 && rows_rp != 0)
         return launch_capped(cheby_batch_rows_kernel<64, 8, 4, false, false, true>, a, grid, st);
     static const int cfg16 = split_cfg("CPG_ROWS_CFG", 16), cfg64 = split_cfg("CPG_ROWS_CFG", 64);
