@@ -689,6 +689,10 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
     uint64_t hot_mb = 64;
     if (const char* e = std::getenv("CPG_HOT_MB")) hot_mb = static_cast<uint64_t>(std::atoll(e));
     const uint32_t hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (hot_mb << 20) / (8 * cols)));
+    // the column-window piece kernel's own hot prefix (graph_build.cu cw_params: the same variable)
+    uint64_t cw_hot_mb = 32;
+    if (const char* e = std::getenv("CPG_CW_HOT_MB")) cw_hot_mb = static_cast<uint64_t>(std::atoll(e));
+    const uint32_t cw_hot_rows = static_cast<uint32_t>(std::min<uint64_t>(g->n_pad, (cw_hot_mb << 20) / (8 * cols)));
     // the plain-row kernel's own hot prefix (CPG_ROWS_HOT_MB; default: the same)
     uint32_t rows_hot_rows = hot_rows;
     if (const char* e = std::getenv("CPG_ROWS_HOT_MB"))
@@ -819,7 +823,10 @@ uint32_t run_batch(cpg_graph* g, Workspace* w, uint32_t K, uint32_t B, uint32_t 
                 if (t.n_hub_items) {
                     BatchArgs h = b;
                     h.n_loc = b.hub_rows;
-                    if (t.meta) h.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
+                    if (t.meta) {
+                        h.job_ctr = w->d_job_ctr + static_cast<size_t>(k - 1) * C + c;
+                        h.hot_rows = cw_hot_rows;
+                    }
                     h.mass_partial = mp_step + rows * B;
 #if CPG_CHECKED
                     h.chk_mass = step_rows - rows;

@@ -579,7 +579,10 @@ CwParams cw_params(const cpg_graph* g, int B, bool split) {
     // (the fused all-gather's PEER instances keep uniform pieces)
     if (!split || p.deg <= 0 || g->p2p || (B != 16 && B != 64)) return p;
     const uint64_t row_bytes = 8ull * static_cast<uint64_t>(B);
-    const uint64_t lo = (env_u64("CPG_HOT_MB", 64) << 20) / row_bytes;
+    // The piece kernel's own hot prefix: with the windows serving the warm tier it wants most of the
+    // L2 for the window, so 32 MB (not the 64 MB of the other kernels): config 5 piece kernel 20.0 ->
+    // 17.9 ms (8-32 MB level; profiles/r02/cw/ab_hot_window.txt).  api.cu passes the same rows.
+    const uint64_t lo = (env_u64("CPG_CW_HOT_MB", 32) << 20) / row_bytes;
     const uint64_t S = std::max<uint64_t>(1024, (env_u64("CPG_CW_MB", 48) << 20) / row_bytes);
     const uint64_t end = std::min<uint64_t>(g->n_pad, (env_u64("CPG_CW_WARM_MB", 1024) << 20) / row_bytes);
     if (end <= lo + S / 2) return p;  // no warm tier: the iterate is (almost) inside the hot prefix

@@ -25,6 +25,7 @@ def hub_graph(cpg):
 def _env(monkeypatch, deg, spread="1"):
     monkeypatch.setenv("CPG_BATCH_SPLIT", "1")   # the piece + row kernels on a small graph
     monkeypatch.setenv("CPG_HOT_MB", "1")        # hot prefix: 8192 rows at B = 16, 2048 at B = 64
+    monkeypatch.setenv("CPG_CW_HOT_MB", "1")     # the piece kernel's own (the first window starts there)
     monkeypatch.setenv("CPG_CW_MB", "1")
     monkeypatch.setenv("CPG_CW_WARM_MB", "3")
     monkeypatch.setenv("CPG_CW_SPREAD", spread)
