@@ -18,7 +18,11 @@ roofline: the step kernel(s), one launch = one step of one source tile (or query
          group); achieved = min(algorithmic bytes per launch (12*nnz +
          8*(n+1) + 32*n single-source, nnz*(4+8B) + 8*(n+1) + 32*n*B batched), the
          ncu-measured DRAM bytes of that launch) / mean CUDA-event launch duration
-         measured here; frac_model keeps the model-only fraction.
+         measured here; frac_model keeps the model-only fraction.  Where the batched step is
+         two kernels (hub-piece kernel + plain-row kernel, graphs of >= 8 M edges) the line is the
+         DOMINANT kernel's: its own ncu DRAM bytes over its own live CUDA-event time
+         (cpg_last_split_profile); `kernels` holds both, `step` the step-level numbers.  The
+         timed call runs with the sparse early steps off, so every launch is a full step.
 cpu_baseline: the reference's own cheby_power (oracle/_ref, compiled from
          /root/reference sources) on all host cores (bounded sample; whole queries
          where they fit, else the SpMV of a query, extrapolated), plus one-thread
