@@ -2059,6 +2059,14 @@ int launch_batch_pieces(const BatchArgs& a, int B, int grid, cudaStream_t st, co
             }
         }
         if (cw16 == 830) return launch_capped(cheby_batch_pieces_kernel<64, 8, 4, false, false, true>, a, grid, st);
+        static const int cw64 = [] {  // A/B: geometry of the B = 64 range-policy instance
+            const char* e = std::getenv("CPG_CW_CFG64");
+            return e ? std::atoi(e) : 84;
+        }();
+        if (cw64 == 124) return launch_capped(cheby_batch_pieces_kernel<64, 12, 4, false, false, true, true>, a, grid, st);
+        if (cw64 == 123) return launch_capped(cheby_batch_pieces_kernel<64, 12, 3, false, false, true, true>, a, grid, st);
+        if (cw64 == 163) return launch_capped(cheby_batch_pieces_kernel<64, 16, 3, false, false, true, true>, a, grid, st);
+        if (cw64 == 85) return launch_capped(cheby_batch_pieces_kernel<64, 8, 5, false, false, true, true>, a, grid, st);
         return launch_capped(cheby_batch_pieces_kernel<64, 8, 4, false, false, true, true>, a, grid, st);
     }
     if (pa) {
