@@ -302,7 +302,7 @@ __global__ void k_iota(uint32_t* v, uint32_t n) {
 // boundaries.  Returns false (nothing allocated) when no row qualifies.
 bool build_cw_hub_items(const int64_t* rowptr, const uint32_t* col, uint32_t row0, uint32_t row1, int64_t piece,
                         int64_t hub_thr, int64_t cw_deg, uint32_t lo, uint32_t S, uint32_t W, int spread,
-                        uint32_t slot_off, ItemTable* t, cudaStream_t st) {
+                        uint32_t min_cut, uint32_t slot_off, ItemTable* t, cudaStream_t st) {
     const uint32_t n_rows = row1 - row0;
     if (!n_rows || !W) return false;
     unsigned int* d_cnt = dalloc<unsigned int>(2);
@@ -314,7 +314,10 @@ bool build_cw_hub_items(const int64_t* rowptr, const uint32_t* col, uint32_t row
     CPG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_cnt);
     const uint32_t n_hub = cnt[0], n_cw = cnt[1];
-    if (!n_cw) return false;
+    // Each window phase holds about one piece per cut row.  The pieces in flight (claimed in list
+    // order) must be a small part of a phase, or several windows are swept at once and none stays
+    // resident: below min_cut rows the table keeps uniform pieces (a sharded rank's chunk tables).
+    if (!n_cw || n_cw < min_cut) return false;
     int64_t* bnd = dalloc<int64_t>(static_cast<size_t>(n_cw) * (W + 1));
     k_cw_bounds<<<grid_for(static_cast<uint64_t>(n_cw) * (W + 1)), kT, 0, st>>>(rowptr, col, row0, n_cw, lo, S, W, bnd);
     uint32_t* P = dalloc<uint32_t>(n_hub + 1);
@@ -565,6 +568,7 @@ struct CwParams {
     int64_t deg = 0, hub = 1 << 30;  // rows above `hub` edges run in the piece kernel (default: the piece length)
     uint32_t lo = 0, S = 0, W = 0;
     int spread = 1;
+    uint32_t min_cut = 0;
 };
 uint64_t env_u64(const char* name, uint64_t dflt) {
     const char* e = std::getenv(name);
@@ -591,6 +595,11 @@ CwParams cw_params(const cpg_graph* g, int B, bool split) {
     p.W = static_cast<uint32_t>(std::min<uint64_t>(64, (end - lo + S - 1) / S));
     p.spread = static_cast<int>(env_u64("CPG_CW_SPREAD", 0));
     p.hub = static_cast<int64_t>(env_u64("CPG_CW_HUB", B == 64 ? 768 : 1 << 30));
+    // B = 16: 4 pieces per warp, 3 CTAs of 8 warps per SM in flight; twice that many cut rows at least
+    // (one rank: 397 K rows; 4 chunks of one rank, 99 K: level with uniform pieces; 8 ranks x 4 chunks,
+    // 12 K: fewer pieces per phase than are in flight).  B = 64 keeps its windows at any size: there
+    // the gain is as much the lower hub threshold and the range policy (config 3: 3-6 K cut rows, +5%).
+    p.min_cut = static_cast<uint32_t>(env_u64("CPG_CW_MIN_ROWS", B == 16 ? 2ull * g->sm_count * 3 * 8 * 4 : 0));
     return p;
 }
 }  // namespace
@@ -618,7 +627,7 @@ const BatchTables& ensure_batch_tables(cpg_graph* g, int B) {
         t.row_begin = c * g->cr;
         t.row_end = (c + 1) * g->cr;
         if (cw.W && build_cw_hub_items(g->rowptr, g->col, t.row_begin, t.row_end, hb, std::min<int64_t>(hb, cw.hub),
-                                       cw.deg, cw.lo, cw.S, cw.W, cw.spread, slots, &t, st)) {
+                                       cw.deg, cw.lo, cw.S, cw.W, cw.spread, cw.min_cut, slots, &t, st)) {
             t.n_items = t.n_hub_items;
             slots += t.n_hub_items;
             bt.tables.push_back(t);

@@ -30,6 +30,7 @@ def _env(monkeypatch, deg, spread="1"):
     monkeypatch.setenv("CPG_CW_WARM_MB", "3")
     monkeypatch.setenv("CPG_CW_SPREAD", spread)
     monkeypatch.setenv("CPG_CW_DEG", str(deg))  # 0 = uniform pieces
+    monkeypatch.setenv("CPG_CW_MIN_ROWS", "1")  # the test graph has a few dozen hub rows
 
 
 @pytest.mark.parametrize("tile", [16, 64])
